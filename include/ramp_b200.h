@@ -1,0 +1,125 @@
+/*
+ * ramp_b200.h -- C ABI of the B200-native RaMP fused-MoE hot path.
+ *
+ * The reference (arxiv 2604.26039, /root/reference/pkg/src/ramp) is a Python
+ * package with no FFI; its hot path is the online selector
+ *   select_config(table, hist, cache, step_id)      ramp/dispatch.py:89-122
+ *   pool_grids(pool, hist)                          ramp/routing.py:206-216
+ *   predict_batch(a, b, c, d, g, sm_count)          ramp/cost_model.py:104-114
+ * plus the fused kernel it only simulates (simulate_pool_times,
+ * ramp/oracle.py:197-254; kernel semantics PAPER.md:155-169, :719-754).
+ * Each entry point below replaces one of those; the Python mirror in
+ * paper_2604_26039_b200/ binds them with ctypes.
+ *
+ * Conventions
+ *   - every pointer argument is DEVICE memory unless the name ends in _host;
+ *     buffers are owned by the caller (torch allocates them);
+ *   - every call is stream-ordered on `stream` (a cudaStream_t, 0 = legacy
+ *     default stream) and never synchronises the host;
+ *   - return value: 0 on success, a RAMP_E* code otherwise; ramp_last_error()
+ *     returns a thread-local message for the last failure on this thread.
+ */
+#ifndef RAMP_B200_H
+#define RAMP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RAMP_OK 0
+#define RAMP_EINVAL 1  /* bad shape / argument  (reference raises ValueError)   */
+#define RAMP_ECUDA 2   /* CUDA runtime / driver failure                           */
+#define RAMP_ENOSYS 3  /* not built for this configuration (e.g. no sm_100a GPU)  */
+
+/* Dispatch table: the pool's per-config integer fields plus the four fitted
+ * floats per config (ramp/dispatch.py:57-86, "4 floats per config",
+ * PAPER.md:701-703).  All arrays are device arrays of length n_cfg, except
+ * ubm (n_ubm distinct bm values, ascending) and ubm_index (n_cfg entries into
+ * ubm), which let the device share the ceil-divs per distinct bm exactly like
+ * pool_grids' np.unique (ramp/routing.py:212-214). */
+typedef struct ramp_table {
+  int32_t n_cfg;
+  int32_t n_ubm;
+  int32_t N;        /* geometry N (= 2 * d_ff for the up/gate GEMM)            */
+  int32_t kappa_ok; /* region_variables(geom).kappa >= 48 (ramp/dispatch.py:86) */
+  int32_t sm_count; /* DispatchTable.sm_count                                   */
+  int32_t reserved[3];
+  const int32_t* bm;
+  const int32_t* ttn;
+  const int32_t* stg;
+  const int32_t* split_k;
+  const int32_t* group_m;
+  const int32_t* ubm;
+  const int32_t* ubm_index;
+  const double* a;
+  const double* b;
+  const double* c;
+  const double* d;
+} ramp_table_t;
+
+/* Library version (major*10000 + minor*100 + patch) and sm_100a build flag. */
+int ramp_version(void);
+/* Thread-local message for the last non-zero return on this thread. */
+const char* ramp_last_error(void);
+/* 1 if a device of compute capability 10.0 is visible and the kernels can run. */
+int ramp_device_ok(void);
+
+/* Expert histogram + moe_align_block_size (north_star (1); SURVEY 8a rows a1,
+ * a19).  Stable counting sort of the flattened topk_ids by expert, each
+ * expert padded to a multiple of bm.
+ *   hist[E]            bincount(topk_ids, minlength=E)
+ *   sorted_ids[cap]    flat assignment indices grouped by expert, ascending
+ *                      within an expert, padding = n_assign; cap must be
+ *                      >= ramp_align_capacity(n_assign, E, bm)
+ *   tile_expert[cap/bm] expert of each bm-row M-tile
+ *   n_post_pad[1]      total padded length (sum_e ceil(c_e/bm)*bm)
+ * Replaces: the M-tile count inside grid_size / m_tile_counts
+ * (ramp/routing.py:191-203) and the routing bincount of PAPER.md:761-762. */
+int ramp_moe_align(const int32_t* topk_ids, int64_t n_assign, int32_t E, int32_t bm,
+                   int32_t* hist, int32_t* sorted_ids, int32_t* tile_expert, int32_t* n_post_pad,
+                   void* stream);
+int64_t ramp_align_capacity(int64_t n_assign, int32_t E, int32_t bm);
+
+/* Routing-aware dispatcher on a device histogram (north_star (3)).
+ * Evaluates T(g) = a + b*ceil(g/SM) + c*g + d*ln(g+1) in fp64 in numpy's
+ * operation order, masks split-K configs failing the gate
+ * (g/split_k)/SM < 0.2 with kappa >= 48, and writes the first argmin.
+ *   cfg_out[1]         selected config id         (select_config's return)
+ *   n_eval_out[1]      number of kept configs     (DispatchTable.evaluations increment)
+ *   grid_out[n_cfg]    optional, pool_grids       (ramp/routing.py:206-216)
+ *   pred_out[n_cfg]    optional, predict_batch    (ramp/cost_model.py:104-114), +inf if masked
+ * Replaces select_config (ramp/dispatch.py:89-122) minus the host StepCache. */
+int ramp_dispatch_select(const int32_t* hist, int32_t E, const ramp_table_t* table,
+                         int32_t* cfg_out, int32_t* n_eval_out, int64_t* grid_out, double* pred_out,
+                         void* stream);
+
+/* Fused MoE layer forward, BF16 (north_star (2)):
+ *   out[t] = sum_j topk_w[t,j] * W2[e] (silu(W1[e,:I] x_t) * (W1[e,I:] x_t)),  e = topk_ids[t,j]
+ * x[S,H] bf16, w1[E,2I,H] bf16 (gate rows first), w2[E,H,I] bf16, topk_w[S,k]
+ * fp32, topk_ids[S,k] int32, out[S,H] bf16.  One call = route kernel
+ * (histogram -> dispatcher -> align -> accumulator clear) + persistent
+ * tcgen05 megakernel + bf16 finalize; no host synchronisation.
+ *   forced_cfg < 0   select on device from the live histogram (routing-aware)
+ *   forced_cfg >= 0  run that config id (static dispatch / exhaustive sweep)
+ *   sel_out          optional device int32[4]: {cfg, n_post_pad, n_work, n_eval}
+ * workspace: >= ramp_fused_moe_workspace_size(...) bytes of device memory.
+ * Replaces the kernel that simulate_pool_times stands in for
+ * (ramp/oracle.py:197-254) together with the select_config call before it. */
+size_t ramp_fused_moe_workspace_size(int32_t S, int32_t H, int32_t E, int32_t top_k);
+int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const float* topk_w,
+                        const int32_t* topk_ids, int32_t S, int32_t H, int32_t I, int32_t E,
+                        int32_t top_k, const ramp_table_t* table, int32_t forced_cfg, void* out,
+                        int32_t* sel_out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Shared-memory bytes the megakernel needs for (bm, ttn, stg); 0 if the
+ * configuration is not realisable on this part (pool admissibility test,
+ * the B200 counterpart of smem_usage/is_valid, ramp/config_space.py:122-138). */
+int64_t ramp_config_smem_bytes(int32_t bm, int32_t ttn, int32_t stg);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RAMP_B200_H */

@@ -1,0 +1,80 @@
+"""fp32 CPU oracle of the fused MoE layer and of moe_align_block_size.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  PARITY UNPINNED BY THE
+REFERENCE: /root/reference has no fused-MoE forward and no alignment code
+(SURVEY.md 0.2); the semantics follow the paper's three-phase description
+(up-projection, SwiGLU, down-projection + scatter via
+atomic add) with vLLM's weight layout (w1 = [E, 2I, H] with
+the gate half first, w2 = [E, H, I]).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def silu(x: np.ndarray) -> np.ndarray:
+    return x / (1.0 + np.exp(-x))
+
+
+def fused_moe_ref(x: np.ndarray, w1: np.ndarray, w2: np.ndarray, topk_w: np.ndarray,
+                  topk_ids: np.ndarray, act_dtype=None) -> np.ndarray:
+    """out[t] = sum_j w[t,j] * W2[e] (silu(W1g[e] x_t) * W1u[e] x_t), e = ids[t,j].
+
+    All math in fp32.  `act_dtype` optionally rounds the SwiGLU activation
+    (e.g. to bf16 via a callable) to model the kernel's on-chip precision;
+    the default keeps it fp32 (the reference-precision oracle).
+    """
+    x = np.asarray(x, dtype=np.float32)
+    S, H = x.shape
+    E, two_i, _ = w1.shape
+    I = two_i // 2
+    k = topk_ids.shape[1]
+    out = np.zeros((S, H), dtype=np.float32)
+    flat_ids = np.asarray(topk_ids).reshape(-1)
+    flat_w = np.asarray(topk_w, dtype=np.float32).reshape(-1)
+    tok = np.repeat(np.arange(S), k)
+    for e in np.unique(flat_ids):
+        sel = np.nonzero(flat_ids == e)[0]
+        xe = x[tok[sel]]                                   # gather  [n, H]
+        h = xe @ np.asarray(w1[e], dtype=np.float32).T     # phase 1 [n, 2I]
+        a = silu(h[:, :I]) * h[:, I:]                      # phase 2 [n, I]
+        if act_dtype is not None:
+            a = act_dtype(a)
+        y = a @ np.asarray(w2[e], dtype=np.float32).T      # phase 3 [n, H]
+        np.add.at(out, tok[sel], y * flat_w[sel, None])    # weighted scatter-reduce
+    return out
+
+
+def moe_align_ref(topk_ids: np.ndarray, E: int, bm: int):
+    """Histogram + stable alignment (the contract of ramp_moe_align).
+
+    Returns (hist[E], sorted_ids[n_post_pad], tile_expert[n_post_pad/bm], n_post_pad):
+    flat assignment indices grouped by expert in ascending order, each
+    expert's run padded with the sentinel n = topk_ids.size up to a multiple
+    of bm; tile_expert[t] is the expert owning rows [t*bm, (t+1)*bm).
+    The M-tile count n_post_pad/bm equals m_tile_counts (ramp/routing.py:197-203).
+    """
+    flat = np.asarray(topk_ids, dtype=np.int64).reshape(-1)
+    n = flat.size
+    if n and (flat.min() < 0 or flat.max() >= E):
+        raise ValueError("expert id out of range")
+    hist = np.bincount(flat, minlength=E).astype(np.int64)
+    padded = -(-hist // bm) * bm
+    order = np.argsort(flat, kind="stable")
+    sorted_ids = np.full(int(padded.sum()), n, dtype=np.int64)
+    tile_expert = np.repeat(np.arange(E), padded // bm)
+    starts = np.concatenate(([0], np.cumsum(padded)[:-1]))
+    cstarts = np.concatenate(([0], np.cumsum(hist)[:-1]))
+    for e in range(E):
+        c = hist[e]
+        if c:
+            sorted_ids[starts[e]:starts[e] + c] = order[cstarts[e]:cstarts[e] + c]
+    return hist, sorted_ids, tile_expert, int(padded.sum())
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    """Round fp32 to the nearest bf16 (ties to even), returned as fp32."""
+    u = np.asarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32)

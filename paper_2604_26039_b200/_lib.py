@@ -1,0 +1,108 @@
+"""ctypes binding of libramp_b200.so (the C ABI in include/ramp_b200.h).
+
+There is deliberately no CPU fallback: if the library or an sm_100a device is
+missing, every call raises.  `load()` is the single place the .so is opened.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libramp_b200.so"
+
+c_i32p = ctypes.POINTER(ctypes.c_int32)
+
+# Every symbol include/ramp_b200.h declares, with (restype, argtypes).
+SIGNATURES = {
+    "ramp_version": (ctypes.c_int, []),
+    "ramp_last_error": (ctypes.c_char_p, []),
+    "ramp_device_ok": (ctypes.c_int, []),
+    "ramp_align_capacity": (ctypes.c_int64, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32]),
+    "ramp_config_smem_bytes": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
+    "ramp_moe_align": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
+         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
+    ),
+    "ramp_dispatch_select": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
+    ),
+    "ramp_fused_moe_workspace_size": (
+        ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
+    ),
+    "ramp_fused_moe_bf16": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+         ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+         ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+         ctypes.c_size_t, ctypes.c_void_p],
+    ),
+}
+
+
+class RampTable(ctypes.Structure):
+    """Mirror of `ramp_table_t`: device pointers + geometry scalars."""
+
+    _fields_ = [
+        ("n_cfg", ctypes.c_int32),
+        ("n_ubm", ctypes.c_int32),
+        ("N", ctypes.c_int32),
+        ("kappa_ok", ctypes.c_int32),
+        ("sm_count", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 3),
+        ("bm", ctypes.c_void_p),
+        ("ttn", ctypes.c_void_p),
+        ("stg", ctypes.c_void_p),
+        ("split_k", ctypes.c_void_p),
+        ("group_m", ctypes.c_void_p),
+        ("ubm", ctypes.c_void_p),
+        ("ubm_index", ctypes.c_void_p),
+        ("a", ctypes.c_void_p),
+        ("b", ctypes.c_void_p),
+        ("c", ctypes.c_void_p),
+        ("d", ctypes.c_void_p),
+    ]
+
+
+class RampError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Open libramp_b200.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        path = os.environ.get("RAMP_B200_LIB", str(LIB_PATH))
+        if not Path(path).exists():
+            raise RampError(
+                f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback)"
+            )
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = load().ramp_last_error().decode(errors="replace")
+        if rc == 1:
+            raise ValueError(msg)
+        raise RampError(f"libramp_b200 error {rc}: {msg}")
+
+
+def require_device() -> None:
+    if not load().ramp_device_ok():
+        raise RampError("libramp_b200 needs an sm_100 (B200) GPU; none is visible")

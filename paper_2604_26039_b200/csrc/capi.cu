@@ -1,0 +1,193 @@
+// extern "C" boundary of libramp_b200.so (declared in include/ramp_b200.h).
+// Argument validation mirrors the reference's ValueError checks; every entry
+// point is stream-ordered and returns a status code instead of throwing.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/ramp_b200.h"
+#include "launch.h"
+#include "route.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t err, const char* where) {
+  return fail(RAMP_ECUDA, std::string(where) + ": " + cudaGetErrorString(err));
+}
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct WorkspaceLayout {
+  size_t ctrl, hist, sorted, tiles, acc, total;
+  int64_t capacity;
+};
+
+WorkspaceLayout layout_for(int32_t S, int32_t H, int32_t E, int32_t top_k) {
+  WorkspaceLayout w{};
+  const int64_t n_assign = (int64_t)S * top_k;
+  w.capacity = ramp_align_capacity(n_assign, E, ramp::kMaxBm);
+  size_t off = 0;
+  w.ctrl = off;
+  off = align_up(off + 64, 256);
+  w.hist = off;
+  off = align_up(off + sizeof(int32_t) * E, 256);
+  w.sorted = off;
+  off = align_up(off + sizeof(int32_t) * w.capacity, 256);
+  w.tiles = off;
+  off = align_up(off + sizeof(int32_t) * w.capacity, 256);
+  w.acc = off;
+  off = align_up(off + sizeof(float) * (size_t)S * H, 256);
+  w.total = off;
+  return w;
+}
+
+int check_table(const ramp_table_t* t) {
+  if (!t) return fail(RAMP_EINVAL, "table is null");
+  if (t->n_cfg < 1) return fail(RAMP_EINVAL, "dispatch table over an empty pool");
+  if (t->n_ubm < 1 || t->n_ubm > ramp::kMaxUbm) return fail(RAMP_EINVAL, "n_ubm out of range [1, 128]");
+  if (t->sm_count < 1) return fail(RAMP_EINVAL, "sm_count must be >= 1");
+  if (t->N < 1) return fail(RAMP_EINVAL, "N must be >= 1");
+  if (!t->bm || !t->ttn || !t->split_k || !t->ubm || !t->ubm_index || !t->a || !t->b || !t->c || !t->d)
+    return fail(RAMP_EINVAL, "table arrays must be non-null");
+  return RAMP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ramp_version(void) { return 100; }
+
+const char* ramp_last_error(void) { return g_last_error.c_str(); }
+
+int ramp_device_ok(void) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return (major == 10 && minor == 0) ? 1 : 0;
+}
+
+int64_t ramp_align_capacity(int64_t n_assign, int32_t E, int32_t bm) {
+  if (n_assign < 0 || E < 1 || bm < 1) return 0;
+  const int64_t cap = n_assign + (int64_t)E * (bm - 1);
+  return (cap + bm - 1) / bm * bm;
+}
+
+int64_t ramp_config_smem_bytes(int32_t bm, int32_t ttn, int32_t stg) {
+  return ramp::config_smem_bytes(bm, ttn, stg);
+}
+
+int ramp_moe_align(const int32_t* topk_ids, int64_t n_assign, int32_t E, int32_t bm, int32_t* hist,
+                   int32_t* sorted_ids, int32_t* tile_expert, int32_t* n_post_pad, void* stream) {
+  if (E < 1 || E > ramp::kMaxExperts) return fail(RAMP_EINVAL, "E must be in [1, 1024]");
+  if (bm < 1) return fail(RAMP_EINVAL, "bm must be >= 1");
+  if (n_assign < 0 || n_assign >= (int64_t(1) << 31) - (int64_t)E * bm)
+    return fail(RAMP_EINVAL, "n_assign out of range");
+  if (!hist || !sorted_ids || !tile_expert || !n_post_pad || (n_assign > 0 && !topk_ids))
+    return fail(RAMP_EINVAL, "null buffer");
+  cudaError_t err = ramp::launch_align(topk_ids, n_assign, E, bm, hist, sorted_ids, tile_expert, n_post_pad,
+                                       static_cast<cudaStream_t>(stream));
+  if (err != cudaSuccess) return cuda_fail(err, "ramp_moe_align");
+  return RAMP_OK;
+}
+
+int ramp_dispatch_select(const int32_t* hist, int32_t E, const ramp_table_t* table, int32_t* cfg_out,
+                         int32_t* n_eval_out, int64_t* grid_out, double* pred_out, void* stream) {
+  if (int rc = check_table(table)) return rc;
+  if (E < 1 || E > ramp::kMaxExperts) return fail(RAMP_EINVAL, "E must be in [1, 1024]");
+  if (!hist || !cfg_out) return fail(RAMP_EINVAL, "null buffer");
+  cudaError_t err = ramp::launch_select(hist, E, *table, cfg_out, n_eval_out, grid_out, pred_out,
+                                        static_cast<cudaStream_t>(stream));
+  if (err != cudaSuccess) return cuda_fail(err, "ramp_dispatch_select");
+  return RAMP_OK;
+}
+
+size_t ramp_fused_moe_workspace_size(int32_t S, int32_t H, int32_t E, int32_t top_k) {
+  if (S < 0 || H < 1 || E < 1 || top_k < 1) return 0;
+  return layout_for(S, H, E, top_k).total;
+}
+
+int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const float* topk_w,
+                        const int32_t* topk_ids, int32_t S, int32_t H, int32_t I, int32_t E, int32_t top_k,
+                        const ramp_table_t* table, int32_t forced_cfg, void* out, int32_t* sel_out,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+  if (int rc = check_table(table)) return rc;
+  if (S < 0) return fail(RAMP_EINVAL, "S must be >= 0");
+  if (E < 1 || E > ramp::kMaxExperts) return fail(RAMP_EINVAL, "E must be in [1, 1024]");
+  if (top_k < 1 || top_k > E) return fail(RAMP_EINVAL, "top_k must be in [1, E]");
+  if (H < 128 || H % 128 != 0) return fail(RAMP_EINVAL, "H (d_model) must be a positive multiple of 128");
+  if (I < 128 || I % 128 != 0) return fail(RAMP_EINVAL, "I (d_ff) must be a positive multiple of 128");
+  if (table->N != 2 * I) return fail(RAMP_EINVAL, "table geometry N must equal 2*I");
+  if (forced_cfg >= table->n_cfg) return fail(RAMP_EINVAL, "forced_cfg out of range");
+  if (S > 0 && (!x || !w1 || !w2 || !topk_w || !topk_ids || !out))
+    return fail(RAMP_EINVAL, "null tensor");
+  for (const void* p : {x, w1, w2, (const void*)out})
+    if (reinterpret_cast<uintptr_t>(p) % 16 != 0) return fail(RAMP_EINVAL, "tensors must be 16-byte aligned");
+  const WorkspaceLayout L = layout_for(S, H, E, top_k);
+  if (!workspace || workspace_bytes < L.total) return fail(RAMP_EINVAL, "workspace too small");
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
+    return fail(RAMP_EINVAL, "workspace must be 256-byte aligned");
+  auto* ws = static_cast<unsigned char*>(workspace);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (S == 0) {
+    if (sel_out) {
+      cudaError_t err = cudaMemsetAsync(sel_out, 0, 4 * sizeof(int32_t), st);
+      if (err != cudaSuccess) return cuda_fail(err, "ramp_fused_moe_bf16");
+    }
+    return RAMP_OK;
+  }
+
+  ramp::RouteArgs ra{};
+  ra.topk_ids = topk_ids;
+  ra.n_assign = (int64_t)S * top_k;
+  ra.E = E;
+  ra.forced_cfg = forced_cfg;
+  ra.table = *table;
+  ra.ctrl = reinterpret_cast<int32_t*>(ws + L.ctrl);
+  ra.hist_out = reinterpret_cast<int32_t*>(ws + L.hist);
+  ra.sorted_ids = reinterpret_cast<int32_t*>(ws + L.sorted);
+  ra.tile_expert = reinterpret_cast<int32_t*>(ws + L.tiles);
+  ra.sel_out = sel_out;
+  ra.acc_clear = reinterpret_cast<float*>(ws + L.acc);
+  ra.acc_clear_n = (int64_t)S * H;
+  int zero_blocks = (int)((ra.acc_clear_n / 4 + 1023) / 1024);
+  if (zero_blocks > 296) zero_blocks = 296;
+  if (zero_blocks < 1) zero_blocks = 1;
+  cudaError_t err = ramp::launch_route(ra, zero_blocks, st);
+  if (err != cudaSuccess) return cuda_fail(err, "route kernel");
+
+  ramp::MoeLaunch ml{};
+  ml.x = x;
+  ml.w1 = w1;
+  ml.w2 = w2;
+  ml.topk_w = topk_w;
+  ml.ctrl = ra.ctrl;
+  ml.sorted_ids = ra.sorted_ids;
+  ml.tile_expert = ra.tile_expert;
+  ml.out_acc = ra.acc_clear;
+  ml.out = out;
+  ml.table = *table;
+  ml.S = S;
+  ml.H = H;
+  ml.I = I;
+  ml.E = E;
+  ml.top_k = top_k;
+  const char* why = nullptr;
+  err = ramp::launch_fused_moe_bf16(ml, st, &why);
+  if (err != cudaSuccess) return why ? fail(RAMP_ECUDA, why) : cuda_fail(err, "fused_moe kernel");
+  return RAMP_OK;
+}
+
+}  // extern "C"

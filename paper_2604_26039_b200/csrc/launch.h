@@ -1,0 +1,55 @@
+// Host-side launchers shared between the translation units of libramp_b200.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../../include/ramp_b200.h"
+
+namespace ramp {
+
+constexpr int kMaxBm = 128;  // largest token block the megakernel supports
+
+struct RouteArgs {
+  const int32_t* topk_ids;
+  int64_t n_assign;
+  int32_t E;
+  int32_t forced_cfg;
+  ramp_table_t table;
+  int32_t* ctrl;         // [16]: cfg, n_post_pad, n_mtiles, n_eval, bad_ids
+  int32_t* hist_out;     // [E] or null
+  int32_t* sorted_ids;   // [capacity]
+  int32_t* tile_expert;  // [capacity]
+  int32_t* sel_out;      // [4] or null
+  int32_t* n_eval_out;   // or null
+  int64_t* grid_out;     // [n_cfg] or null
+  double* pred_out;      // [n_cfg] or null
+  float* acc_clear;      // fp32 accumulator cleared by the helper blocks
+  int64_t acc_clear_n;
+};
+
+cudaError_t launch_route(const RouteArgs& a, int zero_blocks, cudaStream_t stream);
+cudaError_t launch_align(const int32_t* ids, int64_t n, int E, int bm, int32_t* hist, int32_t* sorted_ids,
+                         int32_t* tile_expert, int32_t* n_post_pad, cudaStream_t stream);
+cudaError_t launch_select(const int32_t* hist, int E, const ramp_table_t& t, int32_t* cfg_out,
+                          int32_t* n_eval_out, int64_t* grid_out, double* pred_out,
+                          cudaStream_t stream);
+
+struct MoeLaunch {
+  const void* x;
+  const void* w1;
+  const void* w2;
+  const float* topk_w;
+  const int32_t* ctrl;
+  const int32_t* sorted_ids;
+  const int32_t* tile_expert;
+  float* out_acc;
+  void* out;
+  ramp_table_t table;
+  int32_t S, H, I, E, top_k;
+};
+
+cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const char** why);
+int64_t config_smem_bytes(int bm, int ttn, int stg);
+
+}  // namespace ramp

@@ -1,0 +1,128 @@
+// Route kernels: histogram, dispatcher and alignment (compiled with
+// -fmad=false so the fp64 cost model matches numpy's unfused arithmetic).
+#include <cuda_runtime.h>
+
+#include "launch.h"
+#include "route.cuh"
+
+namespace ramp {
+
+struct RouteStatic {
+  int64_t mt[kMaxUbm];
+  ArgMin red[32];
+  int cnt[32];
+  int warp_tot[32];
+  int bad;
+};
+
+__global__ void __launch_bounds__(kRouteThreads, 1)
+    route_kernel(const RouteArgs a) {
+  if (blockIdx.x > 0) {
+    // Helper blocks clear the fp32 output accumulator of the megakernel.
+    float4* acc4 = reinterpret_cast<float4*>(a.acc_clear);
+    const int64_t n4 = a.acc_clear_n / 4;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = (blockIdx.x - 1) * (int64_t)blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)(gridDim.x - 1) * blockDim.x)
+      acc4[i] = z;
+    for (int64_t i = n4 * 4 + (blockIdx.x - 1) * (int64_t)blockDim.x + threadIdx.x; i < a.acc_clear_n;
+         i += (int64_t)(gridDim.x - 1) * blockDim.x)
+      a.acc_clear[i] = 0.f;
+    return;
+  }
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ RouteStatic st;
+  RouteSmem s = carve_route_smem(dyn, a.E);
+  if (threadIdx.x == 0) st.bad = 0;
+  __syncthreads();
+  block_histogram(a.topk_ids, a.n_assign, a.E, s.hist, &st.bad);
+  int sel = a.forced_cfg;
+  int n_eval = 0;
+  if (sel < 0) {
+    sel = block_dispatch(s.hist, a.E, a.table, a.grid_out, a.pred_out, a.n_eval_out, st.mt, st.red,
+                         st.cnt);
+    n_eval = st.cnt[0];
+  }
+  const int bm = a.table.bm[sel];
+  int32_t* n_post_pad = a.ctrl + 1;
+  block_align(a.topk_ids, a.n_assign, a.E, bm, s, st.warp_tot, a.sorted_ids, a.tile_expert,
+              n_post_pad);
+  for (int e = threadIdx.x; e < a.E; e += blockDim.x)
+    if (a.hist_out) a.hist_out[e] = s.hist[e];
+  if (threadIdx.x == 0) {
+    const int npp = s.off[a.E];
+    a.ctrl[0] = sel;
+    a.ctrl[2] = npp / bm;
+    a.ctrl[3] = n_eval;
+    a.ctrl[4] = st.bad;
+    if (a.sel_out) {
+      a.sel_out[0] = sel;
+      a.sel_out[1] = npp;
+      a.sel_out[2] = npp / bm;
+      a.sel_out[3] = n_eval;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kRouteThreads, 1)
+    align_kernel(const int32_t* ids, int64_t n, int E, int bm, int32_t* hist_out, int32_t* sorted_ids,
+                 int32_t* tile_expert, int32_t* n_post_pad) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ int warp_tot[32];
+  __shared__ int bad;
+  RouteSmem s = carve_route_smem(dyn, E);
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  block_histogram(ids, n, E, s.hist, &bad);
+  block_align(ids, n, E, bm, s, warp_tot, sorted_ids, tile_expert, n_post_pad);
+  for (int e = threadIdx.x; e < E; e += blockDim.x) hist_out[e] = s.hist[e];
+}
+
+__global__ void __launch_bounds__(kRouteThreads, 1)
+    select_kernel(const int32_t* hist, int E, const ramp_table_t t, int32_t* cfg_out, int32_t* n_eval_out,
+                  int64_t* grid_out, double* pred_out) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ RouteStatic st;
+  int32_t* h = reinterpret_cast<int32_t*>(dyn);
+  for (int e = threadIdx.x; e < E; e += blockDim.x) h[e] = hist[e];
+  __syncthreads();
+  const int sel = block_dispatch(h, E, t, grid_out, pred_out, n_eval_out, st.mt, st.red, st.cnt);
+  if (threadIdx.x == 0) *cfg_out = sel;
+}
+
+cudaError_t launch_route(const RouteArgs& a, int zero_blocks, cudaStream_t stream) {
+  const size_t smem = route_smem_bytes(a.E);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t err = cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)route_smem_bytes(kMaxExperts));
+    if (err != cudaSuccess) return err;
+    attr_set = true;
+  }
+  route_kernel<<<1 + zero_blocks, kRouteThreads, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_align(const int32_t* ids, int64_t n, int E, int bm, int32_t* hist, int32_t* sorted_ids,
+                         int32_t* tile_expert, int32_t* n_post_pad, cudaStream_t stream) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t err = cudaFuncSetAttribute(align_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)route_smem_bytes(kMaxExperts));
+    if (err != cudaSuccess) return err;
+    attr_set = true;
+  }
+  align_kernel<<<1, kRouteThreads, route_smem_bytes(E), stream>>>(ids, n, E, bm, hist, sorted_ids,
+                                                                  tile_expert, n_post_pad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select(const int32_t* hist, int E, const ramp_table_t& t, int32_t* cfg_out,
+                          int32_t* n_eval_out, int64_t* grid_out, double* pred_out,
+                          cudaStream_t stream) {
+  select_kernel<<<1, kRouteThreads, sizeof(int32_t) * E, stream>>>(hist, E, t, cfg_out, n_eval_out,
+                                                                   grid_out, pred_out);
+  return cudaGetLastError();
+}
+
+}  // namespace ramp

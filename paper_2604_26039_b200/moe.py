@@ -1,0 +1,216 @@
+"""PyTorch host API of the fused-MoE hot path.
+
+`fused_moe` is the drop-in for the kernel the reference simulates
+(`simulate_pool_times`, ramp/oracle.py:197-254) fused with the dispatch call
+in front of it (`select_config`, ramp/dispatch.py:89-122).  Tensors are torch
+CUDA tensors; the heavy lifting is one C-ABI call into libramp_b200.so, which
+launches three kernels (route, megakernel, finalize) on the current stream
+with no host synchronisation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+@dataclass
+class DeviceTable:
+    """Device-resident dispatch table (`ramp_table_t`): per-config integer
+    fields and the four fitted floats (ramp/dispatch.py:57-86).  Arrays are
+    kept alive by this object; `struct` is what the C ABI receives."""
+
+    bm: np.ndarray
+    ttn: np.ndarray
+    stg: np.ndarray
+    split_k: np.ndarray
+    group_m: np.ndarray
+    a: np.ndarray
+    b: np.ndarray
+    c: np.ndarray
+    d: np.ndarray
+    N: int
+    kappa_ok: bool
+    sm_count: int
+    device: torch.device | str = "cuda"
+    _tensors: dict = field(default_factory=dict, repr=False)
+    struct: _lib.RampTable | None = field(default=None, repr=False)
+
+    def __post_init__(self) -> None:
+        n = len(self.bm)
+        if n == 0:
+            raise ValueError("dispatch table over an empty pool")
+        for name in ("ttn", "stg", "split_k", "group_m", "a", "b", "c", "d"):
+            if len(getattr(self, name)) != n:
+                raise ValueError(f"column {name} has length {len(getattr(self, name))}, expected {n}")
+        ubm, ubm_index = np.unique(np.asarray(self.bm, dtype=np.int64), return_inverse=True)
+        if len(ubm) > 128:
+            raise ValueError("at most 128 distinct bm values are supported")
+        i32 = dict(dtype=torch.int32, device=self.device)
+        f64 = dict(dtype=torch.float64, device=self.device)
+        t = self._tensors
+        for name in ("bm", "ttn", "stg", "split_k", "group_m"):
+            t[name] = torch.as_tensor(np.asarray(getattr(self, name), dtype=np.int32), **i32)
+        t["ubm"] = torch.as_tensor(ubm.astype(np.int32), **i32)
+        t["ubm_index"] = torch.as_tensor(ubm_index.astype(np.int32), **i32)
+        for name in ("a", "b", "c", "d"):
+            t[name] = torch.as_tensor(np.asarray(getattr(self, name), dtype=np.float64), **f64)
+        s = _lib.RampTable()
+        s.n_cfg = n
+        s.n_ubm = len(ubm)
+        s.N = int(self.N)
+        s.kappa_ok = int(bool(self.kappa_ok))
+        s.sm_count = int(self.sm_count)
+        for name in ("bm", "ttn", "stg", "split_k", "group_m", "ubm", "ubm_index", "a", "b", "c", "d"):
+            setattr(s, name, t[name].data_ptr())
+        self.struct = s
+
+    def __len__(self) -> int:
+        return len(self.bm)
+
+    @property
+    def ref(self):
+        return ctypes.byref(self.struct)
+
+
+def workspace_bytes(S: int, H: int, E: int, top_k: int) -> int:
+    return int(_lib.load().ramp_fused_moe_workspace_size(S, H, E, top_k))
+
+
+class Workspace:
+    """Reusable device workspace for `fused_moe` (route outputs + fp32 accumulator)."""
+
+    def __init__(self, S: int, H: int, E: int, top_k: int, device="cuda"):
+        self.key = (S, H, E, top_k)
+        n = workspace_bytes(S, H, E, top_k)
+        self.buf = torch.empty(max(n, 256), dtype=torch.uint8, device=device)
+        self.sel = torch.zeros(4, dtype=torch.int32, device=device)
+
+    def fits(self, S: int, H: int, E: int, top_k: int) -> bool:
+        return self.buf.numel() >= workspace_bytes(S, H, E, top_k)
+
+
+def fused_moe(
+    hidden_states: torch.Tensor,
+    w1: torch.Tensor,
+    w2: torch.Tensor,
+    topk_weights: torch.Tensor,
+    topk_ids: torch.Tensor,
+    table: DeviceTable,
+    forced_cfg: int = -1,
+    out: torch.Tensor | None = None,
+    workspace: Workspace | None = None,
+) -> torch.Tensor:
+    """Fused MoE layer forward, BF16:
+
+        out[t] = sum_j w[t, j] * W2[e] (silu(W1[e, :I] x_t) * W1[e, I:] x_t),  e = ids[t, j]
+
+    hidden_states [S, H] bf16; w1 [E, 2I, H] bf16 (gate rows first, vLLM
+    layout); w2 [E, H, I] bf16; topk_weights [S, k] fp32; topk_ids [S, k]
+    int32.  `forced_cfg < 0` lets the on-device dispatcher choose the tile
+    config from the live histogram; a config id forces it (static dispatch or
+    the exhaustive sweep).  The selection record {cfg, n_post_pad, n_mtiles,
+    n_eval} is left in `workspace.sel` (device int32[4]).
+    """
+    lib = _lib.load()
+    S, H = hidden_states.shape
+    E, two_i, H1 = w1.shape
+    I = two_i // 2
+    k = topk_ids.shape[1]
+    if H1 != H or tuple(w2.shape) != (E, H, I):
+        raise ValueError(f"shape mismatch: x {tuple(hidden_states.shape)}, w1 {tuple(w1.shape)}, w2 {tuple(w2.shape)}")
+    for name, t, dt in (("hidden_states", hidden_states, torch.bfloat16), ("w1", w1, torch.bfloat16),
+                        ("w2", w2, torch.bfloat16), ("topk_weights", topk_weights, torch.float32),
+                        ("topk_ids", topk_ids, torch.int32)):
+        if t.dtype != dt:
+            raise ValueError(f"{name} must be {dt}, got {t.dtype}")
+        if not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+    if tuple(topk_weights.shape) != (S, k):
+        raise ValueError("topk_weights must be [S, top_k]")
+    if out is None:
+        out = torch.empty(S, H, dtype=torch.bfloat16, device=hidden_states.device)
+    if workspace is None or not workspace.fits(S, H, E, k):
+        workspace = Workspace(S, H, E, k, device=hidden_states.device)
+    _lib.check(
+        lib.ramp_fused_moe_bf16(
+            hidden_states.data_ptr(), w1.data_ptr(), w2.data_ptr(), topk_weights.data_ptr(),
+            topk_ids.data_ptr(), S, H, I, E, k, table.ref, int(forced_cfg), out.data_ptr(),
+            workspace.sel.data_ptr(), workspace.buf.data_ptr(), workspace.buf.numel(), _stream(),
+        )
+    )
+    return out
+
+
+def moe_align_block_size(topk_ids: torch.Tensor, num_experts: int, block_size: int):
+    """Histogram + alignment on the GPU (north_star (1)).
+
+    Returns (sorted_token_ids, expert_ids, num_tokens_post_padded, hist), the
+    vLLM names: sorted ids are flat assignment indices (padding value =
+    topk_ids.numel()), expert_ids the expert of every block_size-row tile.
+    Buffers are sized to the worst case; only the first
+    num_tokens_post_padded entries (resp. / block_size) are meaningful."""
+    lib = _lib.load()
+    if topk_ids.dtype != torch.int32 or not topk_ids.is_cuda:
+        raise ValueError("topk_ids must be an int32 CUDA tensor")
+    ids = topk_ids.contiguous().view(-1)
+    n = ids.numel()
+    cap = int(lib.ramp_align_capacity(n, num_experts, block_size))
+    dev = ids.device
+    sorted_ids = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    expert_ids = torch.empty(max(cap // block_size, 1), dtype=torch.int32, device=dev)
+    npp = torch.empty(1, dtype=torch.int32, device=dev)
+    hist = torch.empty(num_experts, dtype=torch.int32, device=dev)
+    _lib.check(
+        lib.ramp_moe_align(ids.data_ptr(), n, num_experts, block_size, hist.data_ptr(),
+                           sorted_ids.data_ptr(), expert_ids.data_ptr(), npp.data_ptr(), _stream())
+    )
+    return sorted_ids, expert_ids, npp, hist
+
+
+def dispatch_select(hist: torch.Tensor, table: DeviceTable, want_grids: bool = False,
+                    want_pred: bool = False):
+    """On-device dispatcher over a device histogram (north_star (3)).
+
+    Returns device tensors (cfg[1], n_eval[1], grids or None, pred or None);
+    nothing is copied to the host."""
+    lib = _lib.load()
+    if hist.dtype != torch.int32 or not hist.is_cuda:
+        raise ValueError("hist must be an int32 CUDA tensor")
+    dev = hist.device
+    cfg = torch.empty(1, dtype=torch.int32, device=dev)
+    n_eval = torch.empty(1, dtype=torch.int32, device=dev)
+    grids = torch.empty(len(table), dtype=torch.int64, device=dev) if want_grids else None
+    pred = torch.empty(len(table), dtype=torch.float64, device=dev) if want_pred else None
+    _lib.check(
+        lib.ramp_dispatch_select(hist.contiguous().data_ptr(), hist.numel(), table.ref, cfg.data_ptr(),
+                                 n_eval.data_ptr(), _ptr(grids), _ptr(pred), _stream())
+    )
+    return cfg, n_eval, grids, pred
+
+
+def flops(S: int, top_k: int, H: int, I: int) -> int:
+    """Algorithmic FLOPs of one layer call: 6*S*k*H*I."""
+    return 6 * S * top_k * H * I
+
+
+def algorithmic_bytes(active_experts: int, S: int, top_k: int, H: int, I: int, w_bytes: int = 2,
+                      x_bytes: int = 2, out_bytes: int = 2) -> int:
+    """Bytes a perfect kernel must move: active experts' weights once, the
+    activations in and out once, ids+weights."""
+    return active_experts * 3 * H * I * w_bytes + S * H * (x_bytes + out_bytes) + 8 * S * top_k
