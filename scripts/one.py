@@ -1,0 +1,45 @@
+"""Run one (S, skew, config) point a few times -- the target for ncu captures."""
+import argparse
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2604_26039_b200 import moe as M  # noqa: E402
+from paper_2604_26039_b200.catalog import MoeGeometry  # noqa: E402
+from paper_2604_26039_b200.config_space import enumerate_b200_configs  # noqa: E402
+from scripts.probe import topk  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--S", type=int, default=512)
+ap.add_argument("--skew", type=float, default=0.0)
+ap.add_argument("--bm", type=int, default=64)
+ap.add_argument("--ttn", type=int, default=512)
+ap.add_argument("--stg", type=int, default=2)
+ap.add_argument("--gm", type=int, default=0)
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--E", type=int, default=64)
+ap.add_argument("--H", type=int, default=2048)
+ap.add_argument("--I", type=int, default=1024)
+ap.add_argument("--k", type=int, default=8)
+a = ap.parse_args()
+E, H, I, k, S = a.E, a.H, a.I, a.k, a.S
+gen = torch.Generator(device="cuda").manual_seed(0)
+w1 = (torch.randn(E, 2 * I, H, device="cuda", generator=gen) / H ** 0.5).to(torch.bfloat16)
+w2 = (torch.randn(E, H, I, device="cuda", generator=gen) / I ** 0.5).to(torch.bfloat16)
+pool = enumerate_b200_configs(MoeGeometry(name="p", E=E, N=2 * I, K=H, top_k=k))
+cols = pool.columns()
+n = len(pool)
+table = M.DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
+                      group_m=cols["group_m"].astype(np.int64), a=np.ones(n), b=np.zeros(n), c=np.zeros(n),
+                      d=np.zeros(n), N=2 * I, kappa_ok=False, sm_count=148)
+cfg = [c.id for c in pool if (c.bm, c.ttn, c.stg, int(c.group_m)) == (a.bm, a.ttn, a.stg, a.gm)][0]
+x = torch.randn(S, H, device="cuda", generator=gen).to(torch.bfloat16)
+ids, w = topk(S, k, E, a.skew, gen)
+ws = M.Workspace(S, H, E, k)
+for _ in range(a.reps):
+    out = M.fused_moe(x, w1, w2, w, ids, table, cfg, workspace=ws)
+torch.cuda.synchronize()
+print("ok", cfg, out.float().abs().mean().item())
