@@ -52,6 +52,7 @@ typedef struct ramp_table {
   const int32_t* stg;
   const int32_t* split_k;
   const int32_t* group_m;
+  const int32_t* mode;    /* megakernel mode: 0 fused (act in smem), 1 split (act in L2); may be null = 0 */
   const int32_t* ubm;
   const int32_t* ubm_index;
   const double* a;
@@ -105,19 +106,27 @@ int ramp_dispatch_select(const int32_t* hist, int32_t E, const ramp_table_t* tab
  *   forced_cfg < 0   select on device from the live histogram (routing-aware)
  *   forced_cfg >= 0  run that config id (static dispatch / exhaustive sweep)
  *   sel_out          optional device int32[4]: {cfg, n_post_pad, n_work, n_eval}
- * workspace: >= ramp_fused_moe_workspace_size(...) bytes of device memory.
+ * workspace: >= ramp_fused_moe_workspace_size(...) bytes of device memory,
+ *            zero-filled once before its first use (it carries the route
+ *            kernel's completion flags between calls).
  * Replaces the kernel that simulate_pool_times stands in for
  * (ramp/oracle.py:197-254) together with the select_config call before it. */
-size_t ramp_fused_moe_workspace_size(int32_t S, int32_t H, int32_t E, int32_t top_k);
+size_t ramp_fused_moe_workspace_size(int32_t S, int32_t H, int32_t I, int32_t E, int32_t top_k);
 int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const float* topk_w,
                         const int32_t* topk_ids, int32_t S, int32_t H, int32_t I, int32_t E,
                         int32_t top_k, const ramp_table_t* table, int32_t forced_cfg, void* out,
                         int32_t* sel_out, void* workspace, size_t workspace_bytes, void* stream);
 
-/* Shared-memory bytes the megakernel needs for (bm, ttn, stg); 0 if the
+/* Shared-memory bytes the megakernel needs for (bm, ttn, stg, mode); 0 if the
  * configuration is not realisable on this part (pool admissibility test,
  * the B200 counterpart of smem_usage/is_valid, ramp/config_space.py:122-138). */
-int64_t ramp_config_smem_bytes(int32_t bm, int32_t ttn, int32_t stg);
+int64_t ramp_config_smem_bytes(int32_t bm, int32_t ttn, int32_t stg, int32_t mode);
+
+/* Diagnostics: when dev_buf is non-null, every later megakernel launch writes
+ * 16 per-CTA cycle counters (producer wait/issue, MMA waits, epilogue phases,
+ * see ProfSlot in csrc/fused_moe.cuh) to dev_buf[blockIdx * 16 + slot].
+ * Pass null to switch it off.  Not used on the timed path. */
+void ramp_set_profile_buffer(unsigned long long* dev_buf);
 
 #ifdef __cplusplus
 }

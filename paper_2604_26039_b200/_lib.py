@@ -18,10 +18,11 @@ c_i32p = ctypes.POINTER(ctypes.c_int32)
 # Every symbol include/ramp_b200.h declares, with (restype, argtypes).
 SIGNATURES = {
     "ramp_version": (ctypes.c_int, []),
+    "ramp_set_profile_buffer": (None, [ctypes.c_void_p]),
     "ramp_last_error": (ctypes.c_char_p, []),
     "ramp_device_ok": (ctypes.c_int, []),
     "ramp_align_capacity": (ctypes.c_int64, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32]),
-    "ramp_config_smem_bytes": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
+    "ramp_config_smem_bytes": (ctypes.c_int64, [ctypes.c_int32] * 4),
     "ramp_moe_align": (
         ctypes.c_int,
         [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
@@ -32,9 +33,7 @@ SIGNATURES = {
         [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
     ),
-    "ramp_fused_moe_workspace_size": (
-        ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
-    ),
+    "ramp_fused_moe_workspace_size": (ctypes.c_size_t, [ctypes.c_int32] * 5),
     "ramp_fused_moe_bf16": (
         ctypes.c_int,
         [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
@@ -60,6 +59,7 @@ class RampTable(ctypes.Structure):
         ("stg", ctypes.c_void_p),
         ("split_k", ctypes.c_void_p),
         ("group_m", ctypes.c_void_p),
+        ("mode", ctypes.c_void_p),
         ("ubm", ctypes.c_void_p),
         ("ubm_index", ctypes.c_void_p),
         ("a", ctypes.c_void_p),

@@ -26,25 +26,33 @@ int cuda_fail(cudaError_t err, const char* where) {
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct WorkspaceLayout {
-  size_t ctrl, hist, sorted, tiles, acc, total;
-  int64_t capacity;
+  size_t ctrl, hist, sorted, tiles, done, acc, xs, act, total;
+  int64_t capacity, rows;
 };
 
-WorkspaceLayout layout_for(int32_t S, int32_t H, int32_t E, int32_t top_k) {
+// Device workspace of one fused_moe call (all regions 256-byte aligned):
+// route control words, histogram, aligned ids, M-tile experts, split-mode
+// counters, the fp32 output accumulator, expert-sorted tokens and the
+// split-mode intermediate activations.
+WorkspaceLayout layout_for(int32_t S, int32_t H, int32_t I, int32_t E, int32_t top_k) {
   WorkspaceLayout w{};
   const int64_t n_assign = (int64_t)S * top_k;
   w.capacity = ramp_align_capacity(n_assign, E, ramp::kMaxBm);
+  w.rows = w.capacity + 128;  // an M-tile box may read up to 128 rows past the end
   size_t off = 0;
-  w.ctrl = off;
-  off = align_up(off + 64, 256);
-  w.hist = off;
-  off = align_up(off + sizeof(int32_t) * E, 256);
-  w.sorted = off;
-  off = align_up(off + sizeof(int32_t) * w.capacity, 256);
-  w.tiles = off;
-  off = align_up(off + sizeof(int32_t) * w.capacity, 256);
-  w.acc = off;
-  off = align_up(off + sizeof(float) * (size_t)S * H, 256);
+  auto take = [&](size_t bytes) {
+    const size_t at = off;
+    off = align_up(off + bytes, 256);
+    return at;
+  };
+  w.ctrl = take(64);
+  w.hist = take(sizeof(int32_t) * E);
+  w.sorted = take(sizeof(int32_t) * w.capacity);
+  w.tiles = take(sizeof(int32_t) * w.capacity);
+  w.done = take(sizeof(int32_t) * w.capacity);
+  w.acc = take(sizeof(float) * (size_t)S * H);
+  w.xs = take(2 * (size_t)w.rows * H);
+  w.act = take(2 * (size_t)w.rows * I);
   w.total = off;
   return w;
 }
@@ -66,6 +74,8 @@ extern "C" {
 
 int ramp_version(void) { return 100; }
 
+void ramp_set_profile_buffer(unsigned long long* dev_buf) { ramp::g_prof_buffer = dev_buf; }
+
 const char* ramp_last_error(void) { return g_last_error.c_str(); }
 
 int ramp_device_ok(void) {
@@ -85,8 +95,8 @@ int64_t ramp_align_capacity(int64_t n_assign, int32_t E, int32_t bm) {
   return (cap + bm - 1) / bm * bm;
 }
 
-int64_t ramp_config_smem_bytes(int32_t bm, int32_t ttn, int32_t stg) {
-  return ramp::config_smem_bytes(bm, ttn, stg);
+int64_t ramp_config_smem_bytes(int32_t bm, int32_t ttn, int32_t stg, int32_t mode) {
+  return ramp::config_smem_bytes(bm, ttn, stg, mode);
 }
 
 int ramp_moe_align(const int32_t* topk_ids, int64_t n_assign, int32_t E, int32_t bm, int32_t* hist,
@@ -114,9 +124,9 @@ int ramp_dispatch_select(const int32_t* hist, int32_t E, const ramp_table_t* tab
   return RAMP_OK;
 }
 
-size_t ramp_fused_moe_workspace_size(int32_t S, int32_t H, int32_t E, int32_t top_k) {
-  if (S < 0 || H < 1 || E < 1 || top_k < 1) return 0;
-  return layout_for(S, H, E, top_k).total;
+size_t ramp_fused_moe_workspace_size(int32_t S, int32_t H, int32_t I, int32_t E, int32_t top_k) {
+  if (S < 0 || H < 1 || I < 1 || E < 1 || top_k < 1) return 0;
+  return layout_for(S, H, I, E, top_k).total;
 }
 
 int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const float* topk_w,
@@ -135,7 +145,7 @@ int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const flo
     return fail(RAMP_EINVAL, "null tensor");
   for (const void* p : {x, w1, w2, (const void*)out})
     if (reinterpret_cast<uintptr_t>(p) % 16 != 0) return fail(RAMP_EINVAL, "tensors must be 16-byte aligned");
-  const WorkspaceLayout L = layout_for(S, H, E, top_k);
+  const WorkspaceLayout L = layout_for(S, H, I, E, top_k);
   if (!workspace || workspace_bytes < L.total) return fail(RAMP_EINVAL, "workspace too small");
   if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
     return fail(RAMP_EINVAL, "workspace must be 256-byte aligned");
@@ -162,9 +172,18 @@ int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const flo
   ra.sel_out = sel_out;
   ra.acc_clear = reinterpret_cast<float*>(ws + L.acc);
   ra.acc_clear_n = (int64_t)S * H;
-  int zero_blocks = (int)((ra.acc_clear_n / 4 + 1023) / 1024);
-  if (zero_blocks > 296) zero_blocks = 296;
-  if (zero_blocks < 1) zero_blocks = 1;
+  ra.done = reinterpret_cast<int*>(ws + L.done);
+  ra.x = x;
+  ra.x_sorted = ws + L.xs;
+  ra.S = S;
+  ra.H = H;
+  ra.top_k = top_k;
+  // helpers: enough to clear the accumulator and gather ~4 rows per warp,
+  // at most two 1024-thread blocks per SM so all of them are co-resident
+  int64_t want = (ra.acc_clear_n / 4 + 4095) / 4096;
+  const int64_t gather = (ra.n_assign + (int64_t)E * 4 + 127) / 128;
+  if (gather > want) want = gather;
+  int zero_blocks = (int)(want < 1 ? 1 : (want > 287 ? 287 : want));
   cudaError_t err = ramp::launch_route(ra, zero_blocks, st);
   if (err != cudaSuccess) return cuda_fail(err, "route kernel");
 
@@ -178,6 +197,10 @@ int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const flo
   ml.tile_expert = ra.tile_expert;
   ml.out_acc = ra.acc_clear;
   ml.out = out;
+  ml.x_sorted = ws + L.xs;
+  ml.act_g = ws + L.act;
+  ml.done = ra.done;
+  ml.rows = L.rows;
   ml.table = *table;
   ml.S = S;
   ml.H = H;

@@ -1,23 +1,34 @@
-// Persistent fused MoE megakernel for sm_100a (north_star (2)).
+// Persistent fused-MoE megakernel for sm_100a (north_star (2)).
 //
-// One work item = (M-tile of bm aligned assignments of one expert) x (stripe
-// of n_i = ttn/2 intermediate features).  For each work item one CTA runs the
-// paper's three phases without touching HBM in
-// between:
-//   P1  acc1[ttn x bm] = W1[e][gate|up stripe] . X[gathered tokens]^T
-//       TMA (weights, 128x64 SW128 boxes) + TMA gather4 (token rows) ->
-//       tcgen05.mma kind::f16, M=128 weight rows, N=bm tokens ("swap-AB":
-//       the weights are the M operand so bm can be 4..128), fp32 in TMEM.
-//   P2  act = silu(gate) * up, TMEM -> registers -> bf16 in shared memory,
-//       written directly in the SW128 K-major layout the next MMA reads.
-//   P3  for every 128-row chunk of H: acc3 = W2[e][chunk, stripe] . act^T
-//       (double-buffered in TMEM), then the epilogue scales by the top-k
-//       weight and scatter-reduces into the fp32 output (red.global.add).
+// The layer  out[t] = sum_j w[t,j] * W2[e] (silu(W1g[e] x_t) * W1u[e] x_t)
+// runs as ONE launch of one CTA per SM that walks a list of jobs.  Token rows
+// were pre-gathered by the route kernel into expert-sorted order (x_sorted),
+// so every operand tile arrives with a single TMA box:
+//
+//   phase 1  acc[ttn x bm] = W1[e][gate|up stripe] . x_sorted[M-tile]^T
+//            one 3D TMA box {64, n_i, 2} brings the gate AND up rows of a
+//            k-block, one 2D box brings bm token rows; tcgen05.mma kind::f16
+//            with M = 128 weight rows, N = bm tokens ("swap-AB", so bm can be
+//            4..128), fp32 accumulators in TMEM.
+//   phase 2  act = silu(gate) * up   (TMEM -> registers -> bf16)
+//   phase 3  acc[128 x bm] = W2[e][h-chunk, :] . act^T, then the epilogue
+//            scales by the top-k weight and scatter-reduces into the fp32
+//            output with 16-byte vector reductions (red.global.v4.f32).
+//
+// Two polymorphic modes (a dispatcher-selected config field, in the spirit of
+// the paper's "polymorphic modes"):
+//   FUSED (mode 0)  one job = (M-tile, I-stripe): all three phases in one CTA,
+//                   act kept in shared memory, phase 3 over every H chunk of
+//                   the stripe and partial sums reduced across stripes.
+//   SPLIT (mode 1)  job A = (M-tile, I-stripe): phases 1-2, act -> L2-resident
+//                   global buffer, then a release on done[M-tile];
+//                   job B = (M-tile, H-chunk): phase 3 over the full I, gated
+//                   by an acquire on done[M-tile] == #stripes.  More, smaller
+//                   jobs (better SM fill at decode sizes) and one reduction
+//                   per assignment instead of one per stripe.
 //
 // Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM
-// allocator, w3 spare, w4-7 epilogue (one TMEM lane = one weight row each).
-// The tile config (bm, ttn, stg, group_m) is read from device memory, so the
-// dispatcher's choice needs no host round trip.
+// allocator, w3 spare, w4-7 epilogue (TMEM lane == weight row).
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -30,22 +41,36 @@
 namespace ramp {
 
 constexpr int kMoeThreads = 256;
-constexpr int kCtrlBytes = 4096;        // barriers + per-tile metadata
-constexpr int kSubTileBytes = 128 * 128;  // 128 rows x 64 bf16 (one SW128 box)
+constexpr int kCtrlBytes = 4096;                  // barriers + per-job metadata
+constexpr int kStageBytesScatter = 16 * 128 * 4;  // 16 tokens x 128 rows fp32 transpose buffer
+constexpr int kSubTileBytes = 128 * 128;          // 128 rows x 64 bf16 (one SW128 box)
 constexpr int kMaxStages = 8;
-constexpr int kSmemLimit = 232448;      // 227 KB opt-in per CTA on sm_100
+constexpr int kSmemLimit = 232448;                // 227 KB opt-in per CTA on sm_100
+constexpr int kModeFused = 0;
+constexpr int kModeSplit = 1;
 
 __host__ __device__ inline int bm_mma(int bm) { return bm <= 16 ? 16 : (bm + 15) / 16 * 16; }
 __host__ __device__ inline int stage_bytes(int bm, int ttn) {
   const int raw = (ttn / 128) * kSubTileBytes + bm_mma(bm) * 128;
   return (raw + 1023) / 1024 * 1024;
 }
-__host__ __device__ inline int act_bytes(int bm, int ttn) { return bm_mma(bm) * ttn; }
-// Total dynamic shared memory (including 1 KB alignment slack); the B200
-// counterpart of smem_usage() (ramp/config_space.py:122-124).
-__host__ __device__ inline int moe_smem_bytes(int bm, int ttn, int stg) {
-  return 1024 + kCtrlBytes + stg * stage_bytes(bm, ttn) + act_bytes(bm, ttn);
+__host__ __device__ inline int act_bytes(int bm, int ttn, int mode) {
+  return mode == kModeFused ? bm_mma(bm) * ttn : 0;
 }
+// Dynamic shared memory of one config (the B200 counterpart of smem_usage(),
+// ramp/config_space.py:122-124): 1 KB alignment slack, control block,
+// scatter transpose buffer, stg ring stages, fused mode's bf16 act tile.
+__host__ __device__ inline int moe_smem_bytes(int bm, int ttn, int stg, int mode) {
+  return 1024 + kCtrlBytes + kStageBytesScatter + stg * stage_bytes(bm, ttn) + act_bytes(bm, ttn, mode);
+}
+__host__ __device__ inline int bmn_index(int bmN) { return bmN <= 16 ? 0 : bmN <= 32 ? 1 : bmN <= 64 ? 2 : 3; }
+
+struct MoeMaps {
+  CUtensorMap xs[4];   // x_sorted [rows, H],  box {64, 16/32/64/128}
+  CUtensorMap act[4];  // act_g    [rows, I],  box {64, 16/32/64/128}
+  CUtensorMap w1[2];   // W1 as [2E, I, H],    box {64, n_i, 2} for n_i = 128 / 256
+  CUtensorMap w2;      // W2 as [E*H, I],      box {64, 128}
+};
 
 struct MoeParams {
   const int32_t* ctrl;         // route output: [0] cfg, [1] n_post_pad, [2] n_mtiles
@@ -53,76 +78,157 @@ struct MoeParams {
   const int32_t* tile_expert;  // [n_mtiles]
   const float* topk_w;         // [S*top_k]
   float* out_acc;              // [S, H] fp32, zeroed by the route kernel
+  __nv_bfloat16* act_g;        // [rows, I] split-mode intermediate
+  int* done;                   // [n_mtiles] split-mode phase-A completion counters (zeroed by route)
   ramp_table_t table;
   int32_t S, H, I, E, top_k, n_assign;
+  unsigned long long* prof;    // optional per-CTA cycle counters [gridDim][16] (diagnostics)
+};
+
+// Diagnostic counters (cycles, per CTA) written when MoeParams::prof != null.
+enum ProfSlot {
+  kPrWaitEmpty = 0, kPrIssue, kMmaWaitFull, kMmaWaitAcc, kMmaWaitAct, kEpiWaitAcc, kEpiSwiglu,
+  kEpiWaitChunk, kEpiScatter, kTotal, kItems, kEpiMeta, kPrWaitDep, kNumProf = 16
+};
+
+struct ProfClock {
+  unsigned long long t;
+  __device__ __forceinline__ void start() { t = clock64(); }
+  __device__ __forceinline__ unsigned long long lap() {
+    const unsigned long long n = clock64();
+    const unsigned long long d = n - t;
+    t = n;
+    return d;
+  }
 };
 
 struct CtrlSmem {
   uint64_t full[kMaxStages];
   uint64_t empty[kMaxStages];
-  uint64_t acc1_full;
-  uint64_t act_full;
-  uint64_t acc3_full[2];
-  uint64_t acc3_empty[2];
+  uint64_t acc_full[2];    // MMA -> epilogue, per TMEM region
+  uint64_t acc_empty[2];   // epilogue -> MMA, per TMEM region (split mode)
+  uint64_t act_full;       // fused: act tile written
+  uint64_t chunk_full[2];  // fused: phase-3 chunk accumulators
+  uint64_t chunk_empty[2];
   uint32_t tmem_base;
-  int32_t prod_rows[kMaxBm];
-  int32_t epi_tok[kMaxBm];
-  float epi_w[kMaxBm];
+  int32_t epi_tok[128];
+  float epi_w[128];
 };
 static_assert(sizeof(CtrlSmem) <= kCtrlBytes, "control block overflow");
 
+// Job decoding, identical in every role.
+struct Job {
+  int kind;  // 0 = phase 1(+2) of (m, s) [fused: +phase 3], 1 = split phase 3 of (m, hc)
+  int m, s, hc;
+};
+
+struct Geometry {
+  int mode, bm, bmN, nA, n_i, stripes, n_mtiles, n_hc, kbH, kbI, nJobA, total, group_m;
+  bool dbl;  // TMEM double buffering across jobs (split mode, fits in 256 columns)
+  __device__ __forceinline__ Job job(int j) const {
+    Job r;
+    if (j < nJobA) {
+      r.kind = 0;
+      r.m = group_m ? (j % n_mtiles) : (j / stripes);
+      r.s = group_m ? (j / n_mtiles) : (j % stripes);
+      r.hc = 0;
+    } else {
+      const int jj = j - nJobA;
+      r.kind = 1;
+      r.m = group_m ? (jj % n_mtiles) : (jj / n_hc);
+      r.hc = group_m ? (jj / n_mtiles) : (jj % n_hc);
+      r.s = 0;
+    }
+    return r;
+  }
+};
+
 __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + __expf(-g)) * u; }
 
+// Scatter-reduce 16 token columns of a [128 x bm] TMEM accumulator block into
+// out (fp32): scale by the top-k weight, transpose through shared memory so
+// each lane owns 4 consecutive rows, then one 16-byte vector reduction.
+__device__ __forceinline__ void scatter16(const float (&v)[16], int j0, int bm, int et, float* tbuf,
+                                          const CtrlSmem& cs, float* out, int H, int h0) {
+#pragma unroll
+  for (int q = 0; q < 16; ++q) tbuf[q * 128 + et] = v[q] * cs.epi_w[j0 + q < bm ? j0 + q : 0];
+  named_bar_sync(1, 128);
+  const int w = et >> 5, l = et & 31;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int q = w * 4 + r;
+    const int j = j0 + q;
+    if (j < bm) {
+      const int tok = cs.epi_tok[j];
+      if (tok >= 0) {
+        const float4 x = *reinterpret_cast<const float4*>(tbuf + q * 128 + 4 * l);
+        red_add_v4_f32(out + static_cast<size_t>(tok) * H + h0 + 4 * l, x);
+      }
+    }
+  }
+  named_bar_sync(1, 128);
+}
+
 __global__ void __launch_bounds__(kMoeThreads, 1)
-    fused_moe_bf16_kernel(const __grid_constant__ CUtensorMap tm_x,
-                          const __grid_constant__ CUtensorMap tm_w1,
-                          const __grid_constant__ CUtensorMap tm_w2, const MoeParams p) {
+    fused_moe_bf16_kernel(const __grid_constant__ MoeMaps maps, const MoeParams p) {
   extern __shared__ unsigned char smem_raw[];
-  // 1 KB alignment for the SW128 operand tiles.
   const uint32_t raw_addr = smem_u32(smem_raw);
-  const uint32_t base_addr = (raw_addr + 1023u) & ~1023u;
+  const uint32_t base_addr = (raw_addr + 1023u) & ~1023u;  // SW128 tiles need 1 KB alignment
   unsigned char* base = smem_raw + (base_addr - raw_addr);
   CtrlSmem& cs = *reinterpret_cast<CtrlSmem*>(base);
-  const uint32_t ring_addr = base_addr + kCtrlBytes;
+  float* tbuf = reinterpret_cast<float*>(base + kCtrlBytes);
+  const uint32_t ring_addr = base_addr + kCtrlBytes + kStageBytesScatter;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  // --- runtime tile config chosen by the dispatcher
+  // --- runtime tile config chosen by the dispatcher (no host round trip)
   const int cfg = p.ctrl[0];
   const int n_post_pad = p.ctrl[1];
-  const int bm = p.table.bm[cfg];
-  const int ttn = p.table.ttn[cfg];
   const int stg = p.table.stg[cfg];
-  const int group_m = p.table.group_m[cfg];
-  const int bmN = bm_mma(bm);
-  const int nA = ttn / 128;       // M=128 MMA tiles per phase-1 k-block (gate + up halves)
-  const int n_i = ttn / 2;        // intermediate features per stripe
-  const int stripes = p.I / n_i;
-  const int n_mtiles = n_post_pad / bm;
-  const int total = n_mtiles * stripes;
-  const int kb1 = p.H / 64;       // phase-1 k-blocks
-  const int n_hc = p.H / 128;     // phase-3 output chunks
-  const int sbytes = stage_bytes(bm, ttn);
+  Geometry G;
+  G.mode = p.table.mode ? p.table.mode[cfg] : kModeFused;
+  G.bm = p.table.bm[cfg];
+  G.bmN = bm_mma(G.bm);
+  const int ttn = p.table.ttn[cfg];
+  G.nA = ttn / 128;
+  G.n_i = ttn / 2;
+  G.stripes = p.I / G.n_i;
+  G.n_mtiles = n_post_pad / G.bm;
+  G.n_hc = p.H / 128;
+  G.kbH = p.H / 64;
+  G.kbI = p.I / 64;
+  G.group_m = p.table.group_m[cfg];
+  G.nJobA = G.n_mtiles * G.stripes;
+  G.total = G.nJobA + (G.mode == kModeSplit ? G.n_mtiles * G.n_hc : 0);
+  G.dbl = G.mode == kModeSplit && G.nA * G.bmN <= 256;
+  const int bmN = G.bmN, nA = G.nA;
+  const int sbytes = stage_bytes(G.bm, ttn);
   const uint32_t act_addr = ring_addr + stg * sbytes;
-  unsigned char* act_ptr = base + kCtrlBytes + stg * sbytes;
+  unsigned char* act_ptr = base + kCtrlBytes + kStageBytesScatter + stg * sbytes;
+  const CUtensorMap* tm_xs = &maps.xs[bmn_index(bmN)];
+  const CUtensorMap* tm_act = &maps.act[bmn_index(bmN)];
+  const CUtensorMap* tm_w1 = &maps.w1[G.n_i == 256 ? 1 : 0];
+  const CUtensorMap* tm_w2 = &maps.w2;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tm_x);
-    tma_prefetch_desc(&tm_w1);
-    tma_prefetch_desc(&tm_w2);
+    tma_prefetch_desc(tm_xs);
+    tma_prefetch_desc(tm_w1);
+    tma_prefetch_desc(tm_w2);
+    if (G.mode == kModeSplit) tma_prefetch_desc(tm_act);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < stg; ++s) {
       mbar_init(smem_u32(&cs.full[s]), 1);
       mbar_init(smem_u32(&cs.empty[s]), 1);
     }
-    mbar_init(smem_u32(&cs.acc1_full), 1);
-    mbar_init(smem_u32(&cs.act_full), 128);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(smem_u32(&cs.acc3_full[b]), 1);
-      mbar_init(smem_u32(&cs.acc3_empty[b]), 128);
+      mbar_init(smem_u32(&cs.acc_full[b]), 1);
+      mbar_init(smem_u32(&cs.acc_empty[b]), 128);
+      mbar_init(smem_u32(&cs.chunk_full[b]), 1);
+      mbar_init(smem_u32(&cs.chunk_empty[b]), 128);
     }
+    mbar_init(smem_u32(&cs.act_full), 128);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(smem_u32(&cs.tmem_base));
@@ -133,175 +239,298 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
 
   if (warp == 0) {
     // ============================ TMA producer ============================
-    const uint64_t pol_w = policy_evict_first();
-    const uint64_t pol_x = policy_evict_last();
-    uint32_t stage = 0, phase = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
-      const int m = group_m ? (w % n_mtiles) : (w / stripes);
-      const int s = group_m ? (w / n_mtiles) : (w % stripes);
-      const int e = p.tile_expert[m];
-      const int row0 = m * bm;
-      for (int j = lane; j < bmN; j += 32) {
-        int tok = 0;
-        if (j < bm) {
-          const int a = p.sorted_ids[row0 + j];
-          if (a < p.n_assign) tok = a / p.top_k;
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      uint32_t stage = 0, phase = 0;
+      unsigned long long c_wait = 0, c_issue = 0, c_dep = 0, t_begin = clock64();
+      ProfClock pc;
+      pc.start();
+      auto next = [&]() {
+        if (++stage == (uint32_t)stg) {
+          stage = 0;
+          phase ^= 1;
         }
-        cs.prod_rows[j] = tok;
-      }
-      __syncwarp();
-      if (lane == 0) {
-        const int gate_row = e * 2 * p.I + s * n_i;
-        const int up_row = gate_row + p.I;
-        const uint32_t tx1 = nA * kSubTileBytes + bmN * 128;
-        for (int kb = 0; kb < kb1; ++kb) {
-          const uint32_t full = smem_u32(&cs.full[stage]);
-          mbar_wait(smem_u32(&cs.empty[stage]), phase ^ 1);
-          mbar_arrive_expect_tx(full, tx1);
-          const uint32_t sb = ring_addr + stage * sbytes;
-          for (int t = 0; t < nA / 2; ++t) {
-            tma_load_2d(sb + t * kSubTileBytes, &tm_w1, full, kb * 64, gate_row + t * 128, pol_w);
-            tma_load_2d(sb + (nA / 2 + t) * kSubTileBytes, &tm_w1, full, kb * 64, up_row + t * 128,
-                        pol_w);
+      };
+      auto acquire = [&](uint32_t tx) -> uint32_t {
+        c_issue += pc.lap();
+        mbar_wait(smem_u32(&cs.empty[stage]), phase ^ 1);
+        c_wait += pc.lap();
+        const uint32_t full = smem_u32(&cs.full[stage]);
+        mbar_arrive_expect_tx(full, tx);
+        return full;
+      };
+      for (int j = blockIdx.x; j < G.total; j += gridDim.x) {
+        const Job jb = G.job(j);
+        const int e = p.tile_expert[jb.m];
+        const int row0 = jb.m * G.bm;
+        if (jb.kind == 0) {
+          const uint32_t tx1 = nA * kSubTileBytes + bmN * 128;
+          for (int kb = 0; kb < G.kbH; ++kb) {
+            const uint32_t full = acquire(tx1);
+            const uint32_t sb = ring_addr + stage * sbytes;
+            tma_load_3d(sb, tm_w1, full, kb * 64, jb.s * G.n_i, 2 * e, pol_w);
+            tma_load_2d(sb + nA * kSubTileBytes, tm_xs, full, kb * 64, row0, pol_x);
+            next();
           }
-          const uint32_t xb = sb + nA * kSubTileBytes;
-          for (int r = 0; r < bmN; r += 4)
-            tma_gather4(xb + r * 128, &tm_x, full, kb * 64, cs.prod_rows[r], cs.prod_rows[r + 1],
-                        cs.prod_rows[r + 2], cs.prod_rows[r + 3], pol_x);
-          if (++stage == (uint32_t)stg) { stage = 0; phase ^= 1; }
-        }
-        const uint32_t tx3 = nA * kSubTileBytes;  // n_i/64 == nA boxes of 128 rows
-        for (int hc = 0; hc < n_hc; ++hc) {
-          const uint32_t full = smem_u32(&cs.full[stage]);
-          mbar_wait(smem_u32(&cs.empty[stage]), phase ^ 1);
-          mbar_arrive_expect_tx(full, tx3);
-          const uint32_t sb = ring_addr + stage * sbytes;
-          for (int kk = 0; kk < nA; ++kk)
-            tma_load_2d(sb + kk * kSubTileBytes, &tm_w2, full, s * n_i + kk * 64, e * p.H + hc * 128,
-                        pol_w);
-          if (++stage == (uint32_t)stg) { stage = 0; phase ^= 1; }
+          if (G.mode == kModeFused) {
+            for (int hc = 0; hc < G.n_hc; ++hc) {
+              const uint32_t full = acquire(nA * kSubTileBytes);  // n_i/64 == nA boxes
+              const uint32_t sb = ring_addr + stage * sbytes;
+              for (int kk = 0; kk < nA; ++kk)
+                tma_load_2d(sb + kk * kSubTileBytes, tm_w2, full, jb.s * G.n_i + kk * 64, e * p.H + hc * 128,
+                            pol_w);
+              next();
+            }
+          }
+        } else {
+          // Split phase 3: weights stream immediately; the act rows wait for
+          // every phase-1 job of this M-tile (release/acquire on done[m]).
+          const uint32_t tx = kSubTileBytes + bmN * 128;
+          uint32_t pend_stage[kMaxStages], pend_bar[kMaxStages];
+          int npend = 0;
+          bool ready = false;
+          for (int kb = 0; kb < G.kbI; ++kb) {
+            const uint32_t full = acquire(tx);
+            const uint32_t sb = ring_addr + stage * sbytes;
+            tma_load_2d(sb, tm_w2, full, kb * 64, e * p.H + jb.hc * 128, pol_w);
+            if (ready) {
+              tma_load_2d(sb + kSubTileBytes, tm_act, full, kb * 64, row0, pol_x);
+            } else {
+              pend_stage[npend] = sb;
+              pend_bar[npend] = full;
+              ++npend;
+              if (npend == stg || kb == G.kbI - 1) {
+                pc.lap();
+                while (ld_acquire_gpu(p.done + jb.m) < G.stripes) __nanosleep(64);
+                fence_proxy_async_global();
+                c_dep += pc.lap();
+                ready = true;
+                for (int q = 0; q < npend; ++q)
+                  tma_load_2d(pend_stage[q] + kSubTileBytes, tm_act, pend_bar[q], (kb - npend + 1 + q) * 64,
+                              row0, pol_x);
+              }
+            }
+            next();
+          }
         }
       }
-      __syncwarp();
+      if (p.prof) {
+        unsigned long long* pr = p.prof + blockIdx.x * kNumProf;
+        pr[kPrWaitEmpty] = c_wait;
+        pr[kPrIssue] = c_issue + pc.lap();
+        pr[kPrWaitDep] = c_dep;
+        pr[kTotal] = clock64() - t_begin;
+      }
     }
+    __syncwarp();
   } else if (warp == 1) {
     // ============================ MMA issuer =============================
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16(128, bmN);
-      uint32_t stage = 0, phase = 0, tile_iter = 0;
-      uint32_t uses[2] = {0, 0};
-      for (int w = blockIdx.x; w < total; w += gridDim.x) {
-        // acc1 aliases the acc3 buffers: wait until the epilogue drained them
-        for (int b = 0; b < 2; ++b)
-          if (uses[b]) mbar_wait(smem_u32(&cs.acc3_empty[b]), (uses[b] - 1) & 1);
+      uint32_t stage = 0, phase = 0, jl = 0, act_iter = 0;
+      uint32_t acc_cnt[2] = {0, 0}, chunk_cnt[2] = {0, 0};
+      unsigned long long c_full = 0, c_acc = 0, c_act = 0, items = 0;
+      ProfClock pc;
+      pc.start();
+      auto wait_full = [&]() -> uint32_t {
+        pc.lap();
+        mbar_wait(smem_u32(&cs.full[stage]), phase);
+        c_full += pc.lap();
         tc_fence_after();
-        for (int kb = 0; kb < kb1; ++kb) {
-          mbar_wait(smem_u32(&cs.full[stage]), phase);
-          tc_fence_after();
-          const uint32_t sb = ring_addr + stage * sbytes;
-          const uint32_t xb = sb + nA * kSubTileBytes;
-          for (int t = 0; t < nA; ++t) {
+        return ring_addr + stage * sbytes;
+      };
+      auto release = [&]() {
+        mma_commit(smem_u32(&cs.empty[stage]));
+        if (++stage == (uint32_t)stg) {
+          stage = 0;
+          phase ^= 1;
+        }
+      };
+      for (int j = blockIdx.x; j < G.total; j += gridDim.x, ++jl) {
+        ++items;
+        const Job jb = G.job(j);
+        const int r = G.dbl ? (jl & 1) : 0;
+        const uint32_t acc = tmem + r * 256;
+        pc.lap();
+        if (G.mode == kModeSplit) {
+          if (acc_cnt[r]) mbar_wait(smem_u32(&cs.acc_empty[r]), (acc_cnt[r] - 1) & 1);
+        } else {
+          for (int b = 0; b < 2; ++b)
+            if (chunk_cnt[b]) mbar_wait(smem_u32(&cs.chunk_empty[b]), (chunk_cnt[b] - 1) & 1);
+        }
+        c_acc += pc.lap();
+        tc_fence_after();
+        if (jb.kind == 0) {
+          for (int kb = 0; kb < G.kbH; ++kb) {
+            const uint32_t sb = wait_full();
+            const uint32_t xb = sb + nA * kSubTileBytes;
+            for (int t = 0; t < nA; ++t) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              mma_bf16(tmem + t * bmN, sw128_kmajor_desc(sb + t * kSubTileBytes + k * 32),
-                       sw128_kmajor_desc(xb + k * 32), idesc, (kb | k) != 0);
+              for (int k = 0; k < 4; ++k)
+                mma_bf16(acc + t * bmN, sw128_kmajor_desc(sb + t * kSubTileBytes + k * 32),
+                         sw128_kmajor_desc(xb + k * 32), idesc, (kb | k) != 0);
+            }
+            release();
+          }
+          mma_commit(smem_u32(&cs.acc_full[r]));
+          ++acc_cnt[r];
+          if (G.mode == kModeFused) {
+            pc.lap();
+            mbar_wait(smem_u32(&cs.act_full), act_iter & 1);
+            c_act += pc.lap();
+            ++act_iter;
+            tc_fence_after();
+            for (int hc = 0; hc < G.n_hc; ++hc) {
+              const int b = hc & 1;
+              pc.lap();
+              if (chunk_cnt[b]) mbar_wait(smem_u32(&cs.chunk_empty[b]), (chunk_cnt[b] - 1) & 1);
+              c_acc += pc.lap();
+              const uint32_t sb = wait_full();
+              for (int kk = 0; kk < nA; ++kk) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  mma_bf16(tmem + b * bmN, sw128_kmajor_desc(sb + kk * kSubTileBytes + k * 32),
+                           sw128_kmajor_desc(act_addr + kk * bmN * 128 + k * 32), idesc, (kk | k) != 0);
+              }
+              release();
+              mma_commit(smem_u32(&cs.chunk_full[b]));
+              ++chunk_cnt[b];
             }
           }
-          mma_commit(smem_u32(&cs.empty[stage]));
-          if (++stage == (uint32_t)stg) { stage = 0; phase ^= 1; }
-        }
-        mma_commit(smem_u32(&cs.acc1_full));
-        mbar_wait(smem_u32(&cs.act_full), tile_iter & 1);
-        tc_fence_after();
-        for (int hc = 0; hc < n_hc; ++hc) {
-          const int b = hc & 1;
-          if (uses[b]) mbar_wait(smem_u32(&cs.acc3_empty[b]), (uses[b] - 1) & 1);
-          mbar_wait(smem_u32(&cs.full[stage]), phase);
-          tc_fence_after();
-          const uint32_t sb = ring_addr + stage * sbytes;
-          for (int kk = 0; kk < nA; ++kk) {
+        } else {
+          for (int kb = 0; kb < G.kbI; ++kb) {
+            const uint32_t sb = wait_full();
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              mma_bf16(tmem + b * bmN, sw128_kmajor_desc(sb + kk * kSubTileBytes + k * 32),
-                       sw128_kmajor_desc(act_addr + kk * bmN * 128 + k * 32), idesc, (kk | k) != 0);
-            }
+            for (int k = 0; k < 4; ++k)
+              mma_bf16(acc, sw128_kmajor_desc(sb + k * 32), sw128_kmajor_desc(sb + kSubTileBytes + k * 32),
+                       idesc, (kb | k) != 0);
+            release();
           }
-          mma_commit(smem_u32(&cs.empty[stage]));
-          mma_commit(smem_u32(&cs.acc3_full[b]));
-          ++uses[b];
-          if (++stage == (uint32_t)stg) { stage = 0; phase ^= 1; }
+          mma_commit(smem_u32(&cs.acc_full[r]));
+          ++acc_cnt[r];
         }
-        ++tile_iter;
+      }
+      if (p.prof) {
+        unsigned long long* pr = p.prof + blockIdx.x * kNumProf;
+        pr[kMmaWaitFull] = c_full;
+        pr[kMmaWaitAcc] = c_acc;
+        pr[kMmaWaitAct] = c_act;
+        pr[kItems] = items;
       }
     }
     __syncwarp();
   } else if (warp >= 4) {
     // ============================ epilogue ===============================
-    const int et = threadIdx.x - 128;                       // TMEM lane == weight row
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>(et & ~31) << 16);
-    uint32_t tile_iter = 0;
-    uint32_t uses[2] = {0, 0};
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
-      const int m = group_m ? (w % n_mtiles) : (w / stripes);
-      const int row0 = m * bm;
-      named_bar_sync(1, 128);
-      for (int j = et; j < bm; j += 128) {
-        const int a = p.sorted_ids[row0 + j];
+    const int et = threadIdx.x - 128;  // TMEM lane == weight row of the 128-row MMA tile
+    const uint32_t lane_off = static_cast<uint32_t>(et & ~31) << 16;
+    uint32_t jl = 0, acc_cnt[2] = {0, 0}, chunk_cnt[2] = {0, 0};
+    unsigned long long c_meta = 0, c_wacc = 0, c_swiglu = 0, c_wchunk = 0, c_scatter = 0;
+    ProfClock pc;
+    pc.start();
+    for (int j = blockIdx.x; j < G.total; j += gridDim.x, ++jl) {
+      const Job jb = G.job(j);
+      const int r = G.dbl ? (jl & 1) : 0;
+      const uint32_t acc = tmem + lane_off + r * 256;
+      const int row0 = jb.m * G.bm;
+      pc.lap();
+      named_bar_sync(1, 128);  // previous job's readers of epi_tok / epi_w are done
+      for (int q = et; q < G.bm; q += 128) {
+        const int a = p.sorted_ids[row0 + q];
         const bool valid = a < p.n_assign;
-        cs.epi_tok[j] = valid ? a / p.top_k : -1;
-        cs.epi_w[j] = valid ? __ldg(p.topk_w + a) : 0.0f;
+        cs.epi_tok[q] = valid ? a / p.top_k : -1;
+        cs.epi_w[q] = valid ? __ldg(p.topk_w + a) : 0.0f;
       }
       named_bar_sync(1, 128);
-
-      // ---- phase 2: SwiGLU into the SW128 K-major act tile
-      mbar_wait(smem_u32(&cs.acc1_full), tile_iter & 1);
+      c_meta += pc.lap();
+      mbar_wait(smem_u32(&cs.acc_full[r]), acc_cnt[r] & 1);
+      ++acc_cnt[r];
+      c_wacc += pc.lap();
       tc_fence_after();
-      for (int th = 0; th < nA / 2; ++th) {
-        const int f = th * 128 + et;  // feature within the stripe == K index of phase 3
-        unsigned char* kblk = act_ptr + (f >> 6) * bmN * 128;
-        const int chunk = (f & 63) >> 3;
-        const int within = (f & 7) * 2;
-        for (int j0 = 0; j0 < bmN; j0 += 16) {
-          float g[16], u[16];
-          tmem_ld16(lane_base + th * bmN + j0, g);
-          tmem_ld16(lane_base + (nA / 2 + th) * bmN + j0, u);
-          tmem_ld_wait();
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int j = j0 + q;
-            const __nv_bfloat16 v = __float2bfloat16(silu_mul(g[q], u[q]));
-            *reinterpret_cast<__nv_bfloat16*>(kblk + j * 128 + ((chunk ^ (j & 7)) << 4) + within) = v;
-          }
-        }
-      }
-      tc_fence_before();
-      fence_proxy_async_smem();
-      mbar_arrive(smem_u32(&cs.act_full));
 
-      // ---- phase 3 epilogue: weighted scatter-reduce of each H chunk
-      for (int hc = 0; hc < n_hc; ++hc) {
-        const int b = hc & 1;
-        mbar_wait(smem_u32(&cs.acc3_full[b]), uses[b] & 1);
-        tc_fence_after();
-        float* orow = p.out_acc + hc * 128 + et;
-        for (int j0 = 0; j0 < bm; j0 += 16) {
-          float v[16];
-          tmem_ld16(lane_base + b * bmN + j0, v);
-          tmem_ld_wait();
+      if (jb.kind == 0) {
+        // ---- phase 2: SwiGLU.  Thread et owns features f = th*128 + et.
+        for (int th = 0; th < nA / 2; ++th) {
+          const int f = th * 128 + et;
+          for (int j0 = 0; j0 < bmN; j0 += 16) {
+            float g[16], u[16];
+            tmem_ld16(acc + th * bmN + j0, g);
+            tmem_ld16(acc + (nA / 2 + th) * bmN + j0, u);
+            tmem_ld_wait();
+            if (G.mode == kModeFused) {
+              // bf16 act tile in the SW128 K-major layout phase 3 reads
+              unsigned char* kblk = act_ptr + (f >> 6) * bmN * 128;
+              const int chunk = (f & 63) >> 3, within = (f & 7) * 2;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int j = j0 + q;
-            if (j < bm) {
-              const int tok = cs.epi_tok[j];
-              if (tok >= 0) red_add_f32(orow + static_cast<size_t>(tok) * p.H, v[q] * cs.epi_w[j]);
+              for (int q = 0; q < 16; ++q) {
+                const int jj = j0 + q;
+                *reinterpret_cast<__nv_bfloat16*>(kblk + jj * 128 + ((chunk ^ (jj & 7)) << 4) + within) =
+                    __float2bfloat16(silu_mul(g[q], u[q]));
+              }
+            } else {
+              __nv_bfloat16* dst = p.act_g + static_cast<size_t>(row0 + j0) * p.I + jb.s * G.n_i + f;
+#pragma unroll
+              for (int q = 0; q < 16; ++q)
+                if (j0 + q < G.bm) dst[static_cast<size_t>(q) * p.I] = __float2bfloat16(silu_mul(g[q], u[q]));
             }
           }
         }
         tc_fence_before();
-        mbar_arrive(smem_u32(&cs.acc3_empty[b]));
-        ++uses[b];
+        if (G.mode == kModeFused) {
+          fence_proxy_async_smem();
+          mbar_arrive(smem_u32(&cs.act_full));
+          c_swiglu += pc.lap();
+          // ---- phase 3 (fused): every 128-row chunk of H for this stripe
+          for (int hc = 0; hc < G.n_hc; ++hc) {
+            const int b = hc & 1;
+            mbar_wait(smem_u32(&cs.chunk_full[b]), chunk_cnt[b] & 1);
+            c_wchunk += pc.lap();
+            tc_fence_after();
+            for (int j0 = 0; j0 < G.bm; j0 += 16) {
+              float v[16];
+              tmem_ld16(tmem + lane_off + b * bmN + j0, v);
+              tmem_ld_wait();
+              if (j0 + 16 >= G.bm) {
+                tc_fence_before();
+                mbar_arrive(smem_u32(&cs.chunk_empty[b]));
+              }
+              scatter16(v, j0, G.bm, et, tbuf, cs, p.out_acc, p.H, hc * 128);
+            }
+            ++chunk_cnt[b];
+            c_scatter += pc.lap();
+          }
+        } else {
+          mbar_arrive(smem_u32(&cs.acc_empty[r]));
+          // publish phase-1 completion of this (m, s) job for the phase-3 jobs
+          named_bar_sync(1, 128);
+          if (et == 0) {
+            __threadfence();
+            atomicAdd(p.done + jb.m, 1);
+          }
+          c_swiglu += pc.lap();
+        }
+      } else {
+        // ---- split phase 3 epilogue: one 128-row chunk, full I reduced in TMEM
+        for (int j0 = 0; j0 < G.bm; j0 += 16) {
+          float v[16];
+          tmem_ld16(acc + j0, v);
+          tmem_ld_wait();
+          if (j0 + 16 >= G.bm) {
+            tc_fence_before();
+            mbar_arrive(smem_u32(&cs.acc_empty[r]));
+          }
+          scatter16(v, j0, G.bm, et, tbuf, cs, p.out_acc, p.H, jb.hc * 128);
+        }
+        c_scatter += pc.lap();
       }
-      ++tile_iter;
+    }
+    if (p.prof && et == 0) {
+      unsigned long long* pr = p.prof + blockIdx.x * kNumProf;
+      pr[kEpiMeta] = c_meta;
+      pr[kEpiWaitAcc] = c_wacc;
+      pr[kEpiSwiglu] = c_swiglu;
+      pr[kEpiWaitChunk] = c_wchunk;
+      pr[kEpiScatter] = c_scatter;
     }
   }
 

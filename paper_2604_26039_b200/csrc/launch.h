@@ -16,7 +16,7 @@ struct RouteArgs {
   int32_t E;
   int32_t forced_cfg;
   ramp_table_t table;
-  int32_t* ctrl;         // [16]: cfg, n_post_pad, n_mtiles, n_eval, bad_ids
+  int32_t* ctrl;         // [16]: cfg, n_post_pad, n_mtiles, n_eval, bad_ids, ready flag, helpers done
   int32_t* hist_out;     // [E] or null
   int32_t* sorted_ids;   // [capacity]
   int32_t* tile_expert;  // [capacity]
@@ -26,6 +26,10 @@ struct RouteArgs {
   double* pred_out;      // [n_cfg] or null
   float* acc_clear;      // fp32 accumulator cleared by the helper blocks
   int64_t acc_clear_n;
+  int* done;             // split-mode per-M-tile counters, zeroed by block 0
+  const void* x;         // [S, H] bf16 tokens
+  void* x_sorted;        // [rows, H] bf16, gathered by the helper blocks (null: skip)
+  int32_t S, H, top_k;
 };
 
 cudaError_t launch_route(const RouteArgs& a, int zero_blocks, cudaStream_t stream);
@@ -45,11 +49,17 @@ struct MoeLaunch {
   const int32_t* tile_expert;
   float* out_acc;
   void* out;
+  void* x_sorted;   // [rows, H] bf16
+  void* act_g;      // [rows, I] bf16
+  int* done;        // [rows] split-mode counters
+  int64_t rows;     // capacity of x_sorted / act_g
   ramp_table_t table;
   int32_t S, H, I, E, top_k;
 };
 
+extern unsigned long long* g_prof_buffer;  // diagnostics, see ramp_set_profile_buffer
+
 cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const char** why);
-int64_t config_smem_bytes(int bm, int ttn, int stg);
+int64_t config_smem_bytes(int bm, int ttn, int stg, int mode);
 
 }  // namespace ramp

@@ -10,6 +10,8 @@
 
 namespace ramp {
 
+unsigned long long* g_prof_buffer = nullptr;
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                                    CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
@@ -29,24 +31,37 @@ static EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-// 2D bf16 row-major [rows, cols] map with a (box_cols x box_rows) SW128 box.
-static bool make_map_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows,
-                        uint32_t box_cols) {
+// bf16 tensor map with a 128-byte swizzle; dims/strides innermost first
+// (strides in bytes for dims 1..rank-1).
+static bool make_map(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides,
+                     const uint32_t* box) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {box_cols, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cuuint64_t d[3], st[2];
+  cuuint32_t b[3], e[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+  }
+  for (int i = 0; i < rank - 1; ++i) st[i] = strides[i];
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), d, st, b, e,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
-int64_t config_smem_bytes(int bm, int ttn, int stg) {
+// Row-major [rows, cols] bf16 matrix, (box_rows x 64) boxes.
+static bool make_map_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  const uint64_t dims[2] = {cols, rows};
+  const uint64_t strides[1] = {cols * 2};
+  const uint32_t box[2] = {64, box_rows};
+  return make_map(map, ptr, 2, dims, strides, box);
+}
+
+int64_t config_smem_bytes(int bm, int ttn, int stg, int mode) {
   if (bm < 1 || bm > kMaxBm || (ttn != 256 && ttn != 512) || stg < 1 || stg > kMaxStages) return 0;
-  const int b = moe_smem_bytes(bm, ttn, stg);
+  if (mode != kModeFused && mode != kModeSplit) return 0;
+  const int b = moe_smem_bytes(bm, ttn, stg, mode);
   return b <= kSmemLimit ? b : 0;
 }
 
@@ -69,10 +84,21 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
     if (err != cudaSuccess) return err;
     attr_set = true;
   }
-  alignas(64) CUtensorMap tm_x, tm_w1, tm_w2;
-  if (!make_map_2d(&tm_x, l.x, l.S, l.H, 1, 64) ||
-      !make_map_2d(&tm_w1, l.w1, (uint64_t)l.E * 2 * l.I, l.H, 128, 64) ||
-      !make_map_2d(&tm_w2, l.w2, (uint64_t)l.E * l.H, l.I, 128, 64)) {
+  alignas(64) MoeMaps maps;  // copied into the launch's parameter buffer
+  bool ok = true;
+  for (int i = 0; i < 4; ++i) {
+    ok = ok && make_map_2d(&maps.xs[i], l.x_sorted, l.rows, l.H, 16u << i);
+    ok = ok && make_map_2d(&maps.act[i], l.act_g, l.rows, l.I, 16u << i);
+  }
+  for (int i = 0; i < 2; ++i) {
+    // W1 viewed as [2E][I][H]: plane 2e = gate rows, 2e+1 = up rows of expert e
+    const uint64_t dims[3] = {(uint64_t)l.H, (uint64_t)l.I, 2ull * l.E};
+    const uint64_t strides[2] = {(uint64_t)l.H * 2, (uint64_t)l.I * l.H * 2};
+    const uint32_t box[3] = {64, 128u << i, 2};
+    ok = ok && ((l.I % (128 << i)) != 0 || make_map(&maps.w1[i], l.w1, 3, dims, strides, box));
+  }
+  ok = ok && make_map_2d(&maps.w2, l.w2, (uint64_t)l.E * l.H, l.I, 128);
+  if (!ok) {
     *why = "cuTensorMapEncodeTiled failed (alignment or driver entry point)";
     return cudaErrorInvalidValue;
   }
@@ -82,6 +108,8 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
   p.tile_expert = l.tile_expert;
   p.topk_w = l.topk_w;
   p.out_acc = l.out_acc;
+  p.act_g = static_cast<__nv_bfloat16*>(l.act_g);
+  p.done = l.done;
   p.table = l.table;
   p.S = l.S;
   p.H = l.H;
@@ -89,7 +117,8 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
   p.E = l.E;
   p.top_k = l.top_k;
   p.n_assign = l.S * l.top_k;
-  fused_moe_bf16_kernel<<<sm_count_cached(), kMoeThreads, kSmemLimit, stream>>>(tm_x, tm_w1, tm_w2, p);
+  p.prof = g_prof_buffer;
+  fused_moe_bf16_kernel<<<sm_count_cached(), kMoeThreads, kSmemLimit, stream>>>(maps, p);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   const int64_t n = (int64_t)l.S * l.H;

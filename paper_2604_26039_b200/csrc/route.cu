@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include "launch.h"
+#include "ptx.cuh"
 #include "route.cuh"
 
 namespace ramp {
@@ -18,16 +19,44 @@ struct RouteStatic {
 __global__ void __launch_bounds__(kRouteThreads, 1)
     route_kernel(const RouteArgs a) {
   if (blockIdx.x > 0) {
-    // Helper blocks clear the fp32 output accumulator of the megakernel.
+    // Helper blocks: clear the fp32 output accumulator, then (once block 0
+    // has published the alignment) gather the token rows into expert-sorted
+    // order so the megakernel can fetch a whole M-tile with one TMA box.
+    const int nh = gridDim.x - 1, hb = blockIdx.x - 1;
     float4* acc4 = reinterpret_cast<float4*>(a.acc_clear);
     const int64_t n4 = a.acc_clear_n / 4;
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int64_t i = (blockIdx.x - 1) * (int64_t)blockDim.x + threadIdx.x; i < n4;
-         i += (int64_t)(gridDim.x - 1) * blockDim.x)
-      acc4[i] = z;
-    for (int64_t i = n4 * 4 + (blockIdx.x - 1) * (int64_t)blockDim.x + threadIdx.x; i < a.acc_clear_n;
-         i += (int64_t)(gridDim.x - 1) * blockDim.x)
+    for (int64_t i = hb * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)nh * blockDim.x) acc4[i] = z;
+    for (int64_t i = n4 * 4 + hb * (int64_t)blockDim.x + threadIdx.x; i < a.acc_clear_n;
+         i += (int64_t)nh * blockDim.x)
       a.acc_clear[i] = 0.f;
+    if (a.x_sorted == nullptr) return;
+    if (threadIdx.x == 0)
+      while (ld_acquire_gpu(a.ctrl + 5) == 0) __nanosleep(128);
+    __syncthreads();
+    const int npp = __ldcg(a.ctrl + 1);
+    const int row_vec = a.H / 8;  // 16-byte vectors per row
+    const int4* xv = reinterpret_cast<const int4*>(a.x);
+    int4* dv = reinterpret_cast<int4*>(a.x_sorted);
+    const int gw = hb * kRouteWarps + (threadIdx.x >> 5), nw = nh * kRouteWarps, lane = threadIdx.x & 31;
+    for (int r = gw; r < npp; r += nw) {
+      const int asg = __ldcg(a.sorted_ids + r);
+      int4* d = dv + static_cast<int64_t>(r) * row_vec;
+      if (asg < a.n_assign) {
+        const int4* s = xv + static_cast<int64_t>(asg / a.top_k) * row_vec;
+        for (int c = lane; c < row_vec; c += 32) d[c] = __ldg(s + c);
+      } else {
+        for (int c = lane; c < row_vec; c += 32) d[c] = make_int4(0, 0, 0, 0);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // the last helper through resets the flag for the next call
+      if (atomicAdd(a.ctrl + 6, 1) == nh - 1) {
+        a.ctrl[6] = 0;
+        a.ctrl[5] = 0;
+      }
+    }
     return;
   }
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -47,10 +76,12 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   int32_t* n_post_pad = a.ctrl + 1;
   block_align(a.topk_ids, a.n_assign, a.E, bm, s, st.warp_tot, a.sorted_ids, a.tile_expert,
               n_post_pad);
+  const int npp = s.off[a.E];
   for (int e = threadIdx.x; e < a.E; e += blockDim.x)
     if (a.hist_out) a.hist_out[e] = s.hist[e];
+  if (a.done)
+    for (int m = threadIdx.x; m < npp / bm; m += blockDim.x) a.done[m] = 0;
   if (threadIdx.x == 0) {
-    const int npp = s.off[a.E];
     a.ctrl[0] = sel;
     a.ctrl[2] = npp / bm;
     a.ctrl[3] = n_eval;
@@ -61,6 +92,11 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
       a.sel_out[2] = npp / bm;
       a.sel_out[3] = n_eval;
     }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && a.x_sorted != nullptr && gridDim.x > 1) {
+    __threadfence();
+    st_release_gpu(a.ctrl + 5, 1);
   }
 }
 

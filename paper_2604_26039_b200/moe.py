@@ -38,6 +38,7 @@ class DeviceTable:
     stg: np.ndarray
     split_k: np.ndarray
     group_m: np.ndarray
+    mode: np.ndarray | None
     a: np.ndarray
     b: np.ndarray
     c: np.ndarray
@@ -53,7 +54,9 @@ class DeviceTable:
         n = len(self.bm)
         if n == 0:
             raise ValueError("dispatch table over an empty pool")
-        for name in ("ttn", "stg", "split_k", "group_m", "a", "b", "c", "d"):
+        if self.mode is None:
+            self.mode = np.zeros(n, dtype=np.int64)
+        for name in ("ttn", "stg", "split_k", "group_m", "mode", "a", "b", "c", "d"):
             if len(getattr(self, name)) != n:
                 raise ValueError(f"column {name} has length {len(getattr(self, name))}, expected {n}")
         ubm, ubm_index = np.unique(np.asarray(self.bm, dtype=np.int64), return_inverse=True)
@@ -62,7 +65,7 @@ class DeviceTable:
         i32 = dict(dtype=torch.int32, device=self.device)
         f64 = dict(dtype=torch.float64, device=self.device)
         t = self._tensors
-        for name in ("bm", "ttn", "stg", "split_k", "group_m"):
+        for name in ("bm", "ttn", "stg", "split_k", "group_m", "mode"):
             t[name] = torch.as_tensor(np.asarray(getattr(self, name), dtype=np.int32), **i32)
         t["ubm"] = torch.as_tensor(ubm.astype(np.int32), **i32)
         t["ubm_index"] = torch.as_tensor(ubm_index.astype(np.int32), **i32)
@@ -74,7 +77,7 @@ class DeviceTable:
         s.N = int(self.N)
         s.kappa_ok = int(bool(self.kappa_ok))
         s.sm_count = int(self.sm_count)
-        for name in ("bm", "ttn", "stg", "split_k", "group_m", "ubm", "ubm_index", "a", "b", "c", "d"):
+        for name in ("bm", "ttn", "stg", "split_k", "group_m", "mode", "ubm", "ubm_index", "a", "b", "c", "d"):
             setattr(s, name, t[name].data_ptr())
         self.struct = s
 
@@ -86,21 +89,23 @@ class DeviceTable:
         return ctypes.byref(self.struct)
 
 
-def workspace_bytes(S: int, H: int, E: int, top_k: int) -> int:
-    return int(_lib.load().ramp_fused_moe_workspace_size(S, H, E, top_k))
+def workspace_bytes(S: int, H: int, I: int, E: int, top_k: int) -> int:
+    return int(_lib.load().ramp_fused_moe_workspace_size(S, H, I, E, top_k))
 
 
 class Workspace:
-    """Reusable device workspace for `fused_moe` (route outputs + fp32 accumulator)."""
+    """Reusable device workspace for `fused_moe`: route outputs, the fp32
+    accumulator, expert-sorted tokens and split-mode activations.  Zeroed
+    once at allocation (it carries the route kernel's flags between calls)."""
 
-    def __init__(self, S: int, H: int, E: int, top_k: int, device="cuda"):
-        self.key = (S, H, E, top_k)
-        n = workspace_bytes(S, H, E, top_k)
-        self.buf = torch.empty(max(n, 256), dtype=torch.uint8, device=device)
+    def __init__(self, S: int, H: int, I: int, E: int, top_k: int, device="cuda"):
+        self.key = (S, H, I, E, top_k)
+        n = workspace_bytes(S, H, I, E, top_k)
+        self.buf = torch.zeros(max(n, 256), dtype=torch.uint8, device=device)
         self.sel = torch.zeros(4, dtype=torch.int32, device=device)
 
-    def fits(self, S: int, H: int, E: int, top_k: int) -> bool:
-        return self.buf.numel() >= workspace_bytes(S, H, E, top_k)
+    def fits(self, S: int, H: int, I: int, E: int, top_k: int) -> bool:
+        return self.buf.numel() >= workspace_bytes(S, H, I, E, top_k)
 
 
 def fused_moe(
@@ -145,8 +150,8 @@ def fused_moe(
         raise ValueError("topk_weights must be [S, top_k]")
     if out is None:
         out = torch.empty(S, H, dtype=torch.bfloat16, device=hidden_states.device)
-    if workspace is None or not workspace.fits(S, H, E, k):
-        workspace = Workspace(S, H, E, k, device=hidden_states.device)
+    if workspace is None or not workspace.fits(S, H, I, E, k):
+        workspace = Workspace(S, H, I, E, k, device=hidden_states.device)
     _lib.check(
         lib.ramp_fused_moe_bf16(
             hidden_states.data_ptr(), w1.data_ptr(), w2.data_ptr(), topk_weights.data_ptr(),

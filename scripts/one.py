@@ -19,11 +19,13 @@ ap.add_argument("--bm", type=int, default=64)
 ap.add_argument("--ttn", type=int, default=512)
 ap.add_argument("--stg", type=int, default=2)
 ap.add_argument("--gm", type=int, default=0)
+ap.add_argument("--mode", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--E", type=int, default=64)
 ap.add_argument("--H", type=int, default=2048)
 ap.add_argument("--I", type=int, default=1024)
 ap.add_argument("--k", type=int, default=8)
+ap.add_argument("--prof", action="store_true")
 a = ap.parse_args()
 E, H, I, k, S = a.E, a.H, a.I, a.k, a.S
 gen = torch.Generator(device="cuda").manual_seed(0)
@@ -33,13 +35,31 @@ pool = enumerate_b200_configs(MoeGeometry(name="p", E=E, N=2 * I, K=H, top_k=k))
 cols = pool.columns()
 n = len(pool)
 table = M.DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
-                      group_m=cols["group_m"].astype(np.int64), a=np.ones(n), b=np.zeros(n), c=np.zeros(n),
+                      group_m=cols["group_m"].astype(np.int64), mode=cols.get("mode"), a=np.ones(n), b=np.zeros(n), c=np.zeros(n),
                       d=np.zeros(n), N=2 * I, kappa_ok=False, sm_count=148)
-cfg = [c.id for c in pool if (c.bm, c.ttn, c.stg, int(c.group_m)) == (a.bm, a.ttn, a.stg, a.gm)][0]
+cfg = [c.id for c in pool if (c.bm, c.ttn, c.stg, int(c.group_m), c.mode) == (a.bm, a.ttn, a.stg, a.gm, a.mode)][0]
 x = torch.randn(S, H, device="cuda", generator=gen).to(torch.bfloat16)
 ids, w = topk(S, k, E, a.skew, gen)
-ws = M.Workspace(S, H, E, k)
+ws = M.Workspace(S, H, I, E, k)
 for _ in range(a.reps):
     out = M.fused_moe(x, w1, w2, w, ids, table, cfg, workspace=ws)
 torch.cuda.synchronize()
+if a.prof:
+    from paper_2604_26039_b200 import _lib
+    buf = torch.zeros(148 * 16, dtype=torch.int64, device="cuda")
+    _lib.load().ramp_set_profile_buffer(buf.data_ptr())
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    out = M.fused_moe(x, w1, w2, w, ids, table, cfg, workspace=ws)
+    e1.record()
+    torch.cuda.synchronize()
+    _lib.load().ramp_set_profile_buffer(None)
+    pr = buf.view(148, 16).cpu().numpy().astype(np.float64)
+    names = ["pr_wait_empty", "pr_issue", "mma_wait_full", "mma_wait_acc3", "mma_wait_act", "epi_wait_acc1",
+             "epi_swiglu", "epi_wait_acc3", "epi_scatter", "total", "items", "epi_meta"]
+    act = pr[:, 10] > 0
+    print(f"S={S} cfg bm={a.bm} ttn={a.ttn} stg={a.stg}: {e0.elapsed_time(e1)*1000:.1f} us (with profiling)")
+    for i, nme in enumerate(names):
+        col = pr[act, i]
+        print(f"  {nme:14s} mean {col.mean():12.0f}  max {col.max():12.0f}")
 print("ok", cfg, out.float().abs().mean().item())

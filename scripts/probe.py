@@ -49,7 +49,7 @@ def main():
     cols = pool.columns()
     n = len(pool)
     table = M.DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
-                          group_m=cols["group_m"].astype(np.int64), a=np.ones(n), b=np.zeros(n),
+                          group_m=cols["group_m"].astype(np.int64), mode=cols.get("mode"), a=np.ones(n), b=np.zeros(n),
                           c=np.zeros(n), d=np.zeros(n), N=2 * I, kappa_ok=False, sm_count=148)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     print(f"pool {n} configs", flush=True)
@@ -58,10 +58,10 @@ def main():
             x = torch.randn(S, H, device="cuda", generator=gen).to(torch.bfloat16)
             ids, w = topk(S, k, E, skew, gen)
             active = int((torch.bincount(ids.view(-1).long(), minlength=E) > 0).sum())
-            ws = M.Workspace(S, H, E, k)
+            ws = M.Workspace(S, H, I, E, k)
             out = torch.empty(S, H, dtype=torch.bfloat16, device="cuda")
             res = []
-            cfgs = list(pool) if a.all else [c for c in pool if c.stg in (2, 4) and not c.group_m]
+            cfgs = list(pool) if a.all else [c for c in pool if c.stg in (2, 4, 8) and not c.group_m]
             for c in cfgs:
                 for _ in range(2):
                     M.fused_moe(x, w1, w2, w, ids, table, c.id, out=out, workspace=ws)
@@ -80,11 +80,11 @@ def main():
             byte = active * 3 * H * I * 2
             best_t, best_c = res[0]
             print(f"S={S:4d} skew={skew:.1f} active={active:3d} best={best_t:8.1f}us "
-                  f"bm={best_c.bm} ttn={best_c.ttn} stg={best_c.stg} gm={int(best_c.group_m)} "
+                  f"bm={best_c.bm} ttn={best_c.ttn} stg={best_c.stg} gm={int(best_c.group_m)} mode={best_c.mode} "
                   f"GB/s={byte / best_t / 1e3:7.0f} TF/s={6 * S * k * H * I / best_t / 1e6:6.1f} "
                   f"worst={res[-1][0]:8.1f}us", flush=True)
             for t, c in res[:6]:
-                print(f"    {t:8.1f}us bm={c.bm} ttn={c.ttn} stg={c.stg} gm={int(c.group_m)}")
+                print(f"    {t:8.1f}us bm={c.bm} ttn={c.ttn} stg={c.stg} gm={int(c.group_m)} mode={c.mode}")
 
 
 if __name__ == "__main__":
