@@ -239,187 +239,222 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
 
   if (warp == 0) {
     // ============================ TMA producer ============================
-    if (lane == 0) {
-      const uint64_t pol_w = policy_evict_first();
-      const uint64_t pol_x = policy_evict_last();
-      uint32_t stage = 0, phase = 0;
-      unsigned long long c_wait = 0, c_issue = 0, c_dep = 0, t_begin = clock64();
-      ProfClock pc;
-      pc.start();
-      auto next = [&]() {
-        if (++stage == (uint32_t)stg) {
-          stage = 0;
-          phase ^= 1;
-        }
-      };
-      auto acquire = [&](uint32_t tx) -> uint32_t {
-        c_issue += pc.lap();
-        mbar_wait(smem_u32(&cs.empty[stage]), phase ^ 1);
-        c_wait += pc.lap();
-        const uint32_t full = smem_u32(&cs.full[stage]);
-        mbar_arrive_expect_tx(full, tx);
-        return full;
-      };
-      for (int j = blockIdx.x; j < G.total; j += gridDim.x) {
-        const Job jb = G.job(j);
-        const int e = p.tile_expert[jb.m];
-        const int row0 = jb.m * G.bm;
-        if (jb.kind == 0) {
-          const uint32_t tx1 = nA * kSubTileBytes + bmN * 128;
-          for (int kb = 0; kb < G.kbH; ++kb) {
-            const uint32_t full = acquire(tx1);
-            const uint32_t sb = ring_addr + stage * sbytes;
-            tma_load_3d(sb, tm_w1, full, kb * 64, jb.s * G.n_i, 2 * e, pol_w);
+    // The whole warp walks the schedule (so every operand is warp-uniform and
+    // stays on the uniform datapath); one elected lane issues each TMA.
+    const uint64_t pol_w = policy_evict_first();
+    const uint64_t pol_x = policy_evict_last();
+    const int u_stg = warp_uniform(stg), u_sbytes = warp_uniform(sbytes);
+    uint32_t stage = 0, phase = 0;
+    unsigned long long c_wait = 0, c_issue = 0, c_dep = 0, t_begin = clock64();
+    ProfClock pc;
+    pc.start();
+    auto next = [&]() {
+      if (++stage == (uint32_t)u_stg) {
+        stage = 0;
+        phase ^= 1;
+      }
+    };
+    auto acquire = [&]() {
+      c_issue += pc.lap();
+      mbar_wait(smem_u32(&cs.empty[stage]), phase ^ 1);
+      c_wait += pc.lap();
+    };
+    for (int j = blockIdx.x; j < G.total; j += gridDim.x) {
+      const Job jb = G.job(j);
+      const int e = warp_uniform(p.tile_expert[jb.m]);
+      const int row0 = jb.m * G.bm;
+      if (jb.kind == 0) {
+        const uint32_t tx1 = nA * kSubTileBytes + bmN * 128;
+        const int wrow = jb.s * G.n_i;
+        for (int kb = 0; kb < G.kbH; ++kb) {
+          acquire();
+          if (elect_one()) {
+            const uint32_t full = smem_u32(&cs.full[stage]);
+            const uint32_t sb = ring_addr + stage * u_sbytes;
+            mbar_arrive_expect_tx(full, tx1);
+            tma_load_3d(sb, tm_w1, full, kb * 64, wrow, 2 * e, pol_w);
             tma_load_2d(sb + nA * kSubTileBytes, tm_xs, full, kb * 64, row0, pol_x);
-            next();
           }
-          if (G.mode == kModeFused) {
-            for (int hc = 0; hc < G.n_hc; ++hc) {
-              const uint32_t full = acquire(nA * kSubTileBytes);  // n_i/64 == nA boxes
-              const uint32_t sb = ring_addr + stage * sbytes;
+          __syncwarp();
+          next();
+        }
+        if (G.mode == kModeFused) {
+          for (int hc = 0; hc < G.n_hc; ++hc) {
+            acquire();
+            if (elect_one()) {
+              const uint32_t full = smem_u32(&cs.full[stage]);
+              const uint32_t sb = ring_addr + stage * u_sbytes;
+              mbar_arrive_expect_tx(full, nA * kSubTileBytes);  // n_i/64 == nA boxes
               for (int kk = 0; kk < nA; ++kk)
                 tma_load_2d(sb + kk * kSubTileBytes, tm_w2, full, jb.s * G.n_i + kk * 64, e * p.H + hc * 128,
                             pol_w);
-              next();
             }
-          }
-        } else {
-          // Split phase 3: weights stream immediately; the act rows wait for
-          // every phase-1 job of this M-tile (release/acquire on done[m]).
-          const uint32_t tx = kSubTileBytes + bmN * 128;
-          uint32_t pend_stage[kMaxStages], pend_bar[kMaxStages];
-          int npend = 0;
-          bool ready = false;
-          for (int kb = 0; kb < G.kbI; ++kb) {
-            const uint32_t full = acquire(tx);
-            const uint32_t sb = ring_addr + stage * sbytes;
-            tma_load_2d(sb, tm_w2, full, kb * 64, e * p.H + jb.hc * 128, pol_w);
-            if (ready) {
-              tma_load_2d(sb + kSubTileBytes, tm_act, full, kb * 64, row0, pol_x);
-            } else {
-              pend_stage[npend] = sb;
-              pend_bar[npend] = full;
-              ++npend;
-              if (npend == stg || kb == G.kbI - 1) {
-                pc.lap();
-                while (ld_acquire_gpu(p.done + jb.m) < G.stripes) __nanosleep(64);
-                fence_proxy_async_global();
-                c_dep += pc.lap();
-                ready = true;
-                for (int q = 0; q < npend; ++q)
-                  tma_load_2d(pend_stage[q] + kSubTileBytes, tm_act, pend_bar[q], (kb - npend + 1 + q) * 64,
-                              row0, pol_x);
-              }
-            }
+            __syncwarp();
             next();
           }
         }
-      }
-      if (p.prof) {
-        unsigned long long* pr = p.prof + blockIdx.x * kNumProf;
-        pr[kPrWaitEmpty] = c_wait;
-        pr[kPrIssue] = c_issue + pc.lap();
-        pr[kPrWaitDep] = c_dep;
-        pr[kTotal] = clock64() - t_begin;
+      } else {
+        // Split phase 3: weights stream immediately; the act rows wait for
+        // every phase-1 job of this M-tile (release/acquire on done[m]).
+        const uint32_t tx = kSubTileBytes + bmN * 128;
+        const int wrow = e * p.H + jb.hc * 128;
+        int first_pending = 0, npend = 0;
+        bool ready = false;
+        for (int kb = 0; kb < G.kbI; ++kb) {
+          acquire();
+          if (elect_one()) {
+            const uint32_t full = smem_u32(&cs.full[stage]);
+            const uint32_t sb = ring_addr + stage * u_sbytes;
+            mbar_arrive_expect_tx(full, tx);
+            tma_load_2d(sb, tm_w2, full, kb * 64, wrow, pol_w);
+            if (ready) tma_load_2d(sb + kSubTileBytes, tm_act, full, kb * 64, row0, pol_x);
+          }
+          __syncwarp();
+          if (!ready) {
+            if (npend == 0) first_pending = kb;
+            ++npend;
+            if (npend == u_stg || kb == G.kbI - 1) {
+              pc.lap();
+              while (ld_acquire_gpu(p.done + jb.m) < G.stripes) __nanosleep(64);
+              fence_proxy_async_global();
+              c_dep += pc.lap();
+              ready = true;
+              if (elect_one()) {
+                // the pending k-blocks sit in the npend stages ending at `stage`
+                for (int q = 0; q < npend; ++q) {
+                  const uint32_t st = (stage + u_stg - (npend - 1) + q) % u_stg;
+                  tma_load_2d(ring_addr + st * u_sbytes + kSubTileBytes, tm_act, smem_u32(&cs.full[st]),
+                              (first_pending + q) * 64, row0, pol_x);
+                }
+              }
+              __syncwarp();
+            }
+          }
+          next();
+        }
       }
     }
-    __syncwarp();
+    if (p.prof && lane == 0) {
+      unsigned long long* pr = p.prof + blockIdx.x * kNumProf;
+      pr[kPrWaitEmpty] = c_wait;
+      pr[kPrIssue] = c_issue + pc.lap();
+      pr[kPrWaitDep] = c_dep;
+      pr[kTotal] = clock64() - t_begin;
+    }
   } else if (warp == 1) {
     // ============================ MMA issuer =============================
-    if (lane == 0) {
-      const uint32_t idesc = idesc_bf16(128, bmN);
-      uint32_t stage = 0, phase = 0, jl = 0, act_iter = 0;
-      uint32_t acc_cnt[2] = {0, 0}, chunk_cnt[2] = {0, 0};
-      unsigned long long c_full = 0, c_acc = 0, c_act = 0, items = 0;
-      ProfClock pc;
-      pc.start();
-      auto wait_full = [&]() -> uint32_t {
-        pc.lap();
-        mbar_wait(smem_u32(&cs.full[stage]), phase);
-        c_full += pc.lap();
-        tc_fence_after();
-        return ring_addr + stage * sbytes;
-      };
-      auto release = [&]() {
-        mma_commit(smem_u32(&cs.empty[stage]));
-        if (++stage == (uint32_t)stg) {
-          stage = 0;
-          phase ^= 1;
-        }
-      };
-      for (int j = blockIdx.x; j < G.total; j += gridDim.x, ++jl) {
-        ++items;
-        const Job jb = G.job(j);
-        const int r = G.dbl ? (jl & 1) : 0;
-        const uint32_t acc = tmem + r * 256;
-        pc.lap();
-        if (G.mode == kModeSplit) {
-          if (acc_cnt[r]) mbar_wait(smem_u32(&cs.acc_empty[r]), (acc_cnt[r] - 1) & 1);
-        } else {
-          for (int b = 0; b < 2; ++b)
-            if (chunk_cnt[b]) mbar_wait(smem_u32(&cs.chunk_empty[b]), (chunk_cnt[b] - 1) & 1);
-        }
-        c_acc += pc.lap();
-        tc_fence_after();
-        if (jb.kind == 0) {
-          for (int kb = 0; kb < G.kbH; ++kb) {
-            const uint32_t sb = wait_full();
-            const uint32_t xb = sb + nA * kSubTileBytes;
+    // Whole warp iterates; one elected lane issues the tcgen05 instructions.
+    const uint32_t idesc = idesc_bf16(128, warp_uniform(bmN));
+    const int u_stg = warp_uniform(stg), u_sbytes = warp_uniform(sbytes);
+    const uint32_t u_tmem = warp_uniform(tmem);
+    const uint64_t act_desc = sw128_kmajor_desc(act_addr);
+    const int a_step = warp_uniform(bmN) * 128 >> 4;  // act K-block stride in descriptor units
+    uint32_t stage = 0, phase = 0, jl = 0, act_iter = 0;
+    uint32_t acc_cnt[2] = {0, 0}, chunk_cnt[2] = {0, 0};
+    unsigned long long c_full = 0, c_acc = 0, c_act = 0, items = 0;
+    ProfClock pc;
+    pc.start();
+    auto wait_full = [&]() -> uint32_t {
+      pc.lap();
+      mbar_wait(smem_u32(&cs.full[stage]), phase);
+      c_full += pc.lap();
+      tc_fence_after();
+      return ring_addr + stage * u_sbytes;
+    };
+    auto release = [&]() {
+      if (elect_one()) mma_commit(smem_u32(&cs.empty[stage]));
+      __syncwarp();
+      if (++stage == (uint32_t)u_stg) {
+        stage = 0;
+        phase ^= 1;
+      }
+    };
+    for (int j = blockIdx.x; j < G.total; j += gridDim.x, ++jl) {
+      ++items;
+      const Job jb = G.job(j);
+      const int r = G.dbl ? (jl & 1) : 0;
+      const uint32_t acc = u_tmem + r * 256;
+      pc.lap();
+      if (G.mode == kModeSplit) {
+        if (acc_cnt[r]) mbar_wait(smem_u32(&cs.acc_empty[r]), (acc_cnt[r] - 1) & 1);
+      } else {
+        for (int b = 0; b < 2; ++b)
+          if (chunk_cnt[b]) mbar_wait(smem_u32(&cs.chunk_empty[b]), (chunk_cnt[b] - 1) & 1);
+      }
+      c_acc += pc.lap();
+      tc_fence_after();
+      if (jb.kind == 0) {
+        for (int kb = 0; kb < G.kbH; ++kb) {
+          const uint32_t sb = wait_full();
+          const uint64_t da = sw128_kmajor_desc(sb);
+          const uint64_t db = sw128_kmajor_desc(sb + nA * kSubTileBytes);
+          if (elect_one()) {
             for (int t = 0; t < nA; ++t) {
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                mma_bf16(acc + t * bmN, sw128_kmajor_desc(sb + t * kSubTileBytes + k * 32),
-                         sw128_kmajor_desc(xb + k * 32), idesc, (kb | k) != 0);
+                mma_bf16(acc + t * bmN, da + ((t * kSubTileBytes + k * 32) >> 4), db + ((k * 32) >> 4), idesc,
+                         (kb | k) != 0);
             }
-            release();
           }
-          mma_commit(smem_u32(&cs.acc_full[r]));
-          ++acc_cnt[r];
-          if (G.mode == kModeFused) {
+          __syncwarp();
+          release();
+        }
+        if (elect_one()) mma_commit(smem_u32(&cs.acc_full[r]));
+        __syncwarp();
+        ++acc_cnt[r];
+        if (G.mode == kModeFused) {
+          pc.lap();
+          mbar_wait(smem_u32(&cs.act_full), act_iter & 1);
+          c_act += pc.lap();
+          ++act_iter;
+          tc_fence_after();
+          for (int hc = 0; hc < G.n_hc; ++hc) {
+            const int b = hc & 1;
             pc.lap();
-            mbar_wait(smem_u32(&cs.act_full), act_iter & 1);
-            c_act += pc.lap();
-            ++act_iter;
-            tc_fence_after();
-            for (int hc = 0; hc < G.n_hc; ++hc) {
-              const int b = hc & 1;
-              pc.lap();
-              if (chunk_cnt[b]) mbar_wait(smem_u32(&cs.chunk_empty[b]), (chunk_cnt[b] - 1) & 1);
-              c_acc += pc.lap();
-              const uint32_t sb = wait_full();
+            if (chunk_cnt[b]) mbar_wait(smem_u32(&cs.chunk_empty[b]), (chunk_cnt[b] - 1) & 1);
+            c_acc += pc.lap();
+            const uint32_t sb = wait_full();
+            const uint64_t da = sw128_kmajor_desc(sb);
+            if (elect_one()) {
               for (int kk = 0; kk < nA; ++kk) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                  mma_bf16(tmem + b * bmN, sw128_kmajor_desc(sb + kk * kSubTileBytes + k * 32),
-                           sw128_kmajor_desc(act_addr + kk * bmN * 128 + k * 32), idesc, (kk | k) != 0);
+                  mma_bf16(u_tmem + b * bmN, da + ((kk * kSubTileBytes + k * 32) >> 4),
+                           act_desc + kk * a_step + ((k * 32) >> 4), idesc, (kk | k) != 0);
               }
-              release();
-              mma_commit(smem_u32(&cs.chunk_full[b]));
-              ++chunk_cnt[b];
             }
+            __syncwarp();
+            release();
+            if (elect_one()) mma_commit(smem_u32(&cs.chunk_full[b]));
+            __syncwarp();
+            ++chunk_cnt[b];
           }
-        } else {
-          for (int kb = 0; kb < G.kbI; ++kb) {
-            const uint32_t sb = wait_full();
+        }
+      } else {
+        for (int kb = 0; kb < G.kbI; ++kb) {
+          const uint32_t sb = wait_full();
+          const uint64_t da = sw128_kmajor_desc(sb);
+          const uint64_t db = sw128_kmajor_desc(sb + kSubTileBytes);
+          if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              mma_bf16(acc, sw128_kmajor_desc(sb + k * 32), sw128_kmajor_desc(sb + kSubTileBytes + k * 32),
-                       idesc, (kb | k) != 0);
-            release();
+              mma_bf16(acc, da + ((k * 32) >> 4), db + ((k * 32) >> 4), idesc, (kb | k) != 0);
           }
-          mma_commit(smem_u32(&cs.acc_full[r]));
-          ++acc_cnt[r];
+          __syncwarp();
+          release();
         }
-      }
-      if (p.prof) {
-        unsigned long long* pr = p.prof + blockIdx.x * kNumProf;
-        pr[kMmaWaitFull] = c_full;
-        pr[kMmaWaitAcc] = c_acc;
-        pr[kMmaWaitAct] = c_act;
-        pr[kItems] = items;
+        if (elect_one()) mma_commit(smem_u32(&cs.acc_full[r]));
+        __syncwarp();
+        ++acc_cnt[r];
       }
     }
-    __syncwarp();
+    if (p.prof && lane == 0) {
+      unsigned long long* pr = p.prof + blockIdx.x * kNumProf;
+      pr[kMmaWaitFull] = c_full;
+      pr[kMmaWaitAcc] = c_acc;
+      pr[kMmaWaitAct] = c_act;
+      pr[kItems] = items;
+    }
   } else if (warp >= 4) {
     // ============================ epilogue ===============================
     const int et = threadIdx.x - 128;  // TMEM lane == weight row of the 128-row MMA tile

@@ -55,8 +55,8 @@ if a.prof:
     torch.cuda.synchronize()
     _lib.load().ramp_set_profile_buffer(None)
     pr = buf.view(148, 16).cpu().numpy().astype(np.float64)
-    names = ["pr_wait_empty", "pr_issue", "mma_wait_full", "mma_wait_acc3", "mma_wait_act", "epi_wait_acc1",
-             "epi_swiglu", "epi_wait_acc3", "epi_scatter", "total", "items", "epi_meta"]
+    names = ["pr_wait_empty", "pr_issue", "mma_wait_full", "mma_wait_acc", "mma_wait_act", "epi_wait_acc",
+             "epi_swiglu", "epi_wait_chunk", "epi_scatter", "total", "items", "epi_meta", "pr_wait_dep"]
     act = pr[:, 10] > 0
     print(f"S={S} cfg bm={a.bm} ttn={a.ttn} stg={a.stg}: {e0.elapsed_time(e1)*1000:.1f} us (with profiling)")
     for i, nme in enumerate(names):
