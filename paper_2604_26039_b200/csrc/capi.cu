@@ -200,6 +200,7 @@ int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const flo
   ml.x_sorted = ws + L.xs;
   ml.act_g = ws + L.act;
   ml.done = ra.done;
+  ml.job_counter = ra.ctrl + 7;
   ml.rows = L.rows;
   ml.table = *table;
   ml.S = S;

@@ -51,7 +51,7 @@ constexpr int kModeSplit = 1;
 
 __host__ __device__ inline int bm_mma(int bm) { return bm <= 16 ? 16 : (bm + 15) / 16 * 16; }
 __host__ __device__ inline int stage_bytes(int bm, int ttn) {
-  const int raw = (ttn / 128) * kSubTileBytes + bm_mma(bm) * 128;
+  const int raw = (ttn >= 256 ? ttn / 128 : 1) * kSubTileBytes + bm_mma(bm) * 128;
   return (raw + 1023) / 1024 * 1024;
 }
 __host__ __device__ inline int act_bytes(int bm, int ttn, int mode) {
@@ -68,7 +68,7 @@ __host__ __device__ inline int bmn_index(int bmN) { return bmN <= 16 ? 0 : bmN <
 struct MoeMaps {
   CUtensorMap xs[4];   // x_sorted [rows, H],  box {64, 16/32/64/128}
   CUtensorMap act[4];  // act_g    [rows, I],  box {64, 16/32/64/128}
-  CUtensorMap w1[2];   // W1 as [2E, I, H],    box {64, n_i, 2} for n_i = 128 / 256
+  CUtensorMap w1[3];   // W1 as [2E, I, H],    box {64, n_i, 2} for n_i = 64 / 128 / 256
   CUtensorMap w2;      // W2 as [E*H, I],      box {64, 128}
 };
 
@@ -80,6 +80,7 @@ struct MoeParams {
   float* out_acc;              // [S, H] fp32, zeroed by the route kernel
   __nv_bfloat16* act_g;        // [rows, I] split-mode intermediate
   int* done;                   // [n_mtiles] split-mode phase-A completion counters (zeroed by route)
+  int* job_counter;            // global job claim counter (zeroed by route)
   ramp_table_t table;
   int32_t S, H, I, E, top_k, n_assign;
   unsigned long long* prof;    // optional per-CTA cycle counters [gridDim][16] (diagnostics)
@@ -110,6 +111,9 @@ struct CtrlSmem {
   uint64_t act_full;       // fused: act tile written
   uint64_t chunk_full[2];  // fused: phase-3 chunk accumulators
   uint64_t chunk_empty[2];
+  uint64_t job_full[4];    // dynamic job ring: producer -> MMA + epilogue
+  uint64_t job_empty[4];
+  int32_t job_slot[4];
   uint32_t tmem_base;
   int32_t epi_tok[128];
   float epi_w[128];
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   G.bm = p.table.bm[cfg];
   G.bmN = bm_mma(G.bm);
   const int ttn = p.table.ttn[cfg];
-  G.nA = ttn / 128;
+  G.nA = ttn >= 256 ? ttn / 128 : 1;  // ttn = 128: one tile = 64 gate rows + 64 up rows
   G.n_i = ttn / 2;
   G.stripes = p.I / G.n_i;
   G.n_mtiles = n_post_pad / G.bm;
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   unsigned char* act_ptr = base + kCtrlBytes + kStageBytesScatter + stg * sbytes;
   const CUtensorMap* tm_xs = &maps.xs[bmn_index(bmN)];
   const CUtensorMap* tm_act = &maps.act[bmn_index(bmN)];
-  const CUtensorMap* tm_w1 = &maps.w1[G.n_i == 256 ? 1 : 0];
+  const CUtensorMap* tm_w1 = &maps.w1[G.n_i == 256 ? 2 : G.n_i == 128 ? 1 : 0];
   const CUtensorMap* tm_w2 = &maps.w2;
 
   if (warp == 0 && lane == 0) {
@@ -229,6 +233,10 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       mbar_init(smem_u32(&cs.chunk_empty[b]), 128);
     }
     mbar_init(smem_u32(&cs.act_full), 128);
+    for (int q = 0; q < 4; ++q) {
+      mbar_init(smem_u32(&cs.job_full[q]), 1);
+      mbar_init(smem_u32(&cs.job_empty[q]), 1 + 128);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(smem_u32(&cs.tmem_base));
@@ -259,7 +267,21 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       mbar_wait(smem_u32(&cs.empty[stage]), phase ^ 1);
       c_wait += pc.lap();
     };
-    for (int j = blockIdx.x; j < G.total; j += gridDim.x) {
+    uint32_t js = 0, jph = 0;
+    while (true) {
+      // claim the next job (dynamic, in global order) and publish it to the ring
+      int j = 0;
+      if (lane == 0) j = atomicAdd(p.job_counter, 1);
+      j = warp_uniform(j);
+      if (j >= G.total) j = -1;
+      mbar_wait(smem_u32(&cs.job_empty[js]), jph ^ 1);
+      if (elect_one()) {
+        cs.job_slot[js] = j;
+        mbar_arrive(smem_u32(&cs.job_full[js]));
+      }
+      __syncwarp();
+      if (++js == 4) { js = 0; jph ^= 1; }
+      if (j < 0) break;
       const Job jb = G.job(j);
       const int e = warp_uniform(p.tile_expert[jb.m]);
       const int row0 = jb.m * G.bm;
@@ -369,7 +391,14 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         phase ^= 1;
       }
     };
-    for (int j = blockIdx.x; j < G.total; j += gridDim.x, ++jl) {
+    uint32_t js = 0, jph = 0;
+    for (;; ++jl) {
+      mbar_wait(smem_u32(&cs.job_full[js]), jph);
+      const int j = warp_uniform(cs.job_slot[js]);
+      if (elect_one()) mbar_arrive(smem_u32(&cs.job_empty[js]));
+      __syncwarp();
+      if (++js == 4) { js = 0; jph ^= 1; }
+      if (j < 0) break;
       ++items;
       const Job jb = G.job(j);
       const int r = G.dbl ? (jl & 1) : 0;
@@ -463,7 +492,13 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     unsigned long long c_meta = 0, c_wacc = 0, c_swiglu = 0, c_wchunk = 0, c_scatter = 0;
     ProfClock pc;
     pc.start();
-    for (int j = blockIdx.x; j < G.total; j += gridDim.x, ++jl) {
+    uint32_t js = 0, jph = 0;
+    for (;; ++jl) {
+      mbar_wait(smem_u32(&cs.job_full[js]), jph);
+      const int j = cs.job_slot[js];
+      mbar_arrive(smem_u32(&cs.job_empty[js]));
+      if (++js == 4) { js = 0; jph ^= 1; }
+      if (j < 0) break;
       const Job jb = G.job(j);
       const int r = G.dbl ? (jl & 1) : 0;
       const uint32_t acc = tmem + lane_off + r * 256;
@@ -484,29 +519,53 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       tc_fence_after();
 
       if (jb.kind == 0) {
-        // ---- phase 2: SwiGLU.  Thread et owns features f = th*128 + et.
-        for (int th = 0; th < nA / 2; ++th) {
-          const int f = th * 128 + et;
+        // ---- phase 2: SwiGLU -> bf16 act (fused: SW128 K-major smem tile that
+        // phase 3 reads; split: L2-resident global rows read by phase-3 jobs)
+        auto store_act = [&](int f, int j0, const float (&g)[16], const float (&u)[16]) {
+          if (G.mode == kModeFused) {
+            unsigned char* kblk = act_ptr + (f >> 6) * bmN * 128;
+            const int chunk = (f & 63) >> 3, within = (f & 7) * 2;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const int jj = j0 + q;
+              *reinterpret_cast<__nv_bfloat16*>(kblk + jj * 128 + ((chunk ^ (jj & 7)) << 4) + within) =
+                  __float2bfloat16(silu_mul(g[q], u[q]));
+            }
+          } else {
+            __nv_bfloat16* dst = p.act_g + static_cast<size_t>(row0 + j0) * p.I + jb.s * G.n_i + f;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (j0 + q < G.bm) dst[static_cast<size_t>(q) * p.I] = __float2bfloat16(silu_mul(g[q], u[q]));
+          }
+        };
+        if (nA == 1) {
+          // ttn = 128: lanes 0-63 hold gate rows, lanes 64-127 the matching up rows
           for (int j0 = 0; j0 < bmN; j0 += 16) {
             float g[16], u[16];
-            tmem_ld16(acc + th * bmN + j0, g);
-            tmem_ld16(acc + (nA / 2 + th) * bmN + j0, u);
+            tmem_ld16(acc + j0, g);
             tmem_ld_wait();
-            if (G.mode == kModeFused) {
-              // bf16 act tile in the SW128 K-major layout phase 3 reads
-              unsigned char* kblk = act_ptr + (f >> 6) * bmN * 128;
-              const int chunk = (f & 63) >> 3, within = (f & 7) * 2;
+            if (et >= 64) {
 #pragma unroll
-              for (int q = 0; q < 16; ++q) {
-                const int jj = j0 + q;
-                *reinterpret_cast<__nv_bfloat16*>(kblk + jj * 128 + ((chunk ^ (jj & 7)) << 4) + within) =
-                    __float2bfloat16(silu_mul(g[q], u[q]));
-              }
-            } else {
-              __nv_bfloat16* dst = p.act_g + static_cast<size_t>(row0 + j0) * p.I + jb.s * G.n_i + f;
+              for (int q = 0; q < 16; ++q) tbuf[q * 64 + (et - 64)] = g[q];
+            }
+            named_bar_sync(1, 128);
+            if (et < 64) {
 #pragma unroll
-              for (int q = 0; q < 16; ++q)
-                if (j0 + q < G.bm) dst[static_cast<size_t>(q) * p.I] = __float2bfloat16(silu_mul(g[q], u[q]));
+              for (int q = 0; q < 16; ++q) u[q] = tbuf[q * 64 + et];
+              store_act(et, j0, g, u);
+            }
+            named_bar_sync(1, 128);
+          }
+        } else {
+          // Thread et owns features f = th*128 + et of the stripe.
+          for (int th = 0; th < nA / 2; ++th) {
+            const int f = th * 128 + et;
+            for (int j0 = 0; j0 < bmN; j0 += 16) {
+              float g[16], u[16];
+              tmem_ld16(acc + th * bmN + j0, g);
+              tmem_ld16(acc + (nA / 2 + th) * bmN + j0, u);
+              tmem_ld_wait();
+              store_act(f, j0, g, u);
             }
           }
         }

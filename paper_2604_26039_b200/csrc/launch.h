@@ -52,6 +52,7 @@ struct MoeLaunch {
   void* x_sorted;   // [rows, H] bf16
   void* act_g;      // [rows, I] bf16
   int* done;        // [rows] split-mode counters
+  int* job_counter; // dynamic scheduler claim counter (zeroed by the route kernel)
   int64_t rows;     // capacity of x_sorted / act_g
   ramp_table_t table;
   int32_t S, H, I, E, top_k;

@@ -59,7 +59,8 @@ static bool make_map_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64
 }
 
 int64_t config_smem_bytes(int bm, int ttn, int stg, int mode) {
-  if (bm < 1 || bm > kMaxBm || (ttn != 256 && ttn != 512) || stg < 1 || stg > kMaxStages) return 0;
+  if (bm < 1 || bm > kMaxBm || (ttn != 128 && ttn != 256 && ttn != 512) || stg < 1 || stg > kMaxStages)
+    return 0;
   if (mode != kModeFused && mode != kModeSplit) return 0;
   const int b = moe_smem_bytes(bm, ttn, stg, mode);
   return b <= kSmemLimit ? b : 0;
@@ -90,12 +91,12 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
     ok = ok && make_map_2d(&maps.xs[i], l.x_sorted, l.rows, l.H, 16u << i);
     ok = ok && make_map_2d(&maps.act[i], l.act_g, l.rows, l.I, 16u << i);
   }
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 3; ++i) {
     // W1 viewed as [2E][I][H]: plane 2e = gate rows, 2e+1 = up rows of expert e
     const uint64_t dims[3] = {(uint64_t)l.H, (uint64_t)l.I, 2ull * l.E};
     const uint64_t strides[2] = {(uint64_t)l.H * 2, (uint64_t)l.I * l.H * 2};
-    const uint32_t box[3] = {64, 128u << i, 2};
-    ok = ok && ((l.I % (128 << i)) != 0 || make_map(&maps.w1[i], l.w1, 3, dims, strides, box));
+    const uint32_t box[3] = {64, 64u << i, 2};
+    ok = ok && ((l.I % (64 << i)) != 0 || make_map(&maps.w1[i], l.w1, 3, dims, strides, box));
   }
   ok = ok && make_map_2d(&maps.w2, l.w2, (uint64_t)l.E * l.H, l.I, 128);
   if (!ok) {
@@ -110,6 +111,7 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
   p.out_acc = l.out_acc;
   p.act_g = static_cast<__nv_bfloat16*>(l.act_g);
   p.done = l.done;
+  p.job_counter = l.job_counter;
   p.table = l.table;
   p.S = l.S;
   p.H = l.H;

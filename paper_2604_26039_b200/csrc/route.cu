@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
     a.ctrl[2] = npp / bm;
     a.ctrl[3] = n_eval;
     a.ctrl[4] = st.bad;
+    a.ctrl[7] = 0;  // megakernel job counter
     if (a.sel_out) {
       a.sel_out[0] = sel;
       a.sel_out[1] = npp;
