@@ -124,7 +124,9 @@ int64_t ramp_config_smem_bytes(int32_t bm, int32_t ttn, int32_t stg, int32_t mod
 
 /* Diagnostics: when dev_buf is non-null, every later megakernel launch writes
  * 16 per-CTA cycle counters (producer wait/issue, MMA waits, epilogue phases,
- * see ProfSlot in csrc/fused_moe.cuh) to dev_buf[blockIdx * 16 + slot].
+ * see ProfSlot in csrc/fused_moe.cuh) to dev_buf[blockIdx * 16 + slot], and
+ * the route kernel writes globaltimer stamps to dev_buf[148 * 16 + 0..15]
+ * (buffer: >= 149 * 16 entries).
  * Pass null to switch it off.  Not used on the timed path. */
 void ramp_set_profile_buffer(unsigned long long* dev_buf);
 

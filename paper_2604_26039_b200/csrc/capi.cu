@@ -175,6 +175,7 @@ int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const flo
   ra.done = reinterpret_cast<int*>(ws + L.done);
   ra.x = x;
   ra.x_sorted = ws + L.xs;
+  ra.prof = ramp::g_prof_buffer ? ramp::g_prof_buffer + 148 * 16 : nullptr;
   ra.S = S;
   ra.H = H;
   ra.top_k = top_k;

@@ -186,6 +186,37 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
+  // Prologue (overlaps the route kernel's tail under PDL): descriptors,
+  // barriers, TMEM.  Nothing here reads the route kernel's outputs.
+  if (warp == 0 && lane < 12) {
+    const CUtensorMap* all = &maps.xs[0];  // xs[4], act[4], w1[3], w2 are contiguous
+    tma_prefetch_desc(all + lane);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kMaxStages; ++s) {
+      mbar_init(smem_u32(&cs.full[s]), 1);
+      mbar_init(smem_u32(&cs.empty[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&cs.acc_full[b]), 1);
+      mbar_init(smem_u32(&cs.acc_empty[b]), 128);
+      mbar_init(smem_u32(&cs.chunk_full[b]), 1);
+      mbar_init(smem_u32(&cs.chunk_empty[b]), 128);
+    }
+    mbar_init(smem_u32(&cs.act_full), 128);
+    for (int q = 0; q < 4; ++q) {
+      mbar_init(smem_u32(&cs.job_full[q]), 1);
+      mbar_init(smem_u32(&cs.job_empty[q]), 1 + 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(smem_u32(&cs.tmem_base));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = cs.tmem_base;
+  pdl_wait();  // the route kernel's selection, alignment and gathered rows are now visible
+
   // --- runtime tile config chosen by the dispatcher (no host round trip)
   const int cfg = p.ctrl[0];
   const int n_post_pad = p.ctrl[1];
@@ -214,36 +245,6 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   const CUtensorMap* tm_act = &maps.act[bmn_index(bmN)];
   const CUtensorMap* tm_w1 = &maps.w1[G.n_i == 256 ? 2 : G.n_i == 128 ? 1 : 0];
   const CUtensorMap* tm_w2 = &maps.w2;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(tm_xs);
-    tma_prefetch_desc(tm_w1);
-    tma_prefetch_desc(tm_w2);
-    if (G.mode == kModeSplit) tma_prefetch_desc(tm_act);
-  }
-  if (warp == 1 && lane == 0) {
-    for (int s = 0; s < stg; ++s) {
-      mbar_init(smem_u32(&cs.full[s]), 1);
-      mbar_init(smem_u32(&cs.empty[s]), 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(smem_u32(&cs.acc_full[b]), 1);
-      mbar_init(smem_u32(&cs.acc_empty[b]), 128);
-      mbar_init(smem_u32(&cs.chunk_full[b]), 1);
-      mbar_init(smem_u32(&cs.chunk_empty[b]), 128);
-    }
-    mbar_init(smem_u32(&cs.act_full), 128);
-    for (int q = 0; q < 4; ++q) {
-      mbar_init(smem_u32(&cs.job_full[q]), 1);
-      mbar_init(smem_u32(&cs.job_empty[q]), 1 + 128);
-    }
-    fence_mbar_init();
-  }
-  if (warp == 2) tmem_alloc<512>(smem_u32(&cs.tmem_base));
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = cs.tmem_base;
 
   if (warp == 0) {
     // ============================ TMA producer ============================
@@ -637,6 +638,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
 // fp32 accumulator -> bf16 output.
 __global__ void finalize_bf16_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ out,
                                      int64_t n) {
+  pdl_wait();  // launched with programmatic serialization behind the megakernel
   const int64_t n4 = n / 4;
   const float4* a4 = reinterpret_cast<const float4*>(acc);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;

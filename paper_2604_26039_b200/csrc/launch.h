@@ -27,6 +27,7 @@ struct RouteArgs {
   float* acc_clear;      // fp32 accumulator cleared by the helper blocks
   int64_t acc_clear_n;
   int* done;             // split-mode per-M-tile counters, zeroed by block 0
+  unsigned long long* prof;  // optional globaltimer stamps (diagnostics)
   const void* x;         // [S, H] bf16 tokens
   void* x_sorted;        // [rows, H] bf16, gathered by the helper blocks (null: skip)
   int32_t S, H, top_k;

@@ -85,23 +85,61 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
     if (err != cudaSuccess) return err;
     attr_set = true;
   }
+  // Tensor maps depend only on pointers and shapes: encode once per
+  // (workspace, weights, shape) and reuse (the encoder costs ~1 us per map).
+  struct MapKey {
+    const void *xs, *act, *w1, *w2;
+    int64_t rows;
+    int32_t H, I, E;
+    bool operator==(const MapKey& o) const {
+      return xs == o.xs && act == o.act && w1 == o.w1 && w2 == o.w2 && rows == o.rows && H == o.H && I == o.I &&
+             E == o.E;
+    }
+  };
+  struct MapEntry {
+    MapKey key;
+    alignas(64) MoeMaps maps;
+    bool used;
+  };
+  static MapEntry cache[16];
+  static int cache_next = 0;
+  static std::mutex cache_mu;
+  const MapKey key{l.x_sorted, l.act_g, l.w1, l.w2, l.rows, l.H, l.I, l.E};
   alignas(64) MoeMaps maps;  // copied into the launch's parameter buffer
-  bool ok = true;
-  for (int i = 0; i < 4; ++i) {
-    ok = ok && make_map_2d(&maps.xs[i], l.x_sorted, l.rows, l.H, 16u << i);
-    ok = ok && make_map_2d(&maps.act[i], l.act_g, l.rows, l.I, 16u << i);
+  bool hit = false;
+  {
+    std::lock_guard<std::mutex> g(cache_mu);
+    for (auto& c : cache)
+      if (c.used && c.key == key) {
+        maps = c.maps;
+        hit = true;
+        break;
+      }
   }
-  for (int i = 0; i < 3; ++i) {
-    // W1 viewed as [2E][I][H]: plane 2e = gate rows, 2e+1 = up rows of expert e
-    const uint64_t dims[3] = {(uint64_t)l.H, (uint64_t)l.I, 2ull * l.E};
-    const uint64_t strides[2] = {(uint64_t)l.H * 2, (uint64_t)l.I * l.H * 2};
-    const uint32_t box[3] = {64, 64u << i, 2};
-    ok = ok && ((l.I % (64 << i)) != 0 || make_map(&maps.w1[i], l.w1, 3, dims, strides, box));
-  }
-  ok = ok && make_map_2d(&maps.w2, l.w2, (uint64_t)l.E * l.H, l.I, 128);
-  if (!ok) {
-    *why = "cuTensorMapEncodeTiled failed (alignment or driver entry point)";
-    return cudaErrorInvalidValue;
+  if (!hit) {
+    bool ok = true;
+    for (int i = 0; i < 4; ++i) {
+      ok = ok && make_map_2d(&maps.xs[i], l.x_sorted, l.rows, l.H, 16u << i);
+      ok = ok && make_map_2d(&maps.act[i], l.act_g, l.rows, l.I, 16u << i);
+    }
+    for (int i = 0; i < 3; ++i) {
+      // W1 viewed as [2E][I][H]: plane 2e = gate rows, 2e+1 = up rows of expert e
+      const uint64_t dims[3] = {(uint64_t)l.H, (uint64_t)l.I, 2ull * l.E};
+      const uint64_t strides[2] = {(uint64_t)l.H * 2, (uint64_t)l.I * l.H * 2};
+      const uint32_t box[3] = {64, 64u << i, 2};
+      ok = ok && ((l.I % (64 << i)) != 0 || make_map(&maps.w1[i], l.w1, 3, dims, strides, box));
+    }
+    ok = ok && make_map_2d(&maps.w2, l.w2, (uint64_t)l.E * l.H, l.I, 128);
+    if (!ok) {
+      *why = "cuTensorMapEncodeTiled failed (alignment or driver entry point)";
+      return cudaErrorInvalidValue;
+    }
+    std::lock_guard<std::mutex> g(cache_mu);
+    MapEntry& c = cache[cache_next];
+    cache_next = (cache_next + 1) % 16;
+    c.key = key;
+    c.maps = maps;
+    c.used = true;
   }
   MoeParams p;
   p.ctrl = l.ctrl;
@@ -120,14 +158,34 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
   p.top_k = l.top_k;
   p.n_assign = l.S * l.top_k;
   p.prof = g_prof_buffer;
-  fused_moe_bf16_kernel<<<sm_count_cached(), kMoeThreads, kSmemLimit, stream>>>(maps, p);
-  cudaError_t err = cudaGetLastError();
+  // Programmatic dependent launch: the megakernel's prologue (barrier init,
+  // TMEM allocation, descriptor prefetch) overlaps the route kernel's tail,
+  // and the finalize kernel's launch overlaps the megakernel's tail.
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(sm_count_cached());
+  cfg.blockDim = dim3(kMoeThreads);
+  cfg.dynamicSmemBytes = kSmemLimit;
+  cfg.stream = stream;
+  cfg.attrs = pdl;
+  cfg.numAttrs = 1;
+  cudaError_t err = cudaLaunchKernelEx(&cfg, fused_moe_bf16_kernel, maps, p);
   if (err != cudaSuccess) return err;
   const int64_t n = (int64_t)l.S * l.H;
   int blocks = (int)((n / 4 + 255) / 256);
   if (blocks > 4 * sm_count_cached()) blocks = 4 * sm_count_cached();
   if (blocks < 1) blocks = 1;
-  finalize_bf16_kernel<<<blocks, 256, 0, stream>>>(l.out_acc, static_cast<__nv_bfloat16*>(l.out), n);
+  cudaLaunchConfig_t fcfg{};
+  fcfg.gridDim = dim3(blocks);
+  fcfg.blockDim = dim3(256);
+  fcfg.stream = stream;
+  fcfg.attrs = pdl;
+  fcfg.numAttrs = 1;
+  err = cudaLaunchKernelEx(&fcfg, finalize_bf16_kernel, static_cast<const float*>(l.out_acc),
+                           static_cast<__nv_bfloat16*>(l.out), n);
+  if (err != cudaSuccess) return err;
   return cudaGetLastError();
 }
 

@@ -18,7 +18,12 @@ struct RouteStatic {
 
 __global__ void __launch_bounds__(kRouteThreads, 1)
     route_kernel(const RouteArgs a) {
+  pdl_launch_dependents();  // let the megakernel's prologue start on idle SMs
+  auto stamp = [&](int slot) {
+    if (a.prof && threadIdx.x == 0) a.prof[slot] = globaltimer();
+  };
   if (blockIdx.x > 0) {
+    if (blockIdx.x == 1) stamp(8);
     // Helper blocks: clear the fp32 output accumulator, then (once block 0
     // has published the alignment) gather the token rows into expert-sorted
     // order so the megakernel can fetch a whole M-tile with one TMA box.
@@ -31,9 +36,11 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
          i += (int64_t)nh * blockDim.x)
       a.acc_clear[i] = 0.f;
     if (a.x_sorted == nullptr) return;
+    if (blockIdx.x == 1) stamp(9);
     if (threadIdx.x == 0)
-      while (ld_acquire_gpu(a.ctrl + 5) == 0) __nanosleep(128);
+      while (ld_acquire_gpu(a.ctrl + 5) == 0) __nanosleep(64);
     __syncthreads();
+    if (blockIdx.x == 1) stamp(10);
     const int npp = __ldcg(a.ctrl + 1);
     const int row_vec = a.H / 8;  // 16-byte vectors per row
     const int4* xv = reinterpret_cast<const int4*>(a.x);
@@ -50,6 +57,7 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
       }
     }
     __syncthreads();
+    if (blockIdx.x == 1) stamp(11);
     if (threadIdx.x == 0) {
       // the last helper through resets the flag for the next call
       if (atomicAdd(a.ctrl + 6, 1) == nh - 1) {
@@ -62,9 +70,11 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ RouteStatic st;
   RouteSmem s = carve_route_smem(dyn, a.E);
+  stamp(0);
   if (threadIdx.x == 0) st.bad = 0;
   __syncthreads();
   block_histogram(a.topk_ids, a.n_assign, a.E, s.hist, &st.bad);
+  stamp(1);
   int sel = a.forced_cfg;
   int n_eval = 0;
   if (sel < 0) {
@@ -72,10 +82,12 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
                          st.cnt);
     n_eval = st.cnt[0];
   }
+  stamp(2);
   const int bm = a.table.bm[sel];
   int32_t* n_post_pad = a.ctrl + 1;
   block_align(a.topk_ids, a.n_assign, a.E, bm, s, st.warp_tot, a.sorted_ids, a.tile_expert,
               n_post_pad);
+  stamp(3);
   const int npp = s.off[a.E];
   for (int e = threadIdx.x; e < a.E; e += blockDim.x)
     if (a.hist_out) a.hist_out[e] = s.hist[e];
@@ -99,6 +111,7 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
     __threadfence();
     st_release_gpu(a.ctrl + 5, 1);
   }
+  stamp(4);
 }
 
 __global__ void __launch_bounds__(kRouteThreads, 1)

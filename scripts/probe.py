@@ -40,6 +40,7 @@ def main():
     ap.add_argument("--skew", default="0,1.0")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--all", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays (no host overhead)")
     a = ap.parse_args()
     E, H, I, k = a.E, a.H, a.I, a.k
     gen = torch.Generator(device="cuda").manual_seed(0)
@@ -65,13 +66,24 @@ def main():
             for c in cfgs:
                 for _ in range(2):
                     M.fused_moe(x, w1, w2, w, ids, table, c.id, out=out, workspace=ws)
+                run = lambda: M.fused_moe(x, w1, w2, w, ids, table, c.id, out=out, workspace=ws)  # noqa: E731
+                if a.graph:
+                    g = torch.cuda.CUDAGraph()
+                    s = torch.cuda.Stream()
+                    s.wait_stream(torch.cuda.current_stream())
+                    with torch.cuda.stream(s):
+                        with torch.cuda.graph(g, stream=s):
+                            run()
+                    torch.cuda.current_stream().wait_stream(s)
+                    run = g.replay
+                    run()
                 ts = []
                 for _ in range(a.iters):
                     flush.zero_()
                     e0 = torch.cuda.Event(enable_timing=True)
                     e1 = torch.cuda.Event(enable_timing=True)
                     e0.record()
-                    M.fused_moe(x, w1, w2, w, ids, table, c.id, out=out, workspace=ws)
+                    run()
                     e1.record()
                     torch.cuda.synchronize()
                     ts.append(e0.elapsed_time(e1) * 1000)
