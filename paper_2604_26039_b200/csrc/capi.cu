@@ -170,21 +170,18 @@ int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const flo
   ra.sorted_ids = reinterpret_cast<int32_t*>(ws + L.sorted);
   ra.tile_expert = reinterpret_cast<int32_t*>(ws + L.tiles);
   ra.sel_out = sel_out;
-  ra.acc_clear = reinterpret_cast<float*>(ws + L.acc);
-  ra.acc_clear_n = (int64_t)S * H;
+  // The megakernel gathers the token rows and clears the accumulator after
+  // converting it, so the route kernel is a single block.
+  ra.acc_clear = nullptr;
+  ra.acc_clear_n = 0;
   ra.done = reinterpret_cast<int*>(ws + L.done);
   ra.x = x;
-  ra.x_sorted = ws + L.xs;
+  ra.x_sorted = nullptr;
   ra.prof = ramp::g_prof_buffer ? ramp::g_prof_buffer + 148 * 16 : nullptr;
   ra.S = S;
   ra.H = H;
   ra.top_k = top_k;
-  // helpers: enough to clear the accumulator and gather ~4 rows per warp,
-  // at most two 1024-thread blocks per SM so all of them are co-resident
-  int64_t want = (ra.acc_clear_n / 4 + 4095) / 4096;
-  const int64_t gather = (ra.n_assign + (int64_t)E * 4 + 127) / 128;
-  if (gather > want) want = gather;
-  int zero_blocks = (int)(want < 1 ? 1 : (want > 287 ? 287 : want));
+  const int zero_blocks = 0;
   cudaError_t err = ramp::launch_route(ra, zero_blocks, st);
   if (err != cudaSuccess) return cuda_fail(err, "route kernel");
 
@@ -196,7 +193,7 @@ int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const flo
   ml.ctrl = ra.ctrl;
   ml.sorted_ids = ra.sorted_ids;
   ml.tile_expert = ra.tile_expert;
-  ml.out_acc = ra.acc_clear;
+  ml.out_acc = reinterpret_cast<float*>(ws + L.acc);
   ml.out = out;
   ml.x_sorted = ws + L.xs;
   ml.act_g = ws + L.act;

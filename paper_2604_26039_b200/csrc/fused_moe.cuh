@@ -81,6 +81,10 @@ struct MoeParams {
   __nv_bfloat16* act_g;        // [rows, I] split-mode intermediate
   int* done;                   // [n_mtiles] split-mode phase-A completion counters (zeroed by route)
   int* job_counter;            // global job claim counter (zeroed by route)
+  int* gbar;                   // [2] grid barriers: rows gathered, all jobs reduced (zeroed by route)
+  const __nv_bfloat16* x;      // [S, H] tokens
+  __nv_bfloat16* x_sorted;     // [rows, H] expert-sorted token rows (gathered in phase 0)
+  __nv_bfloat16* out;          // [S, H] bf16 result
   ramp_table_t table;
   int32_t S, H, I, E, top_k, n_assign;
   unsigned long long* prof;    // optional per-CTA cycle counters [gridDim][16] (diagnostics)
@@ -246,6 +250,38 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   const CUtensorMap* tm_w1 = &maps.w1[G.n_i == 256 ? 2 : G.n_i == 128 ? 1 : 0];
   const CUtensorMap* tm_w2 = &maps.w2;
 
+  // ---- phase 0: gather the token rows of every M-tile into expert-sorted
+  // order (warps 3-7 of every CTA), then arrive on grid barrier 0.  The
+  // producers stream weights meanwhile and hold back token tiles until all
+  // CTAs have arrived.
+  if (warp >= 3) {
+    const int row_vec = p.H / 8;  // 16-byte vectors per row
+    const int gw = blockIdx.x * 5 + (warp - 3), nw = gridDim.x * 5;
+    const int4* xv = reinterpret_cast<const int4*>(p.x);
+    int4* dv = reinterpret_cast<int4*>(p.x_sorted);
+    for (int r = gw; r < n_post_pad; r += nw) {
+      const int asg = p.sorted_ids[r];
+      int4* d = dv + static_cast<int64_t>(r) * row_vec;
+      if (asg < p.n_assign) {
+        const int4* src = xv + static_cast<int64_t>(asg / p.top_k) * row_vec;
+        for (int c0 = lane; c0 < row_vec; c0 += 32 * 4) {
+          int4 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (c0 + 32 * u < row_vec) v[u] = __ldg(src + c0 + 32 * u);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (c0 + 32 * u < row_vec) d[c0 + 32 * u] = v[u];
+        }
+      } else {
+        for (int c0 = lane; c0 < row_vec; c0 += 32) d[c0] = make_int4(0, 0, 0, 0);
+      }
+    }
+    __threadfence();
+    named_bar_sync(2, 160);
+    if (warp == 3 && lane == 0) atomicAdd(p.gbar, 1);
+  }
+
   if (warp == 0) {
     // ============================ TMA producer ============================
     // The whole warp walks the schedule (so every operand is warp-uniform and
@@ -269,6 +305,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       c_wait += pc.lap();
     };
     uint32_t js = 0, jph = 0;
+    bool gathered = false;
     while (true) {
       // claim the next job (dynamic, in global order) and publish it to the ring
       int j = 0;
@@ -289,6 +326,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       if (jb.kind == 0) {
         const uint32_t tx1 = nA * kSubTileBytes + bmN * 128;
         const int wrow = jb.s * G.n_i;
+        int first_pending = 0, npend = 0;
         for (int kb = 0; kb < G.kbH; ++kb) {
           acquire();
           if (elect_one()) {
@@ -296,9 +334,30 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             const uint32_t sb = ring_addr + stage * u_sbytes;
             mbar_arrive_expect_tx(full, tx1);
             tma_load_3d(sb, tm_w1, full, kb * 64, wrow, 2 * e, pol_w);
-            tma_load_2d(sb + nA * kSubTileBytes, tm_xs, full, kb * 64, row0, pol_x);
+            if (gathered) tma_load_2d(sb + nA * kSubTileBytes, tm_xs, full, kb * 64, row0, pol_x);
           }
           __syncwarp();
+          if (!gathered) {
+            // weights stream while phase 0 finishes; token rows follow once
+            // every CTA has published its slice of x_sorted
+            if (npend == 0) first_pending = kb;
+            ++npend;
+            if (npend == u_stg || kb == G.kbH - 1) {
+              pc.lap();
+              while (ld_acquire_gpu(p.gbar) < (int)gridDim.x) __nanosleep(32);
+              fence_proxy_async_global();
+              c_dep += pc.lap();
+              gathered = true;
+              if (elect_one()) {
+                for (int q = 0; q < npend; ++q) {
+                  const uint32_t st = (stage + u_stg - (npend - 1) + q) % u_stg;
+                  tma_load_2d(ring_addr + st * u_sbytes + nA * kSubTileBytes, tm_xs, smem_u32(&cs.full[st]),
+                              (first_pending + q) * 64, row0, pol_x);
+                }
+              }
+              __syncwarp();
+            }
+          }
           next();
         }
         if (G.mode == kModeFused) {
@@ -629,31 +688,34 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     }
   }
 
+  // ---- grid barrier 1: every job's reductions have landed; then convert
+  // the fp32 accumulator to bf16 and clear it for the next call.
+  __threadfence();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<512>(tmem);
-}
-
-// fp32 accumulator -> bf16 output.
-__global__ void finalize_bf16_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ out,
-                                     int64_t n) {
-  pdl_wait();  // launched with programmatic serialization behind the megakernel
-  const int64_t n4 = n / 4;
-  const float4* a4 = reinterpret_cast<const float4*>(acc);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 v = a4[i];
-    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
-    __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
-    uint2 pk;
-    pk.x = *reinterpret_cast<uint32_t*>(&lo);
-    pk.y = *reinterpret_cast<uint32_t*>(&hi);
-    reinterpret_cast<uint2*>(out)[i] = pk;
+  if (threadIdx.x == 0) {
+    atomicAdd(p.gbar + 1, 1);
+    while (ld_acquire_gpu(p.gbar + 1) < (int)gridDim.x) __nanosleep(64);
   }
-  for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = __float2bfloat16(acc[i]);
+  __syncthreads();
+  {
+    const int64_t n4 = static_cast<int64_t>(p.S) * p.H / 4;  // H % 128 == 0
+    float4* a4 = reinterpret_cast<float4*>(p.out_acc);
+    uint2* o2 = reinterpret_cast<uint2*>(p.out);
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+      const float4 v = __ldcg(a4 + i);
+      __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      o2[i] = pk;
+      a4[i] = z;
+    }
+  }
 }
 
 }  // namespace ramp

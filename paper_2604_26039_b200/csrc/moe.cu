@@ -150,6 +150,10 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
   p.act_g = static_cast<__nv_bfloat16*>(l.act_g);
   p.done = l.done;
   p.job_counter = l.job_counter;
+  p.gbar = l.job_counter + 1;
+  p.x = static_cast<const __nv_bfloat16*>(l.x);
+  p.x_sorted = static_cast<__nv_bfloat16*>(l.x_sorted);
+  p.out = static_cast<__nv_bfloat16*>(l.out);
   p.table = l.table;
   p.S = l.S;
   p.H = l.H;
@@ -172,19 +176,6 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
   cudaError_t err = cudaLaunchKernelEx(&cfg, fused_moe_bf16_kernel, maps, p);
-  if (err != cudaSuccess) return err;
-  const int64_t n = (int64_t)l.S * l.H;
-  int blocks = (int)((n / 4 + 255) / 256);
-  if (blocks > 4 * sm_count_cached()) blocks = 4 * sm_count_cached();
-  if (blocks < 1) blocks = 1;
-  cudaLaunchConfig_t fcfg{};
-  fcfg.gridDim = dim3(blocks);
-  fcfg.blockDim = dim3(256);
-  fcfg.stream = stream;
-  fcfg.attrs = pdl;
-  fcfg.numAttrs = 1;
-  err = cudaLaunchKernelEx(&fcfg, finalize_bf16_kernel, static_cast<const float*>(l.out_acc),
-                           static_cast<__nv_bfloat16*>(l.out), n);
   if (err != cudaSuccess) return err;
   return cudaGetLastError();
 }

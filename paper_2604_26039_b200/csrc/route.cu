@@ -99,6 +99,8 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
     a.ctrl[3] = n_eval;
     a.ctrl[4] = st.bad;
     a.ctrl[7] = 0;  // megakernel job counter
+    a.ctrl[8] = 0;  // megakernel grid barrier 0 (rows gathered)
+    a.ctrl[9] = 0;  // megakernel grid barrier 1 (all jobs reduced)
     if (a.sel_out) {
       a.sel_out[0] = sel;
       a.sel_out[1] = npp;

@@ -218,14 +218,17 @@ __device__ inline void block_align(const int32_t* __restrict__ ids, int64_t n, i
     const int rank = __popc(peers & lt_mask);
     if (e >= 0 && rank == 0) my_cnt[e] = static_cast<uint16_t>(__popc(peers));
     __syncthreads();
-    if (tid < E) {
-      int run = 0;
-      for (int w = 0; w < kRouteWarps; ++w) {
-        const int v = s.cnt[w * E + tid];
-        s.cnt[w * E + tid] = static_cast<uint16_t>(run);
-        run += v;
+    // per-expert exclusive prefix over the 32 warps: one warp scan per expert
+    for (int x = warp; x < E; x += kRouteWarps) {
+      const int v = s.cnt[lane * E + x];
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
       }
-      s.rtot[tid] = run;
+      s.cnt[lane * E + x] = static_cast<uint16_t>(incl - v);
+      if (lane == 31) s.rtot[x] = incl;
     }
     __syncthreads();
     if (e >= 0) sorted_ids[s.off[e] + s.cursor[e] + my_cnt[e] + rank] = static_cast<int32_t>(i);
