@@ -77,6 +77,7 @@ int ramp_device_ok(void);
  *                      >= ramp_align_capacity(n_assign, E, bm)
  *   tile_expert[cap/bm] expert of each bm-row M-tile
  *   n_post_pad[1]      total padded length (sum_e ceil(c_e/bm)*bm)
+ * E <= 512.
  * Replaces: the M-tile count inside grid_size / m_tile_counts
  * (ramp/routing.py:191-203) and the routing bincount of PAPER.md:761-762. */
 int ramp_moe_align(const int32_t* topk_ids, int64_t n_assign, int32_t E, int32_t bm,

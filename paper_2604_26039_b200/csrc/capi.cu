@@ -101,7 +101,7 @@ int64_t ramp_config_smem_bytes(int32_t bm, int32_t ttn, int32_t stg, int32_t mod
 
 int ramp_moe_align(const int32_t* topk_ids, int64_t n_assign, int32_t E, int32_t bm, int32_t* hist,
                    int32_t* sorted_ids, int32_t* tile_expert, int32_t* n_post_pad, void* stream) {
-  if (E < 1 || E > ramp::kMaxExperts) return fail(RAMP_EINVAL, "E must be in [1, 1024]");
+  if (E < 1 || E > ramp::kMaxExperts) return fail(RAMP_EINVAL, "E must be in [1, 512]");
   if (bm < 1) return fail(RAMP_EINVAL, "bm must be >= 1");
   if (n_assign < 0 || n_assign >= (int64_t(1) << 31) - (int64_t)E * bm)
     return fail(RAMP_EINVAL, "n_assign out of range");
@@ -116,7 +116,7 @@ int ramp_moe_align(const int32_t* topk_ids, int64_t n_assign, int32_t E, int32_t
 int ramp_dispatch_select(const int32_t* hist, int32_t E, const ramp_table_t* table, int32_t* cfg_out,
                          int32_t* n_eval_out, int64_t* grid_out, double* pred_out, void* stream) {
   if (int rc = check_table(table)) return rc;
-  if (E < 1 || E > ramp::kMaxExperts) return fail(RAMP_EINVAL, "E must be in [1, 1024]");
+  if (E < 1 || E > ramp::kMaxExperts) return fail(RAMP_EINVAL, "E must be in [1, 512]");
   if (!hist || !cfg_out) return fail(RAMP_EINVAL, "null buffer");
   cudaError_t err = ramp::launch_select(hist, E, *table, cfg_out, n_eval_out, grid_out, pred_out,
                                         static_cast<cudaStream_t>(stream));
@@ -135,7 +135,7 @@ int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const flo
                         void* workspace, size_t workspace_bytes, void* stream) {
   if (int rc = check_table(table)) return rc;
   if (S < 0) return fail(RAMP_EINVAL, "S must be >= 0");
-  if (E < 1 || E > ramp::kMaxExperts) return fail(RAMP_EINVAL, "E must be in [1, 1024]");
+  if (E < 1 || E > ramp::kMaxExperts) return fail(RAMP_EINVAL, "E must be in [1, 512]");
   if (top_k < 1 || top_k > E) return fail(RAMP_EINVAL, "top_k must be in [1, E]");
   if (H < 128 || H % 128 != 0) return fail(RAMP_EINVAL, "H (d_model) must be a positive multiple of 128");
   if (I < 128 || I % 128 != 0) return fail(RAMP_EINVAL, "I (d_ff) must be a positive multiple of 128");

@@ -592,10 +592,21 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
                   __float2bfloat16(silu_mul(g[q], u[q]));
             }
           } else {
-            __nv_bfloat16* dst = p.act_g + static_cast<size_t>(row0 + j0) * p.I + jb.s * G.n_i + f;
+            // lanes (f, f+1) swap one value per token pair so each lane writes
+            // a packed bf16x2 (4 B) instead of two 2-byte stores
+            const bool odd = f & 1;
+            __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(
+                p.act_g + static_cast<size_t>(row0 + j0) * p.I + jb.s * G.n_i + (f & ~1));
 #pragma unroll
-            for (int q = 0; q < 16; ++q)
-              if (j0 + q < G.bm) dst[static_cast<size_t>(q) * p.I] = __float2bfloat16(silu_mul(g[q], u[q]));
+            for (int m2 = 0; m2 < 8; ++m2) {
+              const float a0 = silu_mul(g[2 * m2], u[2 * m2]);
+              const float a1 = silu_mul(g[2 * m2 + 1], u[2 * m2 + 1]);
+              const float recv = __shfl_xor_sync(0xffffffffu, odd ? a0 : a1, 1);
+              const int q = 2 * m2 + (odd ? 1 : 0);
+              if (j0 + q < G.bm)
+                dst[static_cast<size_t>(q) * (p.I / 2)] = odd ? __floats2bfloat162_rn(recv, a1)
+                                                             : __floats2bfloat162_rn(a0, recv);
+            }
           }
         };
         if (nA == 1) {

@@ -69,11 +69,11 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   }
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ RouteStatic st;
-  RouteSmem s = carve_route_smem(dyn, a.E);
+  RouteSmem s = carve_route_smem(dyn, a.E, a.n_assign);
   stamp(0);
   if (threadIdx.x == 0) st.bad = 0;
   __syncthreads();
-  block_histogram(a.topk_ids, a.n_assign, a.E, s.hist, &st.bad);
+  block_count(a.topk_ids, a.n_assign, a.E, s, &st.bad);
   stamp(1);
   int sel = a.forced_cfg;
   int n_eval = 0;
@@ -122,10 +122,10 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ int warp_tot[32];
   __shared__ int bad;
-  RouteSmem s = carve_route_smem(dyn, E);
+  RouteSmem s = carve_route_smem(dyn, E, n);
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
-  block_histogram(ids, n, E, s.hist, &bad);
+  block_count(ids, n, E, s, &bad);
   block_align(ids, n, E, bm, s, warp_tot, sorted_ids, tile_expert, n_post_pad);
   for (int e = threadIdx.x; e < E; e += blockDim.x) hist_out[e] = s.hist[e];
 }
@@ -143,11 +143,11 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
 }
 
 cudaError_t launch_route(const RouteArgs& a, int zero_blocks, cudaStream_t stream) {
-  const size_t smem = route_smem_bytes(a.E);
+  const size_t smem = route_smem_bytes(a.E, a.n_assign);
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t err = cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)route_smem_bytes(kMaxExperts));
+                                           (int)route_smem_bytes(kMaxExperts, kIdCache));
     if (err != cudaSuccess) return err;
     attr_set = true;
   }
@@ -160,11 +160,11 @@ cudaError_t launch_align(const int32_t* ids, int64_t n, int E, int bm, int32_t* 
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t err = cudaFuncSetAttribute(align_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)route_smem_bytes(kMaxExperts));
+                                           (int)route_smem_bytes(kMaxExperts, kIdCache));
     if (err != cudaSuccess) return err;
     attr_set = true;
   }
-  align_kernel<<<1, kRouteThreads, route_smem_bytes(E), stream>>>(ids, n, E, bm, hist, sorted_ids,
+  align_kernel<<<1, kRouteThreads, route_smem_bytes(E, n), stream>>>(ids, n, E, bm, hist, sorted_ids,
                                                                   tile_expert, n_post_pad);
   return cudaGetLastError();
 }

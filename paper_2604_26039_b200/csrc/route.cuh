@@ -13,46 +13,79 @@ namespace ramp {
 
 constexpr int kRouteThreads = 1024;
 constexpr int kRouteWarps = kRouteThreads / 32;
-constexpr int kMaxExperts = 1024;
+constexpr int kMaxExperts = 512;
 constexpr int kMaxUbm = 128;
+constexpr int kIdCache = 16384;  // topk ids kept in shared memory between the two passes
 
-// Dynamic shared memory layout of the route block (sized by E).
+// Dynamic shared memory layout of the route block (sized by E and n).
+//   hist[E]       bincount
+//   off[E+1]      exclusive scan of the padded counts
+//   cnt[E][32]    per-(expert, warp) counts, then exclusive prefixes over warps
+//   ids[min(n, kIdCache)]
 struct RouteSmem {
-  int32_t* hist;      // [E]      bincount
-  int32_t* off;       // [E+1]    exclusive scan of padded counts
-  int32_t* cursor;    // [E]      running within-expert rank across rounds
-  int32_t* rtot;      // [E]      per-round totals
-  uint16_t* cnt;      // [32][E]  per-warp counts -> per-warp prefixes
+  int32_t* hist;
+  int32_t* off;
+  int32_t* cnt;
+  int32_t* ids;
+  bool cached;
 };
 
-__host__ __device__ inline size_t route_smem_bytes(int E) {
-  return sizeof(int32_t) * (4 * (size_t)E + 1) + sizeof(uint16_t) * 32 * (size_t)E + 64;
+__host__ __device__ inline size_t route_smem_bytes(int E, int64_t n) {
+  const int64_t cache = n <= kIdCache ? n : 0;
+  return sizeof(int32_t) * ((size_t)E * 34 + 1 + (size_t)cache) + 64;
 }
 
-__device__ inline RouteSmem carve_route_smem(unsigned char* base, int E) {
+__device__ inline RouteSmem carve_route_smem(unsigned char* base, int E, int64_t n) {
   RouteSmem s;
   s.hist = reinterpret_cast<int32_t*>(base);
   s.off = s.hist + E;
-  s.cursor = s.off + E + 1;
-  s.rtot = s.cursor + E;
-  s.cnt = reinterpret_cast<uint16_t*>(s.rtot + E);
+  s.cnt = s.off + E + 1;
+  s.ids = s.cnt + 32 * E;
+  s.cached = n <= kIdCache;
   return s;
 }
 
 // --------------------------------------------------------------- histogram
-// bincount(topk_ids, minlength=E) into shared memory.  Ids outside [0, E)
-// set *bad (the reference's ExpertHistogram rejects them, ramp/routing.py:45-50).
-__device__ inline void block_histogram(const int32_t* __restrict__ ids, int64_t n, int E,
-                                       int32_t* hist, int* bad) {
-  for (int e = threadIdx.x; e < E; e += blockDim.x) hist[e] = 0;
+// Pass 1 of the stable counting sort.  The n flat assignments are cut into 32
+// contiguous segments, one per warp; each warp counts its segment per expert
+// (warp-aggregated with match.any, no atomics: the warp owns column w of
+// cnt), then one warp scan per expert turns the 32 counts into exclusive
+// prefixes and the total, i.e. bincount(topk_ids, minlength=E).
+// Ids outside [0, E) set *bad (ExpertHistogram rejects them, ramp/routing.py:45-50).
+__device__ inline void block_count(const int32_t* __restrict__ ids, int64_t n, int E, RouteSmem& s,
+                                   int* bad) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (s.cached)
+    for (int64_t i = tid; i < n; i += blockDim.x) s.ids[i] = __ldg(ids + i);
+  for (int x = tid; x < 32 * E; x += blockDim.x) s.cnt[x] = 0;
   __syncthreads();
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    int e = __ldg(ids + i);
-    if (e < 0 || e >= E) {
-      *bad = 1;
-      continue;
+  const int64_t seg = (n + kRouteWarps - 1) / kRouteWarps;
+  const int64_t lo = warp * seg, hi = lo + seg < n ? lo + seg : n;
+  for (int64_t c0 = lo; c0 < hi; c0 += 32) {
+    const int64_t i = c0 + lane;
+    int e = -1;
+    if (i < hi) {
+      e = s.cached ? s.ids[i] : __ldg(ids + i);
+      if (e < 0 || e >= E) {
+        *bad = 1;
+        e = -1;
+      }
     }
-    atomicAdd(hist + e, 1);
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    if (e >= 0 && __popc(peers & ((1u << lane) - 1u)) == 0) s.cnt[e * 32 + warp] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int x = warp; x < E; x += kRouteWarps) {
+    const int v = s.cnt[x * 32 + lane];
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    s.cnt[x * 32 + lane] = incl - v;
+    if (lane == 31) s.hist[x] = incl;
   }
   __syncthreads();
 }
@@ -177,11 +210,11 @@ __device__ inline int block_exclusive_scan(int v, int* warp_tot /*[32]*/, int* t
   return before;
 }
 
-// moe_align_block_size: stable counting sort of the flat assignment indices
-// by expert; each expert's run padded to a multiple of bm with the sentinel
-// n (== S*top_k).  Within an expert, indices ascend (a deterministic order we
-// define; the reference has no alignment code).
-// Requires blockDim.x == 1024 and E <= 1024.
+// moe_align_block_size, pass 2 of the stable counting sort: flat assignment
+// indices grouped by expert, ascending within an expert, each expert's run
+// padded to a multiple of bm with the sentinel n (== S*top_k).  (The
+// reference has no alignment code; this order is our contract.)
+// Requires blockDim.x == 1024, E <= kMaxExperts and block_count() first.
 __device__ inline void block_align(const int32_t* __restrict__ ids, int64_t n, int E, int bm,
                                    RouteSmem& s, int* warp_tot, int32_t* __restrict__ sorted_ids,
                                    int32_t* __restrict__ tile_expert, int32_t* n_post_pad_out) {
@@ -195,9 +228,7 @@ __device__ inline void block_align(const int32_t* __restrict__ ids, int64_t n, i
   const int off = block_exclusive_scan(padded, warp_tot, &total);
   if (tid < E) {
     s.off[tid] = off;
-    s.cursor[tid] = 0;
-    // padding slots and per-tile expert ids
-    for (int p = off + c; p < off + padded; ++p) sorted_ids[p] = static_cast<int32_t>(n);
+    for (int q = off + c; q < off + padded; ++q) sorted_ids[q] = static_cast<int32_t>(n);
     for (int tt = off / bm; tt < (off + padded) / bm; ++tt) tile_expert[tt] = tid;
   }
   if (tid == 0) {
@@ -205,35 +236,27 @@ __device__ inline void block_align(const int32_t* __restrict__ ids, int64_t n, i
     if (n_post_pad_out) *n_post_pad_out = total;
   }
   __syncthreads();
-
-  const unsigned lt_mask = (1u << lane) - 1u;
-  uint16_t* my_cnt = s.cnt + warp * E;
-  for (int64_t base = 0; base < n; base += blockDim.x) {
-    const int64_t i = base + tid;
-    int e = i < n ? __ldg(ids + i) : -1;
-    if (e >= E) e = -1;  // invalid ids were flagged by block_histogram
-    for (int x = lane; x < E; x += 32) my_cnt[x] = 0;
-    __syncwarp();
-    const unsigned peers = __match_any_sync(0xffffffffu, e);
-    const int rank = __popc(peers & lt_mask);
-    if (e >= 0 && rank == 0) my_cnt[e] = static_cast<uint16_t>(__popc(peers));
-    __syncthreads();
-    // per-expert exclusive prefix over the 32 warps: one warp scan per expert
-    for (int x = warp; x < E; x += kRouteWarps) {
-      const int v = s.cnt[lane * E + x];
-      int incl = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      s.cnt[lane * E + x] = static_cast<uint16_t>(incl - v);
-      if (lane == 31) s.rtot[x] = incl;
+  // each warp walks its segment again in order; position = expert base +
+  // earlier warps' count + this warp's running count + rank within the chunk
+  const int64_t seg = (n + kRouteWarps - 1) / kRouteWarps;
+  const int64_t lo = warp * seg, hi = lo + seg < n ? lo + seg : n;
+  for (int64_t c0 = lo; c0 < hi; c0 += 32) {
+    const int64_t i = c0 + lane;
+    int e = -1;
+    if (i < hi) {
+      e = s.cached ? s.ids[i] : __ldg(ids + i);
+      if (e < 0 || e >= E) e = -1;
     }
-    __syncthreads();
-    if (e >= 0) sorted_ids[s.off[e] + s.cursor[e] + my_cnt[e] + rank] = static_cast<int32_t>(i);
-    __syncthreads();
-    if (tid < E) s.cursor[tid] += s.rtot[tid];
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    int base = 0;
+    if (e >= 0) {
+      base = s.cnt[e * 32 + warp];
+      sorted_ids[s.off[e] + base + rank] = static_cast<int32_t>(i);
+    }
+    __syncwarp();
+    if (e >= 0 && rank == 0) s.cnt[e * 32 + warp] = base + __popc(peers);
+    __syncwarp();
   }
   __syncthreads();
 }

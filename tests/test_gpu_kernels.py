@@ -55,7 +55,9 @@ ALIGN_CASES = [
     (333, 8, 128, 16, "dup"),
     (4096, 2, 8, 128, "distinct"),
     (3, 1, 1, 4, "distinct"),
-    (2000, 8, 1024, 8, "dup"),
+    (2000, 8, 512, 8, "dup"),
+    (3000, 8, 256, 128, "skew"),
+    (2100, 8, 64, 4, "distinct"),
 ]
 
 
