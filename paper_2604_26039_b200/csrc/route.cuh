@@ -71,9 +71,7 @@ __device__ inline void block_count(const int32_t* __restrict__ ids, int64_t n, i
         e = -1;
       }
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, e);
-    if (e >= 0 && __popc(peers & ((1u << lane) - 1u)) == 0) s.cnt[e * 32 + warp] += __popc(peers);
-    __syncwarp();
+    if (e >= 0) atomicAdd(s.cnt + e * 32 + warp, 1);  // counts commute: no ordering needed here
   }
   __syncthreads();
   for (int x = warp; x < E; x += kRouteWarps) {
