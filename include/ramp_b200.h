@@ -118,6 +118,17 @@ int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const flo
                         int32_t top_k, const ramp_table_t* table, int32_t forced_cfg, void* out,
                         int32_t* sel_out, void* workspace, size_t workspace_bytes, void* stream);
 
+/* The two launches of ramp_fused_moe_bf16 separately, on the same arguments
+ * and workspace: phases = 1 runs only the route kernel (histogram, dispatch,
+ * alignment), 2 only the megakernel (which reads the route kernel's outputs
+ * from the workspace), 3 both.  Lets a caller time the megakernel alone or
+ * reuse one routing decision for several layers that share the histogram. */
+int ramp_fused_moe_bf16_ex(const void* x, const void* w1, const void* w2, const float* topk_w,
+                           const int32_t* topk_ids, int32_t S, int32_t H, int32_t I, int32_t E,
+                           int32_t top_k, const ramp_table_t* table, int32_t forced_cfg, void* out,
+                           int32_t* sel_out, void* workspace, size_t workspace_bytes, int32_t phases,
+                           void* stream);
+
 /* Shared-memory bytes the megakernel needs for (bm, ttn, stg, mode); 0 if the
  * configuration is not realisable on this part (pool admissibility test,
  * the B200 counterpart of smem_usage/is_valid, ramp/config_space.py:122-138). */

@@ -42,6 +42,8 @@ SIGNATURES = {
          ctypes.c_size_t, ctypes.c_void_p],
     ),
 }
+SIGNATURES["ramp_fused_moe_bf16_ex"] = (
+    ctypes.c_int, SIGNATURES["ramp_fused_moe_bf16"][1][:-1] + [ctypes.c_int32, ctypes.c_void_p])
 
 
 class RampTable(ctypes.Structure):

@@ -129,10 +129,11 @@ size_t ramp_fused_moe_workspace_size(int32_t S, int32_t H, int32_t I, int32_t E,
   return layout_for(S, H, I, E, top_k).total;
 }
 
-int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const float* topk_w,
-                        const int32_t* topk_ids, int32_t S, int32_t H, int32_t I, int32_t E, int32_t top_k,
-                        const ramp_table_t* table, int32_t forced_cfg, void* out, int32_t* sel_out,
-                        void* workspace, size_t workspace_bytes, void* stream) {
+int ramp_fused_moe_bf16_ex(const void* x, const void* w1, const void* w2, const float* topk_w,
+                           const int32_t* topk_ids, int32_t S, int32_t H, int32_t I, int32_t E, int32_t top_k,
+                           const ramp_table_t* table, int32_t forced_cfg, void* out, int32_t* sel_out,
+                           void* workspace, size_t workspace_bytes, int32_t phases, void* stream) {
+  if (phases < 1 || phases > 3) return fail(RAMP_EINVAL, "phases must be 1 (route), 2 (megakernel) or 3");
   if (int rc = check_table(table)) return rc;
   if (S < 0) return fail(RAMP_EINVAL, "S must be >= 0");
   if (E < 1 || E > ramp::kMaxExperts) return fail(RAMP_EINVAL, "E must be in [1, 512]");
@@ -182,8 +183,12 @@ int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const flo
   ra.H = H;
   ra.top_k = top_k;
   const int zero_blocks = 0;
-  cudaError_t err = ramp::launch_route(ra, zero_blocks, st);
-  if (err != cudaSuccess) return cuda_fail(err, "route kernel");
+  cudaError_t err = cudaSuccess;
+  if (phases & 1) {
+    err = ramp::launch_route(ra, zero_blocks, st);
+    if (err != cudaSuccess) return cuda_fail(err, "route kernel");
+  }
+  if (!(phases & 2)) return RAMP_OK;
 
   ramp::MoeLaunch ml{};
   ml.x = x;
@@ -210,6 +215,14 @@ int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const flo
   err = ramp::launch_fused_moe_bf16(ml, st, &why);
   if (err != cudaSuccess) return why ? fail(RAMP_ECUDA, why) : cuda_fail(err, "fused_moe kernel");
   return RAMP_OK;
+}
+
+int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const float* topk_w,
+                        const int32_t* topk_ids, int32_t S, int32_t H, int32_t I, int32_t E, int32_t top_k,
+                        const ramp_table_t* table, int32_t forced_cfg, void* out, int32_t* sel_out,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+  return ramp_fused_moe_bf16_ex(x, w1, w2, topk_w, topk_ids, S, H, I, E, top_k, table, forced_cfg, out, sel_out,
+                                workspace, workspace_bytes, 3, stream);
 }
 
 }  // extern "C"

@@ -45,6 +45,26 @@ __device__ inline RouteSmem carve_route_smem(unsigned char* base, int E, int64_t
   return s;
 }
 
+// Lanes of the warp holding the same value e (e < 0 marks an empty lane):
+// __match_any_sync rebuilt from one ballot per bit of e, which is much
+// cheaper than MATCH.ANY when the warp holds many distinct experts.
+__device__ __forceinline__ unsigned match_peers(int e, int nbits) {
+  unsigned peers = 0xffffffffu;
+  for (int b = 0; b < nbits; ++b) {
+    const bool bit = (e >> b) & 1;
+    const unsigned m = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? m : ~m;
+  }
+  const unsigned empty = __ballot_sync(0xffffffffu, e < 0);
+  return peers & (e < 0 ? empty : ~empty);
+}
+
+__host__ __device__ inline int bits_for(int E) {
+  int b = 0;
+  while ((1 << b) < E) ++b;
+  return b;
+}
+
 // --------------------------------------------------------------- histogram
 // Pass 1 of the stable counting sort.  The n flat assignments are cut into 32
 // contiguous segments, one per warp; each warp counts its segment per expert
@@ -236,6 +256,7 @@ __device__ inline void block_align(const int32_t* __restrict__ ids, int64_t n, i
   __syncthreads();
   // each warp walks its segment again in order; position = expert base +
   // earlier warps' count + this warp's running count + rank within the chunk
+  const int nbits = bits_for(E);
   const int64_t seg = (n + kRouteWarps - 1) / kRouteWarps;
   const int64_t lo = warp * seg, hi = lo + seg < n ? lo + seg : n;
   for (int64_t c0 = lo; c0 < hi; c0 += 32) {
@@ -245,7 +266,7 @@ __device__ inline void block_align(const int32_t* __restrict__ ids, int64_t n, i
       e = s.cached ? s.ids[i] : __ldg(ids + i);
       if (e < 0 || e >= E) e = -1;
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const unsigned peers = match_peers(e, nbits);
     const int rank = __popc(peers & ((1u << lane) - 1u));
     int base = 0;
     if (e >= 0) {

@@ -118,6 +118,7 @@ def fused_moe(
     forced_cfg: int = -1,
     out: torch.Tensor | None = None,
     workspace: Workspace | None = None,
+    phases: int = 3,
 ) -> torch.Tensor:
     """Fused MoE layer forward, BF16:
 
@@ -128,7 +129,8 @@ def fused_moe(
     int32.  `forced_cfg < 0` lets the on-device dispatcher choose the tile
     config from the live histogram; a config id forces it (static dispatch or
     the exhaustive sweep).  The selection record {cfg, n_post_pad, n_mtiles,
-    n_eval} is left in `workspace.sel` (device int32[4]).
+    n_eval} is left in `workspace.sel` (device int32[4]).  `phases` = 1 / 2
+    runs only the route kernel / only the megakernel (ramp_fused_moe_bf16_ex).
     """
     lib = _lib.load()
     S, H = hidden_states.shape
@@ -153,10 +155,10 @@ def fused_moe(
     if workspace is None or not workspace.fits(S, H, I, E, k):
         workspace = Workspace(S, H, I, E, k, device=hidden_states.device)
     _lib.check(
-        lib.ramp_fused_moe_bf16(
+        lib.ramp_fused_moe_bf16_ex(
             hidden_states.data_ptr(), w1.data_ptr(), w2.data_ptr(), topk_weights.data_ptr(),
             topk_ids.data_ptr(), S, H, I, E, k, table.ref, int(forced_cfg), out.data_ptr(),
-            workspace.sel.data_ptr(), workspace.buf.data_ptr(), workspace.buf.numel(), _stream(),
+            workspace.sel.data_ptr(), workspace.buf.data_ptr(), workspace.buf.numel(), int(phases), _stream(),
         )
     )
     return out

@@ -1,0 +1,94 @@
+"""One-time B200 profiling sweep -> reference-format trace -> P4 fit -> coeffs.
+
+    python scripts/profile_b200.py --model OLMoE-1B-7B [--plan-reps 3] [--iters 3]
+
+This is the RaMP offline step run on the real megakernel:
+for every (S, beta) point of ramp's profiling plan (5 batch sizes x 5 skews,
+ramp/cost_model.py:212-231) and every routing seed, every config of the B200
+pool is launched and timed (sweep.MeasuredTimer), the samples are written in
+ramp's trace CSV schema (loadable by ramp.load_trace), and each config's four
+coefficients are fitted with the reference's OLS (cost_model.fit, variant P4).
+Outputs (under paper_2604_26039_b200/data/ unless --out is given):
+    trace_<model>_b200.csv, coeffs_<model>_b200.json, fit_<model>_b200.json
+Then it evaluates the fitted table against an exhaustive on-GPU sweep over the
+reference's held-out test points: regret_<model>_b200.csv / speedup_... .csv
+and a JSON summary.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+from paper_2604_26039_b200.catalog import BASELINE_MODELS  # noqa: E402
+from paper_2604_26039_b200.config_space import HardwareModel, enumerate_b200_configs  # noqa: E402
+from paper_2604_26039_b200.cost_model import coeff_store_dict, fit, profiling_plan, write_coeff_store  # noqa: E402
+from paper_2604_26039_b200.dispatch import DispatchTable, evaluate_regret, speedup_ra_vs_static  # noqa: E402
+from paper_2604_26039_b200.moe import DeviceTable  # noqa: E402
+from paper_2604_26039_b200.sweep import MeasuredTimer  # noqa: E402
+from paper_2604_26039_b200.trace import profile  # noqa: E402
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="OLMoE-1B-7B", choices=sorted(BASELINE_MODELS))
+    ap.add_argument("--plan-reps", type=int, default=3)
+    ap.add_argument("--eval-reps", type=int, default=2)
+    ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--out", default=str(ROOT / "paper_2604_26039_b200" / "data"))
+    ap.add_argument("--skip-eval", action="store_true")
+    a = ap.parse_args()
+    out = Path(a.out)
+    out.mkdir(parents=True, exist_ok=True)
+    geom = BASELINE_MODELS[a.model]
+    hw = HardwareModel.b200()
+    pool = enumerate_b200_configs(geom, hw)
+    cols = pool.columns()
+    n = len(pool)
+    flat = DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
+                       group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], a=np.ones(n),
+                       b=np.zeros(n), c=np.zeros(n), d=np.zeros(n), N=geom.N, kappa_ok=False,
+                       sm_count=hw.sm_count)
+    timer = MeasuredTimer(geom, flat, iters=a.iters)
+    plan = profiling_plan(geom)
+    tag = f"{a.model}_b200"
+    trace_path = out / f"trace_{tag}.csv"
+    if trace_path.exists():
+        trace_path.unlink()
+    t0 = time.time()
+    trace = profile(pool, geom, plan, timer, seeds_per_point=a.plan_reps, trace_path=trace_path)
+    t_prof = time.time() - t0
+    by_cfg: dict[int, list] = {}
+    for s in trace.samples:
+        by_cfg.setdefault(s.config_id, []).append(s)
+    reports = {cid: fit(ss, hw, "P4") for cid, ss in by_cfg.items()}
+    write_coeff_store(out / f"coeffs_{tag}.json", coeff_store_dict(a.model, hw.sm_count, reports))
+    r2 = np.array([r.r_squared for r in reports.values()])
+    summary = {"model": a.model, "pool": n, "plan_points": len(plan), "samples": len(trace.samples),
+               "profile_s": round(t_prof, 1), "r2_median": float(np.median(r2)), "r2_min": float(r2.min())}
+    print(json.dumps(summary), flush=True)
+    if not a.skip_eval:
+        table = DispatchTable(model=a.model, pool=pool,
+                              coefficients={c: r.coefficients for c, r in reports.items()},
+                              sm_count=hw.sm_count)
+        t0 = time.time()
+        reg = evaluate_regret(table, pool, geom, timer, seeds_per_point=a.eval_reps)
+        spd = speedup_ra_vs_static(table, pool, geom, timer, seeds_per_point=a.eval_reps)
+        (out / f"regret_{tag}.csv").write_text(reg.to_csv())
+        (out / f"speedup_{tag}.csv").write_text(spd.to_csv())
+        summary.update({"eval_s": round(time.time() - t0, 1), "regret": reg.aggregate(),
+                        "speedup": spd.aggregate()})
+        print(json.dumps({"regret": reg.aggregate(), "speedup": spd.aggregate()}), flush=True)
+    (out / f"fit_{tag}.json").write_text(json.dumps(summary, indent=2) + "\n")
+
+
+if __name__ == "__main__":
+    main()
