@@ -1,0 +1,207 @@
+"""The product's host-side mirror of the reference API (paper_2604_26039_b200)
+against the reference's own outputs and the oracle -- CPU only.
+
+The regret / speedup harness is checked by feeding it the oracle's
+restatement of the reference simulator and the oracle's selector: it must
+reproduce the reference's CSV reports byte for byte (tests/golden/eval.json).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+from oracle import ramp_ref as R
+from paper_2604_26039_b200 import catalog as C
+from paper_2604_26039_b200 import config_space as CS
+from paper_2604_26039_b200 import cost_model as CM
+from paper_2604_26039_b200 import dispatch as D
+from paper_2604_26039_b200 import routing as RT
+from paper_2604_26039_b200 import trace as T
+from tests._util import GEOMS, golden
+from tests.test_oracle_golden import _geom_ENK
+
+
+def _geom(name):
+    E, N, K = _geom_ENK(name)
+    k = GEOMS.get(name, {}).get("top_k", 8)
+    return C.MoeGeometry(name=name, E=E, N=N, K=K, top_k=k)
+
+
+def test_sampler_and_balancedness_bit_exact():
+    for s in golden("histograms.json")["samples"]:
+        if "unreachable" in s:
+            with pytest.raises(RT.BetaUnreachableError):
+                RT.sample_histogram(s["E"], s["S"], s["top_k"], s["beta"], int(s["seed"]))
+            continue
+        smp = RT.sample_histogram(s["E"], s["S"], s["top_k"], s["beta"], int(s["seed"]))
+        assert list(smp.histogram.counts) == s["counts"]
+        assert smp.beta_achieved == pytest.approx(s["beta_achieved"], rel=1e-12, abs=1e-12)
+    for row in golden("histograms.json")["balancedness"]:
+        assert RT.balancedness(RT.ExpertHistogram(tuple(row["counts"]))) == pytest.approx(row["beta"], rel=1e-12)
+
+
+def test_sampler_argument_errors():
+    with pytest.raises(ValueError, match="S must be"):
+        RT.sample_histogram(4, 0, 2, 0.5, 0)
+    with pytest.raises(ValueError, match="top_k must be"):
+        RT.sample_histogram(4, 8, 0, 0.5, 0)
+    with pytest.raises(ValueError, match="beta_target must be"):
+        RT.sample_histogram(4, 8, 2, 1.5, 0)
+    with pytest.raises(RT.BetaUnreachableError, match="E=1"):
+        RT.sample_histogram(1, 8, 2, 0.5, 0)
+
+
+@pytest.mark.parametrize("entry", range(len(golden("pools.json"))))
+def test_reference_pool_mirror(entry):
+    e = golden("pools.json")[entry]
+    g = _geom(e["geom"])
+    hw = CS.HardwareModel.b200() if e["hw"] == "b200" else CS.HardwareModel()
+    pool = CS.enumerate_configs(g, hw, C.classify_regime(C.region_variables(g)))
+    cols = {k: [int(getattr(c, k)) for c in pool] for k in ("bm", "bn", "wn", "stg", "ttn", "group_m", "split_k")}
+    assert len(pool) == e["size"]
+    assert hashlib.sha256(json.dumps(cols, sort_keys=True).encode()).hexdigest() == e["digest"]
+
+
+def test_catalog_classification():
+    for g in C.load_catalog():
+        v = C.region_variables(g)
+        rep = C.classify_regime(v)
+        rho, lam, kappa, regime, modes = C.EXPECTED_CLASSIFICATION[g.name]
+        assert (int(v.rho), v.lam, int(v.kappa), rep.regime, rep.predicted_modes) == (rho, lam, kappa, regime, modes)
+
+
+def test_pool_grids_mirror():
+    for e in golden("grids.json"):
+        g = _geom(e["geom"])
+        hw = CS.HardwareModel.b200() if e["hw"] == "b200" else CS.HardwareModel()
+        pool = CS.enumerate_configs(g, hw, C.classify_regime(C.region_variables(g)))
+        hist = RT.ExpertHistogram(tuple(e["counts"]))
+        assert RT.pool_grids(pool, hist).tolist() == e["grids"]
+        for cfg in list(pool)[::97]:
+            assert RT.grid_size(cfg, hist, g) == e["grids"][cfg.id]
+
+
+def test_fit_mirror():
+    for f in golden("fits.json"):
+        samples = [CM.ProfilingSample(config_id=0, S=8, beta_target=0.5, seed=i, g=g, time_us=t)
+                   for i, (g, t) in enumerate(zip(f["g"], f["t"]))]
+        rep = CM.fit(samples, CS.HardwareModel(), f["variant"])
+        co = rep.coefficients
+        for key in ("a", "b", "c", "d"):
+            assert getattr(co, key) == pytest.approx(f[key], rel=1e-9, abs=1e-9)
+        assert co.uses_log == f["uses_log"]
+        assert rep.condition_flag == f["condition_flag"]
+        assert rep.r_squared == pytest.approx(f["r_squared"], rel=1e-9, abs=1e-12)
+
+
+def test_predict_scalar_and_batch():
+    co = CM.CostCoefficients(a=10.0, b=3.0, c=0.25, d=1.5, uses_log=True, variant="P4")
+    hw = CS.HardwareModel()
+    assert CM.predict(co, 100, hw) == pytest.approx(10 + 3 + 25 + 1.5 * np.log(101))
+    got = CM.predict_batch(np.array([10.0]), np.array([3.0]), np.array([0.25]), np.array([1.5]), [100], 132)
+    assert got[0] == pytest.approx(10 + 3 + 25 + 1.5 * np.log(101))
+
+
+def test_step_cache_contract():
+    cache = D.StepCache()
+    cache.advance(0)
+    cache.selection[64] = 5
+    cache.advance(0)
+    assert cache.selection == {64: 5}
+    cache.advance(1)
+    assert cache.selection == {}
+
+
+def test_plans_and_test_points():
+    g = _geom("OLMoE")
+    assert CM.profiling_plan(g) == [tuple(p) for p in CM.profiling_plan(g)]
+    assert [list(p) for p in D.default_test_points(g)] == golden("eval.json")["default_test_points"]
+
+
+class OracleTimer:
+    """The reference simulator (via the oracle restatement) behind the
+    product's timer interface."""
+
+    def __init__(self, pool, geom, params):
+        self.cfgs = [dict(bm=c.bm, ttn=c.ttn, stg=c.stg, group_m=c.group_m, split_k=c.split_k) for c in pool]
+        self.geom, self.params = geom, params
+
+    def quiet(self):
+        return OracleTimer.__new__(OracleTimer).__init_from(self)
+
+    def __init_from(self, other):
+        self.cfgs, self.geom = other.cfgs, other.geom
+        self.params = dict(other.params, noise_cv=0.0)
+        return self
+
+    def pool_times(self, pool, hist, point_seed, shared_noise=False, grids=None):
+        return R.sim_pool_times(self.cfgs, list(hist.counts), self.geom.N, self.geom.K, self.params, point_seed,
+                                shared_noise=shared_noise)
+
+
+def _olmoe_table():
+    g = _geom("OLMoE")
+    pool = CS.enumerate_configs(g, CS.HardwareModel(), C.classify_regime(C.region_variables(g)))
+    tab = golden("tables.json")[0]
+    coeffs = {i: CM.CostCoefficients(a=c[0], b=c[1], c=c[2], d=c[3], uses_log=bool(c[4]), variant="P4")
+              for i, c in enumerate(tab["coeffs"])}
+    table = D.DispatchTable(model="OLMoE", pool=pool, coefficients=coeffs, sm_count=132)
+    coeff_list = tab["coeffs"]
+    cfgs = [dict(bm=c.bm, ttn=c.ttn, split_k=c.split_k) for c in pool]
+
+    def selector(_, hist):
+        return R.select(cfgs, coeff_list, list(hist.counts), g.N, 132, False)[0]
+
+    return g, pool, table, selector
+
+
+def test_regret_and_speedup_harness_reproduce_reference_reports():
+    g, pool, table, selector = _olmoe_table()
+    ev = golden("eval.json")
+    timer = OracleTimer(pool, g, R.SIM_DEFAULTS)
+    points = [tuple(p) for p in ev["points"]]
+    reg = D.evaluate_regret(table, pool, g, timer, test_points=points, seeds_per_point=2, selector=selector)
+    spd = D.speedup_ra_vs_static(table, pool, g, timer, points=points, seeds_per_point=2, selector=selector)
+    assert reg.to_csv() == ev["regret_csv"]
+    assert spd.to_csv() == ev["speedup_csv"]
+    assert D.static_best(pool, g, timer, [8, 64]) == ev["static_best_8_64"]
+
+
+def test_trace_round_trip_and_validation(tmp_path):
+    g, pool, table, _ = _olmoe_table()
+    timer = OracleTimer(pool, g, R.SIM_DEFAULTS)
+    plan = [(8, 0.5), (32, 1.0)]
+    path = tmp_path / "trace.csv"
+    tr = T.profile(pool, g, plan, timer, seeds_per_point=1, trace_path=path, provenance="simulator")
+    assert path.read_text().splitlines()[0] == T.TRACE_HEADER
+    back = T.load_trace(path, pool)
+    assert [(s.config_id, s.g, s.time_us) for s in back.samples] == [(s.config_id, s.g, s.time_us) for s in tr.samples]
+    T.profile(pool, g, plan, timer, seeds_per_point=1, trace_path=path)  # resume: identical, nothing appended
+    assert len(path.read_text().splitlines()) == 1 + len(tr.samples)
+    bad = tmp_path / "bad.csv"
+    bad.write_text(T.TRACE_HEADER + "\n0,8,0.5,1,5,-1.0\n")
+    with pytest.raises(ValueError, match="non-positive"):
+        T.load_trace(bad, pool)
+
+
+def test_topk_from_histogram_realises_counts():
+    for s in golden("histograms.json")["samples"][:60]:
+        if "counts" not in s:
+            continue
+        ids = RT.topk_from_histogram(s["counts"], s["S"], s["top_k"], 7)
+        assert ids.shape == (s["S"], s["top_k"])
+        assert np.bincount(ids.ravel(), minlength=s["E"]).tolist() == s["counts"]
+
+
+def test_b200_pool_is_kernel_admissible():
+    for name, g in C.BASELINE_MODELS.items():
+        pool = CS.enumerate_b200_configs(g)
+        assert len(pool) > 0
+        for c in pool:
+            assert CS.b200_smem_bytes(c.bm, c.ttn, c.stg, c.mode) <= CS.B200_SMEM_LIMIT
+            assert (g.N // 2) % (c.ttn // 2) == 0
+        assert [c.id for c in pool] == list(range(len(pool)))
