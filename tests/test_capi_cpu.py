@@ -1,0 +1,74 @@
+"""The C-ABI library loads without a GPU, exports every symbol the public
+header declares, and validates arguments before touching the device."""
+
+from __future__ import annotations
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2604_26039_b200 import _lib
+from paper_2604_26039_b200.config_space import B200_SMEM_LIMIT, b200_smem_bytes
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "ramp_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ramp_[a-z0-9_]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    return _lib.load()
+
+
+def test_every_declared_symbol_is_exported(lib):
+    syms = declared_symbols()
+    assert len(syms) >= 9
+    for s in syms:
+        assert hasattr(lib, s), s
+        assert s in _lib.SIGNATURES, f"{s} has no ctypes signature"
+
+
+def test_version_and_capacity(lib):
+    assert lib.ramp_version() >= 100
+    assert lib.ramp_align_capacity(8, 64, 16) == ((8 + 64 * 15 + 15) // 16) * 16
+    assert lib.ramp_align_capacity(-1, 64, 16) == 0
+
+
+def test_smem_formula_matches_python(lib):
+    for bm in (4, 8, 16, 32, 64, 128):
+        for ttn in (128, 256, 512):
+            for stg in range(1, 9):
+                for mode in (0, 1):
+                    want = b200_smem_bytes(bm, ttn, stg, mode)
+                    got = lib.ramp_config_smem_bytes(bm, ttn, stg, mode)
+                    assert got == (want if want <= B200_SMEM_LIMIT else 0), (bm, ttn, stg, mode)
+    assert lib.ramp_config_smem_bytes(4, 384, 2, 0) == 0
+
+
+def test_argument_validation_without_gpu(lib):
+    buf = (ctypes.c_int32 * 16)()
+    p = ctypes.cast(buf, ctypes.c_void_p)
+    rc = lib.ramp_moe_align(p, 8, 0, 16, p, p, p, p, None)
+    assert rc == 1 and b"E must be" in lib.ramp_last_error()
+    rc = lib.ramp_moe_align(p, 8, 64, 0, p, p, p, p, None)
+    assert rc == 1 and b"bm must be" in lib.ramp_last_error()
+    rc = lib.ramp_dispatch_select(p, 64, None, p, p, None, None, None)
+    assert rc == 1 and b"table is null" in lib.ramp_last_error()
+    t = _lib.RampTable()
+    rc = lib.ramp_dispatch_select(p, 64, ctypes.byref(t), p, p, None, None, None)
+    assert rc == 1 and b"empty pool" in lib.ramp_last_error()
+    with pytest.raises(ValueError):
+        _lib.check(1)
+
+
+def test_no_device_reported(lib):
+    import torch
+
+    if not torch.cuda.is_available():
+        assert lib.ramp_device_ok() == 0
