@@ -1,0 +1,403 @@
+"""Benchmark: the OLMoE-1B-7B fused-MoE layer sweep on B200 (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload ("step"): one pass over the beta x batch sweep of BASELINE.json
+configs[1] -- OLMoE-1B-7B (E=64, top-8, d=2048, d_ff=1024), BF16,
+S in {1,2,4,...,512} x beta in {0.2,0.5,1.0} (beta=1 is unreachable for
+S*k < E and dropped, as ramp.profiling_plan drops it) -- 27 layer calls, each
+routed by the on-device dispatcher (routing-aware, forced_cfg = -1).  The
+histograms are the reference's own evaluation draws
+(sample_histogram(E, S, 8, beta, derive_seed(42, 3, S, 1000*beta, 0))),
+expanded into concrete top-k ids; tokens, routing weights and expert weights
+are synthetic / random-init.  Every layer call uses the next of 8 resident
+copies of the expert weights (8 x 805 MB >> 126 MB L2), so weights are cold as
+in a real multi-layer model; no flush is needed inside the timed region.
+
+metric / value: whole-job TFLOP/s over the sweep (6*S*k*H*I per layer, all
+ranks' layers / max-over-ranks time); the per-point microseconds, the
+routing-aware-vs-static speedup and the dispatch regret against an
+exhaustive on-GPU sweep are reported beside it.  N > 1 runs independent
+replicas (the OLMoE layer is not expert-sharded).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+MODEL = "OLMoE-1B-7B"
+BATCHES = (1, 2, 4, 8, 16, 32, 64, 128, 256, 512)
+BETAS = (0.2, 0.5, 1.0)
+N_COPIES = 8
+METRIC = "fused-MoE layer TFLOP/s over the OLMoE-1B-7B beta x batch sweep (routing-aware dispatch)"
+
+
+def sweep_points(geom):
+    from paper_2604_26039_b200.dispatch import EVAL_HIST_DOMAIN, derive_seed
+    from paper_2604_26039_b200.routing import BetaUnreachableError, sample_histogram
+
+    pts = []
+    for S in BATCHES:
+        for beta in BETAS:
+            seed = derive_seed(42, EVAL_HIST_DOMAIN, S, round(beta * 1000), 0)
+            try:
+                hist = sample_histogram(geom.E, S, geom.top_k, beta, seed).histogram
+            except BetaUnreachableError:
+                continue
+            pts.append(dict(S=S, beta=beta, seed=seed, hist=hist))
+    return pts
+
+
+def layer_flops(geom, S):
+    return 6 * S * geom.top_k * geom.K * (geom.N // 2)
+
+
+def layer_bytes(geom, hist, S):
+    """Algorithmic HBM bytes of one layer call: active experts'
+    weights once, tokens in and out once, ids + weights."""
+    H, I = geom.K, geom.N // 2
+    return hist.active_experts * 3 * H * I * 2 + S * H * 4 + 8 * S * geom.top_k
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([f.strip() for f in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ CPU oracle
+def cpu_weights(geom, seed=42):
+    """fp32 host copy of random-init weights for the CPU (oracle) arm."""
+    rng = np.random.default_rng(seed)
+    E, H, I = geom.E, geom.K, geom.N // 2
+    w1 = (rng.standard_normal((E, 2 * I, H), dtype=np.float32) * np.float32(H ** -0.5))
+    w2 = (rng.standard_normal((E, H, I), dtype=np.float32) * np.float32(I ** -0.5))
+    return w1, w2
+
+
+def cpu_inputs(geom, pt):
+    from paper_2604_26039_b200.dispatch import derive_seed
+    from paper_2604_26039_b200.routing import topk_from_histogram
+
+    S, k = pt["S"], geom.top_k
+    ids = topk_from_histogram(pt["hist"].counts, S, k, derive_seed(pt["seed"], 6) % (2 ** 63))
+    rng = np.random.default_rng(derive_seed(pt["seed"], 8))
+    lg = rng.standard_normal((S, k)).astype(np.float32)
+    w = np.exp(lg - lg.max(1, keepdims=True))
+    w /= w.sum(1, keepdims=True)
+    x = rng.standard_normal((S, geom.K)).astype(np.float32)
+    return x, ids, w.astype(np.float32)
+
+
+def run_cpu_sweep(geom, pts, w1, w2, budget_s=None):
+    """One pass of the fp32 oracle over the sweep points (bounded by budget_s)."""
+    from oracle.moe_ref import fused_moe_ref
+
+    flops, t_total, n = 0, 0.0, 0
+    for pt in pts:
+        x, ids, w = cpu_inputs(geom, pt)
+        t0 = time.perf_counter()
+        fused_moe_ref(x, w1, w2, w, ids)
+        t_total += time.perf_counter() - t0
+        flops += layer_flops(geom, pt["S"])
+        n += 1
+        if budget_s is not None and t_total > budget_s:
+            break
+    return flops, t_total, n
+
+
+def reference_arm(args, geom):
+    """--impl reference: the reference path has no fused-MoE kernel, so its CPU
+    implementation of the layer is the oracle port (oracle/moe_ref.py, the
+    paper's three phases in fp32 numpy with all host threads)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    pts = sweep_points(geom)
+    w1, w2 = cpu_weights(geom)
+    for _ in range(args.warmup):
+        run_cpu_sweep(geom, pts[:3], w1, w2)
+    flops, secs = 0, 0.0
+    for _ in range(args.steps):
+        f, t, _ = run_cpu_sweep(geom, pts, w1, w2)
+        flops += f
+        secs += t
+    value = flops / secs / 1e12
+    cores = os.cpu_count()
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (random-init weights, reference evaluation histograms)",
+            "config": {"workload": f"{MODEL} MoE layer beta x batch sweep, fp32 CPU oracle port",
+                       "points": len(pts)},
+            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                             "sample": f"full {len(pts)}-point sweep per step, numpy fp32 (oracle/moe_ref.py)"},
+            "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def load_table(geom, pool, hw):
+    from paper_2604_26039_b200.cost_model import parse_coeff_store, read_coeff_store
+    from paper_2604_26039_b200.dispatch import DispatchTable
+
+    path = ROOT / "paper_2604_26039_b200" / "data" / f"coeffs_{MODEL}_b200.json"
+    if not path.exists():
+        raise SystemExit(f"{path} missing: run scripts/profile_b200.py on a B200 first")
+    _, sm, coeffs = parse_coeff_store(read_coeff_store(path))
+    return DispatchTable(model=MODEL, pool=pool, coefficients=coeffs, sm_count=sm), path
+
+
+def ours(args, geom):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_26039_b200 import _lib, moe
+    from paper_2604_26039_b200.config_space import HardwareModel, enumerate_b200_configs
+    from paper_2604_26039_b200.dispatch import evaluate_regret, speedup_ra_vs_static
+    from paper_2604_26039_b200.sweep import MeasuredTimer, make_inputs, make_weights
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    _lib.require_device()
+    dev = torch.device("cuda", local)
+    hw = HardwareModel.b200()
+    pool = enumerate_b200_configs(geom, hw)
+    table, coeff_path = load_table(geom, pool, hw)
+    dtab = table.device_table(device=dev)
+    pts = sweep_points(geom)
+    copies = [make_weights(geom, seed=42 + c, device=dev) for c in range(N_COPIES)]
+    inputs = [make_inputs(geom, pt["hist"], pt["seed"], dev) for pt in pts]
+    H, I = geom.K, geom.N // 2
+    wss = [moe.Workspace(pt["S"], H, I, geom.E, geom.top_k, device=dev) for pt in pts]
+    outs = [torch.empty(pt["S"], H, dtype=torch.bfloat16, device=dev) for pt in pts]
+    step_flops = sum(layer_flops(geom, pt["S"]) for pt in pts)
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        for p, (pt, (x, ids, w)) in enumerate(zip(pts, inputs)):
+            w1, w2 = copies[(i * len(pts) + p) % N_COPIES]
+            moe.fused_moe(x, w1, w2, w, ids, dtab, -1, out=outs[p], workspace=wss[p])
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        step(i)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record(stream)
+        for i in range(args.steps):
+            step(args.warmup + i)
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = step_flops * args.steps * world / (ms / 1e3) / 1e12
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---------------- diagnostics (untimed): per-point latency, megakernel roofline
+    per_point = []
+    k3_bytes, k3_time = 0.0, 0.0
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    for p, (pt, (x, ids, w)) in enumerate(zip(pts, inputs)):
+        lat, k3 = [], []
+        for r in range(5):
+            w1, w2 = copies[(p + r) % N_COPIES]
+            a0, a1 = ev(), ev()
+            a0.record()
+            moe.fused_moe(x, w1, w2, w, ids, dtab, -1, out=outs[p], workspace=wss[p])
+            a1.record()
+            w1, w2 = copies[(p + r + 3) % N_COPIES]
+            moe.fused_moe(x, w1, w2, w, ids, dtab, -1, out=outs[p], workspace=wss[p], phases=1)
+            b0, b1 = ev(), ev()
+            b0.record()
+            moe.fused_moe(x, w1, w2, w, ids, dtab, -1, out=outs[p], workspace=wss[p], phases=2)
+            b1.record()
+            torch.cuda.synchronize()
+            lat.append(a0.elapsed_time(a1) * 1e3)
+            k3.append(b0.elapsed_time(b1) * 1e3)
+        cfg = int(wss[p].sel[0].item())
+        us, k3us = float(np.median(lat)), float(np.median(k3))
+        nbytes = layer_bytes(geom, pt["hist"], pt["S"])
+        k3_bytes += nbytes
+        k3_time += k3us
+        c = pool.by_id(cfg)
+        per_point.append({"S": pt["S"], "beta": pt["beta"], "active": pt["hist"].active_experts, "us": round(us, 2),
+                          "megakernel_us": round(k3us, 2), "tflops": round(layer_flops(geom, pt["S"]) / us / 1e6, 2),
+                          "gbs": round(nbytes / k3us / 1e3, 1),
+                          "cfg": {"id": cfg, "bm": c.bm, "ttn": c.ttn, "stg": c.stg, "group_m": int(c.group_m),
+                                  "mode": c.mode}})
+    geo_us = math.exp(np.mean([math.log(r["us"]) for r in per_point]))
+
+    # ---------------- routing-aware vs static and regret against an exhaustive on-GPU sweep
+    ra = None
+    if not args.no_sweep:
+        timer = MeasuredTimer(geom, dtab, w1=copies[0][0], w2=copies[0][1], iters=3, device=dev)
+        points = [(pt["S"], pt["beta"]) for pt in pts]
+        spd = speedup_ra_vs_static(table, pool, geom, timer, points=points, seeds_per_point=1)
+        reg = evaluate_regret(table, pool, geom, timer, test_points=points, seeds_per_point=1)
+        ra = {"ra_vs_static_geomean": spd.geomean, "per_beta": spd.aggregate()["per_beta_geomean"],
+              "regret_mean_pct": reg.mean * 100, "regret_max_pct": reg.max * 100, "points": len(points)}
+
+    # ---------------- e2e through the public API with host buffers
+    pinned = []
+    for (x, ids, w), pt in zip(inputs, pts):
+        pinned.append((x.cpu().pin_memory(), ids.cpu().pin_memory(), w.cpu().pin_memory(),
+                       torch.empty(pt["S"], H, dtype=torch.bfloat16).pin_memory()))
+    h2d = sum(a.numel() * a.element_size() + b.numel() * b.element_size() + c.numel() * c.element_size()
+              for a, b, c, _ in pinned)
+    d2h = sum(o.numel() * o.element_size() for *_, o in pinned)
+    dev_bufs = [(torch.empty_like(x), torch.empty_like(i), torch.empty_like(w)) for x, i, w in inputs]
+
+    def e2e_step(i):
+        for p, ((hx, hi, hw_, ho), (dx, di, dw)) in enumerate(zip(pinned, dev_bufs)):
+            dx.copy_(hx, non_blocking=True)
+            di.copy_(hi, non_blocking=True)
+            dw.copy_(hw_, non_blocking=True)
+            w1, w2 = copies[(i * len(pts) + p) % N_COPIES]
+            moe.fused_moe(dx, w1, w2, dw, di, dtab, -1, out=outs[p], workspace=wss[p])
+            ho.copy_(outs[p], non_blocking=True)
+
+    e2e_step(0)
+    torch.cuda.synchronize()
+    f0, f1 = ev(), ev()
+    f0.record()
+    for i in range(max(1, args.steps // 2)):
+        e2e_step(i + 1)
+    f1.record()
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / max(1, args.steps // 2)
+    e2e_val = step_flops / (e2e_ms / 1e3) / 1e12
+
+    # ---------------- CPU baseline (oracle port, bounded sample)
+    cpu = None
+    if not args.no_cpu:
+        w1c, w2c = cpu_weights(geom)
+        run_cpu_sweep(geom, pts[:2], w1c, w2c)
+        f, t, n = run_cpu_sweep(geom, pts, w1c, w2c, budget_s=20.0)
+        cpu = {"value": f / t / 1e12, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"first {n} of {len(pts)} sweep points (fp32 numpy oracle, oracle/moe_ref.py)"}
+
+    peaks = {}
+    pk_path = ROOT / "MEASURED_PEAKS.json"
+    if pk_path.exists():
+        peaks = json.loads(pk_path.read_text())
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = k3_bytes / k3_time / 1e3  # GB/s over the sweep (bytes-weighted)
+    traffic = None
+    tr_path = ROOT / "profiles" / "k3_traffic.json"
+    if tr_path.exists():
+        traffic = json.loads(tr_path.read_text()).get("traffic_bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init weights, reference evaluation histograms)",
+        "config": {"workload": f"{MODEL} MoE layer (E=64, top-8, d=2048, d_ff=1024) BF16, S=1..512 x "
+                               f"beta in {{0.2,0.5,1.0}} ({len(pts)} layer calls/step), routing-aware dispatch",
+                   "l2": f"inputs larger than L2: {N_COPIES} rotating weight copies of 805 MB",
+                   "parallelism": "replicas" if world > 1 else "single GPU", "coeffs": coeff_path.name},
+        "gpu_launches": 2 * len(pts) * args.steps,
+        "us_per_layer_geomean": geo_us,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "fused_moe_bf16_kernel",
+                     "note": "algorithmic bytes / megakernel time summed over the sweep; peak = measured hbm_gbs"},
+        "clocks": clocks.summary(),
+        "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "cpu_baseline": cpu,
+        "dispatch": ra,
+        "per_point": per_point,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the exhaustive RA/static/regret sweep")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    from paper_2604_26039_b200.catalog import BASELINE_MODELS
+
+    geom = BASELINE_MODELS[MODEL]
+    if args.impl == "reference":
+        reference_arm(args, geom)
+    else:
+        ours(args, geom)
+
+
+if __name__ == "__main__":
+    main()
