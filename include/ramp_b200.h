@@ -59,6 +59,13 @@ typedef struct ramp_table {
   const double* b;
   const double* c;
   const double* d;
+  /* Optional generalisations (the reference behaviour when null / <= 0):
+   * ntile[i]   work tiles per M-tile of config i, replacing ceil(N/ttn) in
+   *            g = M-tiles * ntile * split_k -- the B200 megakernel's split
+   *            mode runs I-stripe jobs AND H-chunk jobs per M-tile;
+   * omega_max  split-K gate threshold (reference: 0.2, ramp/dispatch.py:31). */
+  const int32_t* ntile;
+  double omega_max;
 } ramp_table_t;
 
 /* Library version (major*10000 + minor*100 + patch) and sm_100a build flag. */

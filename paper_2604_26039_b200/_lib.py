@@ -68,6 +68,8 @@ class RampTable(ctypes.Structure):
         ("b", ctypes.c_void_p),
         ("c", ctypes.c_void_p),
         ("d", ctypes.c_void_p),
+        ("ntile", ctypes.c_void_p),
+        ("omega_max", ctypes.c_double),
     ]
 
 

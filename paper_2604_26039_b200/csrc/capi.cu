@@ -26,7 +26,7 @@ int cuda_fail(cudaError_t err, const char* where) {
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct WorkspaceLayout {
-  size_t ctrl, hist, sorted, tiles, done, acc, xs, act, total;
+  size_t ctrl, hist, sorted, tiles, done, acc, xs, act, acc_a, split_cnt, total;
   int64_t capacity, rows;
 };
 
@@ -53,6 +53,8 @@ WorkspaceLayout layout_for(int32_t S, int32_t H, int32_t I, int32_t E, int32_t t
   w.acc = take(sizeof(float) * (size_t)S * H);
   w.xs = take(2 * (size_t)w.rows * H);
   w.act = take(2 * (size_t)w.rows * I);
+  w.acc_a = take(4 * (size_t)w.rows * 2 * I);
+  w.split_cnt = take(sizeof(int32_t) * w.capacity);
   w.total = off;
   return w;
 }
@@ -205,6 +207,8 @@ int ramp_fused_moe_bf16_ex(const void* x, const void* w1, const void* w2, const 
   ml.done = ra.done;
   ml.job_counter = ra.ctrl + 7;
   ml.rows = L.rows;
+  ml.acc_a = reinterpret_cast<float*>(ws + L.acc_a);
+  ml.split_cnt = reinterpret_cast<int*>(ws + L.split_cnt);
   ml.table = *table;
   ml.S = S;
   ml.H = H;

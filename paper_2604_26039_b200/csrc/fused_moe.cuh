@@ -82,6 +82,8 @@ struct MoeParams {
   int* done;                   // [n_mtiles] split-mode phase-A completion counters (zeroed by route)
   int* job_counter;            // global job claim counter (zeroed by route)
   int* gbar;                   // [2] grid barriers: rows gathered, all jobs reduced (zeroed by route)
+  float* acc_a;                // [rows, 2I] split-K phase-1 partial sums (read and cleared by the finisher)
+  int* split_cnt;              // [n_mtiles * stripes] split-K arrival counters (reset by the finisher)
   const __nv_bfloat16* x;      // [S, H] tokens
   __nv_bfloat16* x_sorted;     // [rows, H] expert-sorted token rows (gathered in phase 0)
   __nv_bfloat16* out;          // [S, H] bf16 result
@@ -119,6 +121,7 @@ struct CtrlSmem {
   uint64_t job_empty[4];
   int32_t job_slot[4];
   uint32_t tmem_base;
+  int32_t fin;  // split-K: this CTA completed the (m, s) reduction
   int32_t epi_tok[128];
   float epi_w[128];
 };
@@ -128,27 +131,34 @@ static_assert(sizeof(CtrlSmem) <= kCtrlBytes, "control block overflow");
 struct Job {
   int kind;  // 0 = phase 1(+2) of (m, s) [fused: +phase 3], 1 = split phase 3 of (m, hc)
   int m, s, hc;
+  int kq;    // split-K slice of the job's reduction dimension (split mode)
 };
 
 struct Geometry {
-  int mode, bm, bmN, nA, n_i, stripes, n_mtiles, n_hc, kbH, kbI, nJobA, total, group_m;
+  int mode, bm, bmN, nA, n_i, stripes, n_mtiles, n_hc, kbH, kbI, nJobA, total, group_m, sk;
   bool dbl;  // TMEM double buffering across jobs (split mode, fits in 256 columns)
   __device__ __forceinline__ Job job(int j) const {
     Job r;
     if (j < nJobA) {
+      const int u = j / sk;  // the sk K-slices of one (m, s) are consecutive jobs
       r.kind = 0;
-      r.m = group_m ? (j % n_mtiles) : (j / stripes);
-      r.s = group_m ? (j / n_mtiles) : (j % stripes);
+      r.kq = j % sk;
+      r.m = group_m ? (u % n_mtiles) : (u / stripes);
+      r.s = group_m ? (u / n_mtiles) : (u % stripes);
       r.hc = 0;
     } else {
-      const int jj = j - nJobA;
+      const int jj = j - nJobA, u = jj / sk;
       r.kind = 1;
-      r.m = group_m ? (jj % n_mtiles) : (jj / n_hc);
-      r.hc = group_m ? (jj / n_mtiles) : (jj % n_hc);
+      r.kq = jj % sk;
+      r.m = group_m ? (u % n_mtiles) : (u / n_hc);
+      r.hc = group_m ? (u / n_mtiles) : (u % n_hc);
       r.s = 0;
     }
     return r;
   }
+  // k-block range [lo, hi) of a job's reduction (H for phase 1, I for phase 3)
+  __device__ __forceinline__ int kb_lo(const Job& jb) const { return jb.kq * (jb.kind ? kbI : kbH) / sk; }
+  __device__ __forceinline__ int kb_hi(const Job& jb) const { return (jb.kq + 1) * (jb.kind ? kbI : kbH) / sk; }
 };
 
 __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + __expf(-g)) * u; }
@@ -238,8 +248,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   G.kbH = p.H / 64;
   G.kbI = p.I / 64;
   G.group_m = p.table.group_m[cfg];
-  G.nJobA = G.n_mtiles * G.stripes;
-  G.total = G.nJobA + (G.mode == kModeSplit ? G.n_mtiles * G.n_hc : 0);
+  G.sk = (G.mode == kModeSplit && p.table.split_k[cfg] > 1) ? p.table.split_k[cfg] : 1;
+  G.nJobA = G.n_mtiles * G.stripes * G.sk;
+  G.total = G.nJobA + (G.mode == kModeSplit ? G.n_mtiles * G.n_hc * G.sk : 0);
   G.dbl = G.mode == kModeSplit && G.nA * G.bmN <= 256;
   const int bmN = G.bmN, nA = G.nA;
   const int sbytes = stage_bytes(G.bm, ttn);
@@ -326,8 +337,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       if (jb.kind == 0) {
         const uint32_t tx1 = nA * kSubTileBytes + bmN * 128;
         const int wrow = jb.s * G.n_i;
+        const int kb0 = G.kb_lo(jb), kb1 = G.kb_hi(jb);
         int first_pending = 0, npend = 0;
-        for (int kb = 0; kb < G.kbH; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           acquire();
           if (elect_one()) {
             const uint32_t full = smem_u32(&cs.full[stage]);
@@ -342,7 +354,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             // every CTA has published its slice of x_sorted
             if (npend == 0) first_pending = kb;
             ++npend;
-            if (npend == u_stg || kb == G.kbH - 1) {
+            if (npend == u_stg || kb == kb1 - 1) {
               pc.lap();
               while (ld_acquire_gpu(p.gbar) < (int)gridDim.x) __nanosleep(32);
               fence_proxy_async_global();
@@ -380,9 +392,10 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         // every phase-1 job of this M-tile (release/acquire on done[m]).
         const uint32_t tx = kSubTileBytes + bmN * 128;
         const int wrow = e * p.H + jb.hc * 128;
+        const int kb0 = G.kb_lo(jb), kb1 = G.kb_hi(jb);
         int first_pending = 0, npend = 0;
         bool ready = false;
-        for (int kb = 0; kb < G.kbI; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           acquire();
           if (elect_one()) {
             const uint32_t full = smem_u32(&cs.full[stage]);
@@ -395,7 +408,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           if (!ready) {
             if (npend == 0) first_pending = kb;
             ++npend;
-            if (npend == u_stg || kb == G.kbI - 1) {
+            if (npend == u_stg || kb == kb1 - 1) {
               pc.lap();
               while (ld_acquire_gpu(p.done + jb.m) < G.stripes) __nanosleep(64);
               fence_proxy_async_global();
@@ -472,8 +485,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       }
       c_acc += pc.lap();
       tc_fence_after();
+      const int kb0 = G.kb_lo(jb), kb1 = G.kb_hi(jb);
       if (jb.kind == 0) {
-        for (int kb = 0; kb < G.kbH; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           const uint32_t sb = wait_full();
           const uint64_t da = sw128_kmajor_desc(sb);
           const uint64_t db = sw128_kmajor_desc(sb + nA * kSubTileBytes);
@@ -482,7 +496,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
 #pragma unroll
               for (int k = 0; k < 4; ++k)
                 mma_bf16(acc + t * bmN, da + ((t * kSubTileBytes + k * 32) >> 4), db + ((k * 32) >> 4), idesc,
-                         (kb | k) != 0);
+                         ((kb - kb0) | k) != 0);
             }
           }
           __syncwarp();
@@ -520,14 +534,14 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           }
         }
       } else {
-        for (int kb = 0; kb < G.kbI; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           const uint32_t sb = wait_full();
           const uint64_t da = sw128_kmajor_desc(sb);
           const uint64_t db = sw128_kmajor_desc(sb + kSubTileBytes);
           if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              mma_bf16(acc, da + ((k * 32) >> 4), db + ((k * 32) >> 4), idesc, (kb | k) != 0);
+              mma_bf16(acc, da + ((k * 32) >> 4), db + ((k * 32) >> 4), idesc, ((kb - kb0) | k) != 0);
           }
           __syncwarp();
           release();
@@ -609,34 +623,65 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             }
           }
         };
-        if (nA == 1) {
-          // ttn = 128: lanes 0-63 hold gate rows, lanes 64-127 the matching up rows
-          for (int j0 = 0; j0 < bmN; j0 += 16) {
-            float g[16], u[16];
-            tmem_ld16(acc + j0, g);
-            tmem_ld_wait();
-            if (et >= 64) {
-#pragma unroll
-              for (int q = 0; q < 16; ++q) tbuf[q * 64 + (et - 64)] = g[q];
-            }
-            named_bar_sync(1, 128);
-            if (et < 64) {
-#pragma unroll
-              for (int q = 0; q < 16; ++q) u[q] = tbuf[q * 64 + et];
-              store_act(et, j0, g, u);
-            }
-            named_bar_sync(1, 128);
-          }
-        } else {
-          // Thread et owns features f = th*128 + et of the stripe.
-          for (int th = 0; th < nA / 2; ++th) {
-            const int f = th * 128 + et;
+        if (G.sk == 1) {
+          if (nA == 1) {
+            // ttn = 128: lanes 0-63 hold gate rows, lanes 64-127 the matching up rows
             for (int j0 = 0; j0 < bmN; j0 += 16) {
               float g[16], u[16];
-              tmem_ld16(acc + th * bmN + j0, g);
-              tmem_ld16(acc + (nA / 2 + th) * bmN + j0, u);
+              tmem_ld16(acc + j0, g);
               tmem_ld_wait();
-              store_act(f, j0, g, u);
+              if (et >= 64) {
+  #pragma unroll
+                for (int q = 0; q < 16; ++q) tbuf[q * 64 + (et - 64)] = g[q];
+              }
+              named_bar_sync(1, 128);
+              if (et < 64) {
+  #pragma unroll
+                for (int q = 0; q < 16; ++q) u[q] = tbuf[q * 64 + et];
+                store_act(et, j0, g, u);
+              }
+              named_bar_sync(1, 128);
+            }
+          } else {
+            // Thread et owns features f = th*128 + et of the stripe.
+            for (int th = 0; th < nA / 2; ++th) {
+              const int f = th * 128 + et;
+              for (int j0 = 0; j0 < bmN; j0 += 16) {
+                float g[16], u[16];
+                tmem_ld16(acc + th * bmN + j0, g);
+                tmem_ld16(acc + (nA / 2 + th) * bmN + j0, u);
+                tmem_ld_wait();
+                store_act(f, j0, g, u);
+              }
+            }
+          }
+        } else {
+          // split-K slice: reduce this job's partial gate/up sums into acc_a
+          // (fp32, L2-resident) with 16-byte vector reductions; the last
+          // slice to arrive applies SwiGLU below.
+          const int two_i = 2 * p.I;
+          auto col_of = [&](int t, int lane_row) {
+            if (nA == 1) return lane_row < 64 ? jb.s * 64 + lane_row : p.I + jb.s * 64 + (lane_row - 64);
+            return (t < nA / 2 ? 0 : p.I) + jb.s * G.n_i + (t % (nA / 2)) * 128 + lane_row;
+          };
+          const int w4 = et >> 5, l4 = et & 31;
+          for (int t = 0; t < nA; ++t) {
+            const int c4 = col_of(t, 4 * l4);
+            for (int j0 = 0; j0 < G.bm; j0 += 16) {
+              float v[16];
+              tmem_ld16(acc + t * bmN + j0, v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int q = 0; q < 16; ++q) tbuf[q * 128 + et] = v[q];
+              named_bar_sync(1, 128);
+#pragma unroll
+              for (int rr = 0; rr < 4; ++rr) {
+                const int q = w4 * 4 + rr, jj = j0 + q;
+                if (jj < G.bm)
+                  red_add_v4_f32(p.acc_a + static_cast<size_t>(row0 + jj) * two_i + c4,
+                                 *reinterpret_cast<const float4*>(tbuf + q * 128 + 4 * l4));
+              }
+              named_bar_sync(1, 128);
             }
           }
         }
@@ -666,11 +711,48 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           }
         } else {
           mbar_arrive(smem_u32(&cs.acc_empty[r]));
-          // publish phase-1 completion of this (m, s) job for the phase-3 jobs
-          named_bar_sync(1, 128);
-          if (et == 0) {
+          bool publish = true;
+          if (G.sk > 1) {
+            // count this slice in; the last of the sk slices finishes the stripe
             __threadfence();
-            atomicAdd(p.done + jb.m, 1);
+            named_bar_sync(1, 128);
+            if (et == 0) {
+              int* cnt = p.split_cnt + jb.m * G.stripes + jb.s;
+              const int old = atomicAdd(cnt, 1);
+              cs.fin = old == G.sk - 1;
+              if (cs.fin) *cnt = 0;  // every slice has arrived: reset for the next call
+              __threadfence();
+            }
+            named_bar_sync(1, 128);
+            publish = cs.fin != 0;
+            if (publish) {
+              const int two_i = 2 * p.I;
+              for (int f = et; f < G.n_i; f += 128) {
+                for (int j0 = 0; j0 < G.bm; j0 += 16) {
+                  float g[16], u[16];
+#pragma unroll
+                  for (int q = 0; q < 16; ++q) {
+                    g[q] = u[q] = 0.f;
+                    if (j0 + q < G.bm) {
+                      float* rowp = p.acc_a + static_cast<size_t>(row0 + j0 + q) * two_i + jb.s * G.n_i + f;
+                      g[q] = __ldcg(rowp);
+                      u[q] = __ldcg(rowp + p.I);
+                      rowp[0] = 0.f;  // leave acc_a cleared for the next call
+                      rowp[p.I] = 0.f;
+                    }
+                  }
+                  store_act(f, j0, g, u);
+                }
+              }
+            }
+          }
+          if (publish) {
+            // publish phase-1 completion of this (m, s) stripe for the phase-3 jobs
+            named_bar_sync(1, 128);
+            if (et == 0) {
+              __threadfence();
+              atomicAdd(p.done + jb.m, 1);
+            }
           }
           c_swiglu += pc.lap();
         }

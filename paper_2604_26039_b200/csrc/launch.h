@@ -54,6 +54,8 @@ struct MoeLaunch {
   void* act_g;      // [rows, I] bf16
   int* done;        // [rows] split-mode counters
   int* job_counter; // dynamic scheduler claim counter (zeroed by the route kernel)
+  float* acc_a;     // [rows, 2I] split-K partial sums
+  int* split_cnt;   // [rows] split-K arrival counters
   int64_t rows;     // capacity of x_sorted / act_g
   ramp_table_t table;
   int32_t S, H, I, E, top_k;

@@ -151,6 +151,8 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
   p.done = l.done;
   p.job_counter = l.job_counter;
   p.gbar = l.job_counter + 1;
+  p.acc_a = l.acc_a;
+  p.split_cnt = l.split_cnt;
   p.x = static_cast<const __nv_bfloat16*>(l.x);
   p.x_sorted = static_cast<__nv_bfloat16*>(l.x_sorted);
   p.out = static_cast<__nv_bfloat16*>(l.out);

@@ -149,15 +149,16 @@ __device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_tabl
   __syncthreads();
 
   const double sm = static_cast<double>(t.sm_count);
+  const double omega_max = t.omega_max > 0.0 ? t.omega_max : 0.2;
   ArgMin best{CUDART_INF, 0x7fffffff};
   int kept = 0;
   for (int i = threadIdx.x; i < t.n_cfg; i += blockDim.x) {
     const int ttn = t.ttn[i], sk = t.split_k[i];
-    const long long stripes = (static_cast<long long>(t.N) + ttn - 1) / ttn;
+    const long long stripes = t.ntile ? t.ntile[i] : (static_cast<long long>(t.N) + ttn - 1) / ttn;
     const long long g = mt_smem[t.ubm_index[i]] * stripes * sk;
     const double gd = static_cast<double>(g);
     bool keep = true;
-    if (sk > 1) keep = t.kappa_ok && (__ddiv_rn(__ddiv_rn(gd, static_cast<double>(sk)), sm) < 0.2);
+    if (sk > 1) keep = t.kappa_ok && (__ddiv_rn(__ddiv_rn(gd, static_cast<double>(sk)), sm) < omega_max);
     double p = __dadd_rn(t.a[i], __dmul_rn(t.b[i], ceil(__ddiv_rn(gd, sm))));
     p = __dadd_rn(p, __dmul_rn(t.c[i], gd));
     p = __dadd_rn(p, __dmul_rn(t.d[i], log(__dadd_rn(gd, 1.0))));

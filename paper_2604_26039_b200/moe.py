@@ -47,6 +47,8 @@ class DeviceTable:
     kappa_ok: bool
     sm_count: int
     device: torch.device | str = "cuda"
+    ntile: np.ndarray | None = None   # work tiles per M-tile (default ceil(N/ttn))
+    omega_max: float = 0.0            # split-K gate threshold (<= 0: the reference's 0.2)
     _tensors: dict = field(default_factory=dict, repr=False)
     struct: _lib.RampTable | None = field(default=None, repr=False)
 
@@ -71,6 +73,10 @@ class DeviceTable:
         t["ubm_index"] = torch.as_tensor(ubm_index.astype(np.int32), **i32)
         for name in ("a", "b", "c", "d"):
             t[name] = torch.as_tensor(np.asarray(getattr(self, name), dtype=np.float64), **f64)
+        if self.ntile is not None:
+            if len(self.ntile) != n:
+                raise ValueError("ntile must have one entry per config")
+            t["ntile"] = torch.as_tensor(np.asarray(self.ntile, dtype=np.int32), **i32)
         s = _lib.RampTable()
         s.n_cfg = n
         s.n_ubm = len(ubm)
@@ -79,6 +85,8 @@ class DeviceTable:
         s.sm_count = int(self.sm_count)
         for name in ("bm", "ttn", "stg", "split_k", "group_m", "mode", "ubm", "ubm_index", "a", "b", "c", "d"):
             setattr(s, name, t[name].data_ptr())
+        s.ntile = t["ntile"].data_ptr() if "ntile" in t else None
+        s.omega_max = float(self.omega_max)
         self.struct = s
 
     def __len__(self) -> int:

@@ -99,7 +99,11 @@ class MeasuredTimer:
                     graph.replay()
                     e1.record(stream)
             stream.synchronize()
-            res[n] = float(np.median([e0.elapsed_time(e1) * 1e3 for e0, e1 in ev]))
+            # CUDA event timestamps are quantised (~0.5-1 us on this part):
+            # average the middle replays instead of taking one median sample
+            ts = np.sort([e0.elapsed_time(e1) * 1e3 for e0, e1 in ev])
+            trim = len(ts) // 4
+            res[n] = float(ts[trim:len(ts) - trim].mean())
         return res
 
     def pool_times(self, pool: ConfigPool, hist: ExpertHistogram, point_seed: int, shared_noise: bool = False,
