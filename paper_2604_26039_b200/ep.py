@@ -1,0 +1,114 @@
+"""Expert parallelism for the expert-sharded configs (north_star (4)).
+
+Rank r of a P-rank group owns experts [r*E/P, (r+1)*E/P).  One MoE layer:
+
+  1. dispatch: every (token, expert) assignment is routed to the owner rank
+     of its expert.  Assignments of one token bound for the same rank are
+     merged into one row (the token is sent once per destination rank, with up
+     to k (local expert, weight) pairs), so the wire carries unique
+     (token, rank) pairs -- the "pre-reduce per (token, rank)" of SURVEY §8e.
+  2. the owner runs the fused-MoE megakernel on its local experts: the
+     received rows are its tokens, their local expert ids / weights its top-k
+     (unused slots carry weight 0 and expert 0);
+  3. combine: the per-(token, rank) partial outputs travel back and are
+     summed into the origin tokens.
+
+The exchanges are NCCL all-to-alls (torch.distributed.all_to_all_single over
+NVLink 5 / NVSwitch); the split sizes need one small host read of the
+per-destination counts (exchanged with an all-to-all of int64 counts first).
+The local computation is pluggable (`local_fn`), which lets the gloo CPU tests
+check the routing, packing and combine arithmetic against a dense oracle.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+@dataclass
+class EPPlan:
+    """Send-side bookkeeping of one dispatch (kept for the combine)."""
+
+    send_counts: list[int]
+    recv_counts: list[int]
+    order: torch.Tensor        # unique (token, rank) pairs sorted by destination rank
+    pair_token: torch.Tensor   # origin token of every sent row (sorted order)
+
+
+def expert_owner(ids: torch.Tensor, E: int, world: int) -> torch.Tensor:
+    per = E // world
+    return torch.div(ids, per, rounding_mode="floor")
+
+
+def dispatch(x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor, E: int, group=None):
+    """Route token rows to expert owners.  Returns (plan, recv_x [R, H],
+    recv_ids [R, k] local expert ids, recv_w [R, k])."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    per = E // world
+    S, k = topk_ids.shape
+    dev = x.device
+    owner = expert_owner(topk_ids.long(), E, world)                     # [S, k]
+    # unique (token, rank) pairs, ordered by destination rank then token
+    key = owner * S + torch.arange(S, device=dev)[:, None]               # [S, k]
+    pairs = torch.unique(key.reshape(-1))                                # sorted => grouped by rank
+    pair_rank = torch.div(pairs, S, rounding_mode="floor")
+    pair_token = pairs % S
+    send_counts = torch.bincount(pair_rank, minlength=world)
+    recv_counts = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv_counts, send_counts, group=group)
+    sc, rc = send_counts.tolist(), recv_counts.tolist()                  # the one host read
+    # per sent row: the token's assignments that live on that rank (others -> weight 0)
+    row_owner = owner[pair_token]                                        # [P, k]
+    hit = row_owner == pair_rank[:, None]
+    row_ids = torch.where(hit, topk_ids[pair_token].long() - pair_rank[:, None] * per, 0)
+    row_w = torch.where(hit, topk_w[pair_token], torch.zeros((), dtype=topk_w.dtype, device=dev))
+    send_x = x[pair_token].contiguous()
+    R = sum(rc)
+    recv_x = torch.empty(R, x.shape[1], dtype=x.dtype, device=dev)
+    recv_ids = torch.empty(R, k, dtype=torch.int64, device=dev)
+    recv_w = torch.empty(R, k, dtype=topk_w.dtype, device=dev)
+    dist.all_to_all_single(recv_x, send_x, rc, sc, group=group)
+    dist.all_to_all_single(recv_ids, row_ids.contiguous(), rc, sc, group=group)
+    dist.all_to_all_single(recv_w, row_w.contiguous(), rc, sc, group=group)
+    plan = EPPlan(send_counts=sc, recv_counts=rc, order=pairs, pair_token=pair_token)
+    return plan, recv_x, recv_ids.to(torch.int32), recv_w
+
+
+def combine(plan: EPPlan, partial: torch.Tensor, S: int, group=None) -> torch.Tensor:
+    """Return per-(token, rank) partial outputs to their origin and sum them."""
+    back = torch.empty(sum(plan.send_counts), partial.shape[1], dtype=partial.dtype, device=partial.device)
+    dist.all_to_all_single(back, partial.contiguous(), plan.send_counts, plan.recv_counts, group=group)
+    out = torch.zeros(S, partial.shape[1], dtype=torch.float32, device=partial.device)
+    out.index_add_(0, plan.pair_token, back.float())
+    return out.to(partial.dtype)
+
+
+def ep_moe_layer(x, topk_ids, topk_w, E: int, local_fn, group=None):
+    """dispatch -> local_fn(recv_x, recv_ids, recv_w) -> combine."""
+    plan, rx, rids, rw = dispatch(x, topk_ids, topk_w, E, group)
+    partial = local_fn(rx, rids, rw)
+    return combine(plan, partial, x.shape[0], group)
+
+
+def make_local_megakernel(w1_local, w2_local, table, workspace_cache: dict | None = None):
+    """local_fn running the B200 megakernel on this rank's experts."""
+    from .moe import Workspace, fused_moe
+
+    cache = workspace_cache if workspace_cache is not None else {}
+
+    def run(rx, rids, rw):
+        if rx.shape[0] == 0:
+            return torch.zeros(0, rx.shape[1], dtype=rx.dtype, device=rx.device)
+        E_l, two_i, H = w1_local.shape
+        key = (rx.shape[0], rids.shape[1])
+        ws = cache.get(key)
+        if ws is None:
+            ws = cache[key] = Workspace(rx.shape[0], H, two_i // 2, E_l, rids.shape[1], device=rx.device)
+        return fused_moe(rx.contiguous(), w1_local, w2_local, rw.float().contiguous(), rids.contiguous(), table,
+                         workspace=ws)
+
+    return run
