@@ -44,7 +44,7 @@ constexpr int kMoeThreads = 256;
 constexpr int kCtrlBytes = 4096;                  // barriers + per-job metadata
 constexpr int kStageBytesScatter = 16 * 128 * 4;  // 16 tokens x 128 rows fp32 transpose buffer
 constexpr int kSubTileBytes = 128 * 128;          // 128 rows x 64 bf16 (one SW128 box)
-constexpr int kMaxStages = 8;
+constexpr int kMaxStages = 12;
 constexpr int kSmemLimit = 232448;                // 227 KB opt-in per CTA on sm_100
 constexpr int kModeFused = 0;
 constexpr int kModeSplit = 1;
@@ -395,6 +395,13 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         const int kb0 = G.kb_lo(jb), kb1 = G.kb_hi(jb);
         int first_pending = 0, npend = 0;
         bool ready = false;
+        // Pull this job's whole W2 slice toward L2 now: while the act rows are
+        // still being produced by the phase-1 jobs, HBM keeps streaming weights,
+        // and once the dependency resolves the slice arrives from L2.
+        if (ld_acquire_gpu(p.done + jb.m) < G.stripes) {
+          for (int kb = kb0 + u_stg + lane; kb < kb1; kb += 32) tma_prefetch_2d(tm_w2, kb * 64, wrow);
+        }
+        __syncwarp();
         for (int kb = kb0; kb < kb1; ++kb) {
           acquire();
           if (elect_one()) {

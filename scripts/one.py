@@ -20,6 +20,7 @@ ap.add_argument("--ttn", type=int, default=512)
 ap.add_argument("--stg", type=int, default=2)
 ap.add_argument("--gm", type=int, default=0)
 ap.add_argument("--mode", type=int, default=0)
+ap.add_argument("--sk", type=int, default=1)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--E", type=int, default=64)
 ap.add_argument("--H", type=int, default=2048)
@@ -37,7 +38,7 @@ n = len(pool)
 table = M.DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
                       group_m=cols["group_m"].astype(np.int64), mode=cols.get("mode"), a=np.ones(n), b=np.zeros(n), c=np.zeros(n),
                       d=np.zeros(n), N=2 * I, kappa_ok=False, sm_count=148)
-cfg = [c.id for c in pool if (c.bm, c.ttn, c.stg, int(c.group_m), c.mode) == (a.bm, a.ttn, a.stg, a.gm, a.mode)][0]
+cfg = [c.id for c in pool if (c.bm, c.ttn, c.stg, int(c.group_m), c.mode, c.split_k) == (a.bm, a.ttn, a.stg, a.gm, a.mode, a.sk)][0]
 x = torch.randn(S, H, device="cuda", generator=gen).to(torch.bfloat16)
 ids, w = topk(S, k, E, a.skew, gen)
 ws = M.Workspace(S, H, I, E, k)

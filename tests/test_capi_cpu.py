@@ -43,7 +43,7 @@ def test_version_and_capacity(lib):
 def test_smem_formula_matches_python(lib):
     for bm in (4, 8, 16, 32, 64, 128):
         for ttn in (128, 256, 512):
-            for stg in range(1, 9):
+            for stg in range(1, 13):
                 for mode in (0, 1):
                     want = b200_smem_bytes(bm, ttn, stg, mode)
                     got = lib.ramp_config_smem_bytes(bm, ttn, stg, mode)
