@@ -142,10 +142,11 @@ int ramp_fused_moe_bf16_ex(const void* x, const void* w1, const void* w2, const 
 int64_t ramp_config_smem_bytes(int32_t bm, int32_t ttn, int32_t stg, int32_t mode);
 
 /* Diagnostics: when dev_buf is non-null, every later megakernel launch writes
- * 16 per-CTA cycle counters (producer wait/issue, MMA waits, epilogue phases,
- * see ProfSlot in csrc/fused_moe.cuh) to dev_buf[blockIdx * 16 + slot], and
- * the route kernel writes globaltimer stamps to dev_buf[148 * 16 + 0..15]
- * (buffer: >= 149 * 16 entries).
+ * 32 per-CTA slots (cycle counters of the producer / MMA / epilogue roles and
+ * globaltimer stamps of the kernel's phases, see ProfSlot in
+ * csrc/fused_moe.cuh) to dev_buf[blockIdx * 32 + slot], and the route kernel
+ * writes globaltimer stamps to dev_buf[148 * 32 + 0..15]
+ * (buffer: >= 149 * 32 entries).
  * Pass null to switch it off.  Not used on the timed path. */
 void ramp_set_profile_buffer(unsigned long long* dev_buf);
 

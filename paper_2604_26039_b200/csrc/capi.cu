@@ -180,7 +180,7 @@ int ramp_fused_moe_bf16_ex(const void* x, const void* w1, const void* w2, const 
   ra.done = reinterpret_cast<int*>(ws + L.done);
   ra.x = x;
   ra.x_sorted = nullptr;
-  ra.prof = ramp::g_prof_buffer ? ramp::g_prof_buffer + 148 * 16 : nullptr;
+  ra.prof = ramp::g_prof_buffer ? ramp::g_prof_buffer + 148 * 32 : nullptr;
   ra.S = S;
   ra.H = H;
   ra.top_k = top_k;

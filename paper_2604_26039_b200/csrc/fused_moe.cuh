@@ -95,7 +95,10 @@ struct MoeParams {
 // Diagnostic counters (cycles, per CTA) written when MoeParams::prof != null.
 enum ProfSlot {
   kPrWaitEmpty = 0, kPrIssue, kMmaWaitFull, kMmaWaitAcc, kMmaWaitAct, kEpiWaitAcc, kEpiSwiglu,
-  kEpiWaitChunk, kEpiScatter, kTotal, kItems, kEpiMeta, kPrWaitDep, kNumProf = 16
+  kEpiWaitChunk, kEpiScatter, kTotal, kItems, kEpiMeta, kPrWaitDep,
+  // globaltimer stamps (ns)
+  kTsEntry = 16, kTsStart, kTsGathered, kTsProducerDone, kTsEpilogueDone, kTsEndArrive, kTsEndPass, kTsFinal,
+  kNumProf = 32
 };
 
 struct ProfClock {
@@ -199,6 +202,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  unsigned long long* const ts = p.prof ? p.prof + blockIdx.x * kNumProf : nullptr;
+  if (ts && threadIdx.x == 0) ts[kTsEntry] = globaltimer();
 
   // Prologue (overlaps the route kernel's tail under PDL): descriptors,
   // barriers, TMEM.  Nothing here reads the route kernel's outputs.
@@ -230,6 +235,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   tc_fence_after();
   const uint32_t tmem = cs.tmem_base;
   pdl_wait();  // the route kernel's selection, alignment and gathered rows are now visible
+  if (ts && threadIdx.x == 0) ts[kTsStart] = globaltimer();
 
   // --- runtime tile config chosen by the dispatcher (no host round trip)
   const int cfg = p.ctrl[0];
@@ -262,35 +268,34 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   const CUtensorMap* tm_w2 = &maps.w2;
 
   // ---- phase 0: gather the token rows of every M-tile into expert-sorted
-  // order (warps 3-7 of every CTA), then arrive on grid barrier 0.  The
-  // producers stream weights meanwhile and hold back token tiles until all
-  // CTAs have arrived.
-  if (warp >= 3) {
+  // order (warps 2-7 of every CTA, 8 x 16-byte loads in flight per lane),
+  // then arrive on grid barrier 0.  The producers stream weights meanwhile
+  // and hold back token tiles until all CTAs have arrived.
+  if (warp >= 2) {
+    constexpr int kGatherWarps = 6, kUnroll = 8;
     const int row_vec = p.H / 8;  // 16-byte vectors per row
-    const int gw = blockIdx.x * 5 + (warp - 3), nw = gridDim.x * 5;
+    const int gw = blockIdx.x * kGatherWarps + (warp - 2), nw = gridDim.x * kGatherWarps;
     const int4* xv = reinterpret_cast<const int4*>(p.x);
     int4* dv = reinterpret_cast<int4*>(p.x_sorted);
     for (int r = gw; r < n_post_pad; r += nw) {
       const int asg = p.sorted_ids[r];
       int4* d = dv + static_cast<int64_t>(r) * row_vec;
-      if (asg < p.n_assign) {
-        const int4* src = xv + static_cast<int64_t>(asg / p.top_k) * row_vec;
-        for (int c0 = lane; c0 < row_vec; c0 += 32 * 4) {
-          int4 v[4];
+      const int4* src = xv + static_cast<int64_t>(asg < p.n_assign ? asg / p.top_k : 0) * row_vec;
+      for (int c0 = lane; c0 < row_vec; c0 += 32 * kUnroll) {
+        int4 v[kUnroll];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (c0 + 32 * u < row_vec) v[u] = __ldg(src + c0 + 32 * u);
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (c0 + 32 * u < row_vec) d[c0 + 32 * u] = v[u];
+        for (int u = 0; u < kUnroll; ++u) {
+          v[u] = make_int4(0, 0, 0, 0);
+          if (asg < p.n_assign && c0 + 32 * u < row_vec) v[u] = __ldg(src + c0 + 32 * u);
         }
-      } else {
-        for (int c0 = lane; c0 < row_vec; c0 += 32) d[c0] = make_int4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+          if (c0 + 32 * u < row_vec) d[c0 + 32 * u] = v[u];
       }
     }
     __threadfence();
-    named_bar_sync(2, 160);
-    if (warp == 3 && lane == 0) atomicAdd(p.gbar, 1);
+    named_bar_sync(2, 32 * kGatherWarps);
+    if (warp == 2 && lane == 0) atomicAdd(p.gbar, 1);
   }
 
   if (warp == 0) {
@@ -360,6 +365,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
               fence_proxy_async_global();
               c_dep += pc.lap();
               gathered = true;
+              if (ts && lane == 0) ts[kTsGathered] = globaltimer();
               if (elect_one()) {
                 for (int q = 0; q < npend; ++q) {
                   const uint32_t st = (stage + u_stg - (npend - 1) + q) % u_stg;
@@ -438,6 +444,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     }
     if (p.prof && lane == 0) {
       unsigned long long* pr = p.prof + blockIdx.x * kNumProf;
+      pr[kTsProducerDone] = globaltimer();
       pr[kPrWaitEmpty] = c_wait;
       pr[kPrIssue] = c_issue + pc.lap();
       pr[kPrWaitDep] = c_dep;
@@ -780,6 +787,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     }
     if (p.prof && et == 0) {
       unsigned long long* pr = p.prof + blockIdx.x * kNumProf;
+      pr[kTsEpilogueDone] = globaltimer();
       pr[kEpiMeta] = c_meta;
       pr[kEpiWaitAcc] = c_wacc;
       pr[kEpiSwiglu] = c_swiglu;
@@ -796,8 +804,10 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   tc_fence_after();
   if (warp == 2) tmem_dealloc<512>(tmem);
   if (threadIdx.x == 0) {
+    if (ts) ts[kTsEndArrive] = globaltimer();
     atomicAdd(p.gbar + 1, 1);
     while (ld_acquire_gpu(p.gbar + 1) < (int)gridDim.x) __nanosleep(64);
+    if (ts) ts[kTsEndPass] = globaltimer();
   }
   __syncthreads();
   {
@@ -816,6 +826,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       a4[i] = z;
     }
   }
+  if (ts && threadIdx.x == 0) ts[kTsFinal] = globaltimer();
 }
 
 }  // namespace ramp

@@ -83,6 +83,8 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
     cudaError_t err =
         cudaFuncSetAttribute(fused_moe_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(fused_moe_bf16_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (err != cudaSuccess) return err;
     attr_set = true;
   }
   // Tensor maps depend only on pointers and shapes: encode once per

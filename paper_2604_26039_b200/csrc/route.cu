@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   const int bm = a.table.bm[sel];
   int32_t* n_post_pad = a.ctrl + 1;
   block_align(a.topk_ids, a.n_assign, a.E, bm, s, st.warp_tot, a.sorted_ids, a.tile_expert,
-              n_post_pad);
+              n_post_pad, a.prof);
   stamp(3);
   const int npp = s.off[a.E];
   for (int e = threadIdx.x; e < a.E; e += blockDim.x)
@@ -148,6 +148,10 @@ cudaError_t launch_route(const RouteArgs& a, int zero_blocks, cudaStream_t strea
   if (!attr_set) {
     cudaError_t err = cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)route_smem_bytes(kMaxExperts, kIdCache));
+    if (err != cudaSuccess) return err;
+    // same shared-memory carveout as the megakernel, so SMs need no
+    // reconfiguration when the megakernel launches behind it (PDL overlap)
+    err = cudaFuncSetAttribute(route_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (err != cudaSuccess) return err;
     attr_set = true;
   }

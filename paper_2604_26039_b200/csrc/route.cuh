@@ -236,7 +236,15 @@ __device__ inline int block_exclusive_scan(int v, int* warp_tot /*[32]*/, int* t
 // Requires blockDim.x == 1024, E <= kMaxExperts and block_count() first.
 __device__ inline void block_align(const int32_t* __restrict__ ids, int64_t n, int E, int bm,
                                    RouteSmem& s, int* warp_tot, int32_t* __restrict__ sorted_ids,
-                                   int32_t* __restrict__ tile_expert, int32_t* n_post_pad_out) {
+                                   int32_t* __restrict__ tile_expert, int32_t* n_post_pad_out,
+                                   unsigned long long* stamps = nullptr) {
+  auto stamp = [&](int slot) {
+    if (stamps && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      stamps[slot] = t;
+    }
+  };
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   int padded = 0, c = 0;
   if (tid < E) {
@@ -255,6 +263,7 @@ __device__ inline void block_align(const int32_t* __restrict__ ids, int64_t n, i
     if (n_post_pad_out) *n_post_pad_out = total;
   }
   __syncthreads();
+  stamp(5);
   // each warp walks its segment again in order; position = expert base +
   // earlier warps' count + this warp's running count + rank within the chunk
   const int nbits = bits_for(E);

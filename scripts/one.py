@@ -47,7 +47,7 @@ for _ in range(a.reps):
 torch.cuda.synchronize()
 if a.prof:
     from paper_2604_26039_b200 import _lib
-    buf = torch.zeros(149 * 16, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(149 * 32, dtype=torch.int64, device="cuda")
     _lib.load().ramp_set_profile_buffer(buf.data_ptr())
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -55,10 +55,15 @@ if a.prof:
     e1.record()
     torch.cuda.synchronize()
     _lib.load().ramp_set_profile_buffer(None)
-    allb = buf.view(149, 16).cpu().numpy().astype(np.float64)
+    allb = buf.view(149, 32).cpu().numpy().astype(np.float64)
     pr = allb[:148]
     rt = allb[148]
-    print('route stamps (ns from start): hist %.0f dispatch %.0f align %.0f flag %.0f | helper start %.0f zeroed %.0f flag-seen %.0f gathered %.0f' % tuple(rt[i] - rt[0] for i in (1, 2, 3, 4, 8, 9, 10, 11)))
+    t0 = rt[0]
+    tl = ["entry", "start", "gathered", "producer_done", "epilogue_done", "end_arrive", "end_pass", "final"]
+    print("timeline (us from route start): " + "  ".join(
+        f"{n} {np.min(pr[:, 16 + i] - t0) / 1e3:.1f}/{np.median(pr[:, 16 + i] - t0) / 1e3:.1f}/{np.max(pr[:, 16 + i] - t0) / 1e3:.1f}"
+        for i, n in enumerate(tl) if np.all(pr[:, 16 + i] > 0)))
+    print('route stamps (ns from start): hist %.0f dispatch %.0f scan+pad %.0f align %.0f done %.0f' % tuple(rt[i] - rt[0] for i in (1, 2, 5, 3, 4)))
     names = ["pr_wait_empty", "pr_issue", "mma_wait_full", "mma_wait_acc", "mma_wait_act", "epi_wait_acc",
              "epi_swiglu", "epi_wait_chunk", "epi_scatter", "total", "items", "epi_meta", "pr_wait_dep"]
     act = pr[:, 10] > 0
