@@ -344,12 +344,6 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         const int wrow = jb.s * G.n_i;
         const int kb0 = G.kb_lo(jb), kb1 = G.kb_hi(jb);
         int first_pending = 0, npend = 0;
-        if (!gathered) {
-          // token rows are still being gathered (phase 0): keep HBM busy by
-          // pulling the rest of this job's weight slice toward L2 meanwhile
-          for (int kb = kb0 + u_stg + lane; kb < kb1; kb += 32) tma_prefetch_3d(tm_w1, kb * 64, wrow, 2 * e);
-          __syncwarp();
-        }
         for (int kb = kb0; kb < kb1; ++kb) {
           acquire();
           if (elect_one()) {

@@ -99,12 +99,6 @@ __device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int32_t c0, in
                "r"(c0), "r"(c1)
                : "memory");
 }
-__device__ __forceinline__ void tma_prefetch_3d(const void* tmap, int32_t c0, int32_t c1, int32_t c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
-                   reinterpret_cast<uint64_t>(tmap)),
-               "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
-}
 // Gathers four arbitrary rows (r0..r3) of a 2D tensor, `box_inner` columns each,
 // starting at column c0; rows land back to back in shared memory.
 __device__ __forceinline__ void tma_gather4(uint32_t dst, const void* tmap, uint32_t bar, int32_t c0,

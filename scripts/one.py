@@ -21,7 +21,6 @@ ap.add_argument("--stg", type=int, default=2)
 ap.add_argument("--gm", type=int, default=0)
 ap.add_argument("--mode", type=int, default=0)
 ap.add_argument("--sk", type=int, default=1)
-ap.add_argument("--side", action="store_true", help="run on a non-default stream")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--E", type=int, default=64)
 ap.add_argument("--H", type=int, default=2048)
@@ -43,8 +42,6 @@ cfg = [c.id for c in pool if (c.bm, c.ttn, c.stg, int(c.group_m), c.mode, c.spli
 x = torch.randn(S, H, device="cuda", generator=gen).to(torch.bfloat16)
 ids, w = topk(S, k, E, a.skew, gen)
 ws = M.Workspace(S, H, I, E, k)
-if a.side:
-    torch.cuda.set_stream(torch.cuda.Stream())
 for _ in range(a.reps):
     out = M.fused_moe(x, w1, w2, w, ids, table, cfg, workspace=ws)
 torch.cuda.synchronize()
