@@ -70,6 +70,7 @@ struct MoeMaps {
   CUtensorMap act[4];  // act_g    [rows, I],  box {64, 16/32/64/128}
   CUtensorMap w1[3];   // W1 as [2E, I, H],    box {64, n_i, 2} for n_i = 64 / 128 / 256
   CUtensorMap w2;      // W2 as [E*H, I],      box {64, 128}
+  CUtensorMap x;       // x [S, H], box {64, 1}: TMA gather4 of token rows (bm <= 16 configs)
 };
 
 struct MoeParams {
@@ -207,8 +208,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
 
   // Prologue (overlaps the route kernel's tail under PDL): descriptors,
   // barriers, TMEM.  Nothing here reads the route kernel's outputs.
-  if (warp == 0 && lane < 12) {
-    const CUtensorMap* all = &maps.xs[0];  // xs[4], act[4], w1[3], w2 are contiguous
+  if (warp == 0 && lane < 13) {
+    const CUtensorMap* all = &maps.xs[0];  // xs[4], act[4], w1[3], w2, x are contiguous
     tma_prefetch_desc(all + lane);
   }
   if (warp == 1 && lane == 0) {
@@ -271,7 +272,11 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   // order (warps 2-7 of every CTA, 8 x 16-byte loads in flight per lane),
   // then arrive on grid barrier 0.  The producers stream weights meanwhile
   // and hold back token tiles until all CTAs have arrived.
-  if (warp >= 2) {
+  // Token blocks of <= 16 rows skip phase 0: their producer gathers the rows
+  // straight from x with TMA gather4 (4 rows per instruction), so decode-size
+  // calls need no grid barrier before the first MMA.
+  const bool direct_x = bmN == 16;
+  if (warp >= 2 && !direct_x) {
     constexpr int kGatherWarps = 6, kUnroll = 8;
     const int row_vec = p.H / 8;  // 16-byte vectors per row
     const int gw = blockIdx.x * kGatherWarps + (warp - 2), nw = gridDim.x * kGatherWarps;
@@ -321,7 +326,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       c_wait += pc.lap();
     };
     uint32_t js = 0, jph = 0;
-    bool gathered = false;
+    bool gathered = direct_x;
     while (true) {
       // claim the next job (dynamic, in global order) and publish it to the ring
       int j = 0;
@@ -344,6 +349,16 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         const int wrow = jb.s * G.n_i;
         const int kb0 = G.kb_lo(jb), kb1 = G.kb_hi(jb);
         int first_pending = 0, npend = 0;
+        int trow[16];  // direct_x: token row of each of the 16 MMA columns
+        if (direct_x) {
+          int mine = 0;
+          if (lane < G.bm) {
+            const int a = p.sorted_ids[row0 + lane];
+            mine = a < p.n_assign ? a / p.top_k : 0;
+          }
+#pragma unroll
+          for (int q = 0; q < 16; ++q) trow[q] = __shfl_sync(0xffffffffu, mine, q);
+        }
         for (int kb = kb0; kb < kb1; ++kb) {
           acquire();
           if (elect_one()) {
@@ -351,7 +366,14 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             const uint32_t sb = ring_addr + stage * u_sbytes;
             mbar_arrive_expect_tx(full, tx1);
             tma_load_3d(sb, tm_w1, full, kb * 64, wrow, 2 * e, pol_w);
-            if (gathered) tma_load_2d(sb + nA * kSubTileBytes, tm_xs, full, kb * 64, row0, pol_x);
+            if (direct_x) {
+#pragma unroll
+              for (int q = 0; q < 16; q += 4)
+                tma_gather4(sb + nA * kSubTileBytes + q * 128, &maps.x, full, kb * 64, trow[q], trow[q + 1],
+                            trow[q + 2], trow[q + 3], pol_x);
+            } else if (gathered) {
+              tma_load_2d(sb + nA * kSubTileBytes, tm_xs, full, kb * 64, row0, pol_x);
+            }
           }
           __syncwarp();
           if (!gathered) {

@@ -90,12 +90,12 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
   // Tensor maps depend only on pointers and shapes: encode once per
   // (workspace, weights, shape) and reuse (the encoder costs ~1 us per map).
   struct MapKey {
-    const void *xs, *act, *w1, *w2;
+    const void *xs, *act, *w1, *w2, *x;
     int64_t rows;
-    int32_t H, I, E;
+    int32_t S, H, I, E;
     bool operator==(const MapKey& o) const {
-      return xs == o.xs && act == o.act && w1 == o.w1 && w2 == o.w2 && rows == o.rows && H == o.H && I == o.I &&
-             E == o.E;
+      return xs == o.xs && act == o.act && w1 == o.w1 && w2 == o.w2 && x == o.x && rows == o.rows && S == o.S &&
+             H == o.H && I == o.I && E == o.E;
     }
   };
   struct MapEntry {
@@ -106,7 +106,7 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
   static MapEntry cache[16];
   static int cache_next = 0;
   static std::mutex cache_mu;
-  const MapKey key{l.x_sorted, l.act_g, l.w1, l.w2, l.rows, l.H, l.I, l.E};
+  const MapKey key{l.x_sorted, l.act_g, l.w1, l.w2, l.x, l.rows, l.S, l.H, l.I, l.E};
   alignas(64) MoeMaps maps;  // copied into the launch's parameter buffer
   bool hit = false;
   {
@@ -132,6 +132,7 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
       ok = ok && ((l.I % (64 << i)) != 0 || make_map(&maps.w1[i], l.w1, 3, dims, strides, box));
     }
     ok = ok && make_map_2d(&maps.w2, l.w2, (uint64_t)l.E * l.H, l.I, 128);
+    ok = ok && make_map_2d(&maps.x, l.x, (uint64_t)l.S, l.H, 1);
     if (!ok) {
       *why = "cuTensorMapEncodeTiled failed (alignment or driver entry point)";
       return cudaErrorInvalidValue;

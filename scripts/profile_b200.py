@@ -1,4 +1,4 @@
-"""One-time B200 profiling sweep -> reference-format trace -> P4 fit -> coeffs.
+"""One-time B200 profiling sweep -> reference-format trace -> fit -> coeffs.
 
     python scripts/profile_b200.py --model OLMoE-1B-7B [--plan-reps 3] [--iters 3]
 
@@ -7,7 +7,10 @@ for every (S, beta) point of ramp's profiling plan (5 batch sizes x 5 skews,
 ramp/cost_model.py:212-231) and every routing seed, every config of the B200
 pool is launched and timed (sweep.MeasuredTimer), the samples are written in
 ramp's trace CSV schema (loadable by ramp.load_trace), and each config's four
-coefficients are fitted with the reference's OLS (cost_model.fit, variant P4).
+coefficients are fitted with the reference's OLS (cost_model.fit).  The model
+variant (P2 / P3 / P4, the reference's ablation ladder) is chosen by held-out
+dispatch regret on the sweep itself (choose_variant): on the persistent,
+dynamically scheduled megakernel the wave staircase is weak and P2 wins.
 Outputs (under paper_2604_26039_b200/data/ unless --out is given):
     trace_<model>_b200.csv, coeffs_<model>_b200.json, fit_<model>_b200.json
 Then it evaluates the fitted table against an exhaustive on-GPU sweep over the
@@ -37,6 +40,35 @@ from paper_2604_26039_b200.sweep import MeasuredTimer  # noqa: E402
 from paper_2604_26039_b200.trace import profile  # noqa: E402
 
 
+def choose_variant(pool, trace, hw):
+    """Pick the cost-model variant (P2 / P3 / P4, ramp/cost_model.py:163-196)
+    with the lowest held-out dispatch regret: fit on routing seeds 0-1 of every
+    plan point, select on seed 2, compare with the measured best there."""
+    from paper_2604_26039_b200.cost_model import predict_batch
+
+    points: dict = {}
+    for s in trace.samples:
+        points.setdefault((s.S, s.beta_target), {}).setdefault(s.seed, {})[s.config_id] = s
+    train, test = [], []
+    for _, by_seed in sorted(points.items()):
+        seeds = sorted(by_seed)
+        train += [by_seed[x] for x in seeds[:-1]]
+        test += [by_seed[seeds[-1]]]
+    ids = [c.id for c in pool]
+    out = {}
+    for variant in ("P2", "P3", "P4"):
+        co = [fit([pt[c] for pt in train], hw, variant).coefficients for c in ids]
+        a, b, c_, d = (np.array([getattr(x, f) for x in co]) for f in "abcd")
+        regs = []
+        for pt in test:
+            g = np.array([pt[c].g for c in ids])
+            t = np.array([pt[c].time_us for c in ids])
+            sel = int(np.argmin(predict_batch(a, b, c_, d, g, hw.sm_count)))
+            regs.append(t[sel] / t.min() - 1.0)
+        out[variant] = float(np.mean(regs))
+    return min(out, key=out.get), out
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="OLMoE-1B-7B", choices=sorted(BASELINE_MODELS))
@@ -45,6 +77,7 @@ def main() -> None:
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--out", default=str(ROOT / "paper_2604_26039_b200" / "data"))
     ap.add_argument("--skip-eval", action="store_true")
+    ap.add_argument("--eval-iters", type=int, default=7)
     a = ap.parse_args()
     out = Path(a.out)
     out.mkdir(parents=True, exist_ok=True)
@@ -69,17 +102,20 @@ def main() -> None:
     by_cfg: dict[int, list] = {}
     for s in trace.samples:
         by_cfg.setdefault(s.config_id, []).append(s)
-    reports = {cid: fit(ss, hw, "P4") for cid, ss in by_cfg.items()}
+    variant, validation = choose_variant(pool, trace, hw)
+    reports = {cid: fit(ss, hw, variant) for cid, ss in by_cfg.items()}
     write_coeff_store(out / f"coeffs_{tag}.json", coeff_store_dict(a.model, hw.sm_count, reports))
     r2 = np.array([r.r_squared for r in reports.values()])
     summary = {"model": a.model, "pool": n, "plan_points": len(plan), "samples": len(trace.samples),
-               "profile_s": round(t_prof, 1), "r2_median": float(np.median(r2)), "r2_min": float(r2.min())}
+               "profile_s": round(t_prof, 1), "r2_median": float(np.median(r2)), "r2_min": float(r2.min()),
+               "variant": variant, "heldout_regret_by_variant": validation}
     print(json.dumps(summary), flush=True)
     if not a.skip_eval:
         table = DispatchTable(model=a.model, pool=pool,
                               coefficients={c: r.coefficients for c, r in reports.items()},
                               sm_count=hw.sm_count)
         t0 = time.time()
+        timer.iters = a.eval_iters
         reg = evaluate_regret(table, pool, geom, timer, seeds_per_point=a.eval_reps)
         spd = speedup_ra_vs_static(table, pool, geom, timer, seeds_per_point=a.eval_reps)
         (out / f"regret_{tag}.csv").write_text(reg.to_csv())
