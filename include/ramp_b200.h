@@ -136,6 +136,21 @@ int ramp_fused_moe_bf16_ex(const void* x, const void* w1, const void* w2, const 
                            int32_t* sel_out, void* workspace, size_t workspace_bytes, int32_t phases,
                            void* stream);
 
+/* Fused MoE layer forward, block-scaled FP8 (MXFP8: E4M3 operands with one
+ * UE8M0 scale per 32 K elements, kind::mxf8f6f4.block_scale MMAs).
+ * w1_q [E,2I,H] / w2_q [E,H,I] e4m3; w1_sf / w2_sf their scale atoms tiled as
+ * [rows/128][K/128][512 B] (paper_2604_26039_b200/quant.py tile_scales);
+ * tokens arrive in bf16 and are quantised on the fly (per token, per 32).
+ * The table must hold FP8 configs (split mode, bm >= 16, ttn >= 256,
+ * ramp_config_smem_bytes_fp8 > 0).  d_ff must be a multiple of 256.
+ * Replaces the W8A8 FP8 kernel of the paper. */
+int ramp_fused_moe_fp8(const void* x, const void* w1_q, const uint8_t* w1_sf, const void* w2_q,
+                       const uint8_t* w2_sf, const float* topk_w, const int32_t* topk_ids, int32_t S, int32_t H,
+                       int32_t I, int32_t E, int32_t top_k, const ramp_table_t* table, int32_t forced_cfg,
+                       void* out, int32_t* sel_out, void* workspace, size_t workspace_bytes, int32_t phases,
+                       void* stream);
+int64_t ramp_config_smem_bytes_fp8(int32_t bm, int32_t ttn, int32_t stg);
+
 /* Shared-memory bytes the megakernel needs for (bm, ttn, stg, mode); 0 if the
  * configuration is not realisable on this part (pool admissibility test,
  * the B200 counterpart of smem_usage/is_valid, ramp/config_space.py:122-138). */

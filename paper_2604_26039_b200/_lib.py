@@ -42,6 +42,11 @@ SIGNATURES = {
          ctypes.c_size_t, ctypes.c_void_p],
     ),
 }
+SIGNATURES["ramp_config_smem_bytes_fp8"] = (ctypes.c_int64, [ctypes.c_int32] * 3)
+SIGNATURES["ramp_fused_moe_fp8"] = (
+    ctypes.c_int,
+    [ctypes.c_void_p] * 7 + [ctypes.c_int32] * 5 + [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                                                    ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32, ctypes.c_void_p])
 SIGNATURES["ramp_fused_moe_bf16_ex"] = (
     ctypes.c_int, SIGNATURES["ramp_fused_moe_bf16"][1][:-1] + [ctypes.c_int32, ctypes.c_void_p])
 

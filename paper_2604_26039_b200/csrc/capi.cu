@@ -26,7 +26,7 @@ int cuda_fail(cudaError_t err, const char* where) {
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct WorkspaceLayout {
-  size_t ctrl, hist, sorted, tiles, done, acc, xs, act, acc_a, split_cnt, total;
+  size_t ctrl, hist, sorted, tiles, done, acc, xs, act, acc_a, split_cnt, xq, xsf, actq, actsf, total;
   int64_t capacity, rows;
 };
 
@@ -55,6 +55,11 @@ WorkspaceLayout layout_for(int32_t S, int32_t H, int32_t I, int32_t E, int32_t t
   w.act = take(2 * (size_t)w.rows * I);
   w.acc_a = take(4 * (size_t)w.rows * 2 * I);
   w.split_cnt = take(sizeof(int32_t) * w.capacity);
+  const int64_t mt_max = w.capacity / 16 + 1;  // FP8 configs use bm >= 16
+  w.xq = take((size_t)w.rows * H);
+  w.xsf = take((size_t)mt_max * (H / 128 + 1) * 512);
+  w.actq = take((size_t)w.rows * I);
+  w.actsf = take((size_t)mt_max * (I / 128 + 1) * 512);
   w.total = off;
   return w;
 }
@@ -98,7 +103,12 @@ int64_t ramp_align_capacity(int64_t n_assign, int32_t E, int32_t bm) {
 }
 
 int64_t ramp_config_smem_bytes(int32_t bm, int32_t ttn, int32_t stg, int32_t mode) {
-  return ramp::config_smem_bytes(bm, ttn, stg, mode);
+  return ramp::config_smem_bytes(bm, ttn, stg, mode, false);
+}
+
+int64_t ramp_config_smem_bytes_fp8(int32_t bm, int32_t ttn, int32_t stg) {
+  if (bm < 16 || ttn < 256 || (ttn / 128) * ramp::bm_mma_host(bm) > 448) return 0;
+  return ramp::config_smem_bytes(bm, ttn, stg, 1, true);
 }
 
 int ramp_moe_align(const int32_t* topk_ids, int64_t n_assign, int32_t E, int32_t bm, int32_t* hist,
@@ -131,10 +141,10 @@ size_t ramp_fused_moe_workspace_size(int32_t S, int32_t H, int32_t I, int32_t E,
   return layout_for(S, H, I, E, top_k).total;
 }
 
-int ramp_fused_moe_bf16_ex(const void* x, const void* w1, const void* w2, const float* topk_w,
-                           const int32_t* topk_ids, int32_t S, int32_t H, int32_t I, int32_t E, int32_t top_k,
-                           const ramp_table_t* table, int32_t forced_cfg, void* out, int32_t* sel_out,
-                           void* workspace, size_t workspace_bytes, int32_t phases, void* stream) {
+static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const void* w2, const uint8_t* w2_sf,
+                      const float* topk_w, const int32_t* topk_ids, int32_t S, int32_t H, int32_t I, int32_t E,
+                      int32_t top_k, const ramp_table_t* table, int32_t forced_cfg, void* out, int32_t* sel_out,
+                      void* workspace, size_t workspace_bytes, int32_t phases, void* stream, bool fp8) {
   if (phases < 1 || phases > 3) return fail(RAMP_EINVAL, "phases must be 1 (route), 2 (megakernel) or 3");
   if (int rc = check_table(table)) return rc;
   if (S < 0) return fail(RAMP_EINVAL, "S must be >= 0");
@@ -209,6 +219,13 @@ int ramp_fused_moe_bf16_ex(const void* x, const void* w1, const void* w2, const 
   ml.rows = L.rows;
   ml.acc_a = reinterpret_cast<float*>(ws + L.acc_a);
   ml.split_cnt = reinterpret_cast<int*>(ws + L.split_cnt);
+  ml.fp8 = fp8;
+  ml.w1_sf = w1_sf;
+  ml.w2_sf = w2_sf;
+  ml.x_q = ws + L.xq;
+  ml.x_sf = ws + L.xsf;
+  ml.act_q = ws + L.actq;
+  ml.act_sf = ws + L.actsf;
   ml.table = *table;
   ml.S = S;
   ml.H = H;
@@ -216,9 +233,17 @@ int ramp_fused_moe_bf16_ex(const void* x, const void* w1, const void* w2, const 
   ml.E = E;
   ml.top_k = top_k;
   const char* why = nullptr;
-  err = ramp::launch_fused_moe_bf16(ml, st, &why);
+  err = ramp::launch_fused_moe(ml, st, &why);
   if (err != cudaSuccess) return why ? fail(RAMP_ECUDA, why) : cuda_fail(err, "fused_moe kernel");
   return RAMP_OK;
+}
+
+int ramp_fused_moe_bf16_ex(const void* x, const void* w1, const void* w2, const float* topk_w,
+                           const int32_t* topk_ids, int32_t S, int32_t H, int32_t I, int32_t E, int32_t top_k,
+                           const ramp_table_t* table, int32_t forced_cfg, void* out, int32_t* sel_out,
+                           void* workspace, size_t workspace_bytes, int32_t phases, void* stream) {
+  return fused_impl(x, w1, nullptr, w2, nullptr, topk_w, topk_ids, S, H, I, E, top_k, table, forced_cfg, out,
+                    sel_out, workspace, workspace_bytes, phases, stream, false);
 }
 
 int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const float* topk_w,
@@ -227,6 +252,16 @@ int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const flo
                         void* workspace, size_t workspace_bytes, void* stream) {
   return ramp_fused_moe_bf16_ex(x, w1, w2, topk_w, topk_ids, S, H, I, E, top_k, table, forced_cfg, out, sel_out,
                                 workspace, workspace_bytes, 3, stream);
+}
+
+int ramp_fused_moe_fp8(const void* x, const void* w1_q, const uint8_t* w1_sf, const void* w2_q,
+                       const uint8_t* w2_sf, const float* topk_w, const int32_t* topk_ids, int32_t S, int32_t H,
+                       int32_t I, int32_t E, int32_t top_k, const ramp_table_t* table, int32_t forced_cfg, void* out,
+                       int32_t* sel_out, void* workspace, size_t workspace_bytes, int32_t phases, void* stream) {
+  if (S > 0 && (!w1_sf || !w2_sf)) return fail(RAMP_EINVAL, "null scale-factor tensor");
+  if (I % 256 != 0) return fail(RAMP_EINVAL, "FP8 path needs d_ff a multiple of 256");
+  return fused_impl(x, w1_q, w1_sf, w2_q, w2_sf, topk_w, topk_ids, S, H, I, E, top_k, table, forced_cfg, out,
+                    sel_out, workspace, workspace_bytes, phases, stream, true);
 }
 
 }  // extern "C"

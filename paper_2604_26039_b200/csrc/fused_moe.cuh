@@ -54,15 +54,24 @@ __host__ __device__ inline int stage_bytes(int bm, int ttn) {
   const int raw = (ttn >= 256 ? ttn / 128 : 1) * kSubTileBytes + bm_mma(bm) * 128;
   return (raw + 1023) / 1024 * 1024;
 }
+// FP8 (MXFP8) stages also carry the 512-byte scale-factor atoms of the nA
+// weight tiles and of the token tile.
+__host__ __device__ inline int stage_bytes_fp8(int bm, int ttn) {
+  const int nA = ttn >= 256 ? ttn / 128 : 1;
+  const int raw = nA * kSubTileBytes + bm_mma(bm) * 128 + (nA + 1) * 512;
+  return (raw + 1023) / 1024 * 1024;
+}
 __host__ __device__ inline int act_bytes(int bm, int ttn, int mode) {
   return mode == kModeFused ? bm_mma(bm) * ttn : 0;
 }
 // Dynamic shared memory of one config (the B200 counterpart of smem_usage(),
 // ramp/config_space.py:122-124): 1 KB alignment slack, control block,
 // scatter transpose buffer, stg ring stages, fused mode's bf16 act tile.
-__host__ __device__ inline int moe_smem_bytes(int bm, int ttn, int stg, int mode) {
-  return 1024 + kCtrlBytes + kStageBytesScatter + stg * stage_bytes(bm, ttn) + act_bytes(bm, ttn, mode);
+__host__ __device__ inline int moe_smem_bytes(int bm, int ttn, int stg, int mode, bool fp8 = false) {
+  return 1024 + kCtrlBytes + kStageBytesScatter + stg * (fp8 ? stage_bytes_fp8(bm, ttn) : stage_bytes(bm, ttn)) +
+         (fp8 ? 0 : act_bytes(bm, ttn, mode));
 }
+constexpr int kSfCol = 480;  // TMEM columns 480.. hold the scale factors of the FP8 MMAs
 __host__ __device__ inline int bmn_index(int bmN) { return bmN <= 16 ? 0 : bmN <= 32 ? 1 : bmN <= 64 ? 2 : 3; }
 
 struct MoeMaps {
@@ -71,6 +80,11 @@ struct MoeMaps {
   CUtensorMap w1[3];   // W1 as [2E, I, H],    box {64, n_i, 2} for n_i = 64 / 128 / 256
   CUtensorMap w2;      // W2 as [E*H, I],      box {64, 128}
   CUtensorMap x;       // x [S, H], box {64, 1}: TMA gather4 of token rows (bm <= 16 configs)
+  // FP8 path (byte tensors, 128 elements per 128-byte swizzled row)
+  CUtensorMap xq[4];   // x_q   [rows, H] e4m3, box {128, 16/32/64/128}
+  CUtensorMap actq[4]; // act_q [rows, I] e4m3, box {128, 16/32/64/128}
+  CUtensorMap w1q[2];  // W1 e4m3 as [2E, I, H], box {128, n_i, 2} for n_i = 128 / 256
+  CUtensorMap w2q;     // W2 e4m3 as [E*H, I],   box {128, 128}
 };
 
 struct MoeParams {
@@ -88,6 +102,13 @@ struct MoeParams {
   const __nv_bfloat16* x;      // [S, H] tokens
   __nv_bfloat16* x_sorted;     // [rows, H] expert-sorted token rows (gathered in phase 0)
   __nv_bfloat16* out;          // [S, H] bf16 result
+  // FP8 (MXFP8): e4m3 operands + UE8M0 scale atoms [row block][k block][512 B]
+  const uint8_t* w1_sf;        // [2E*I/128][H/128][512]
+  const uint8_t* w2_sf;        // [E*H/128][I/128][512]
+  uint8_t* x_q;                // [rows, H] quantised, expert-sorted tokens (phase 0)
+  uint8_t* x_sf;               // [M-tiles][H/128][512]
+  uint8_t* act_q;              // [rows, I] quantised SwiGLU activations
+  uint8_t* act_sf;             // [M-tiles][I/128][512]
   ramp_table_t table;
   int32_t S, H, I, E, top_k, n_assign;
   unsigned long long* prof;    // optional per-CTA cycle counters [gridDim][16] (diagnostics)
@@ -191,8 +212,10 @@ __device__ __forceinline__ void scatter16(const float (&v)[16], int j0, int bm, 
   named_bar_sync(1, 128);
 }
 
+template <bool kFp8>
 __global__ void __launch_bounds__(kMoeThreads, 1)
-    fused_moe_bf16_kernel(const __grid_constant__ MoeMaps maps, const MoeParams p) {
+    fused_moe_kernel(const __grid_constant__ MoeMaps maps, const MoeParams p) {
+  constexpr int kKb = kFp8 ? 128 : 64;  // K elements per 128-byte swizzled row / k-block
   extern __shared__ unsigned char smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   const uint32_t base_addr = (raw_addr + 1023u) & ~1023u;  // SW128 tiles need 1 KB alignment
@@ -209,8 +232,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   // Prologue (overlaps the route kernel's tail under PDL): descriptors,
   // barriers, TMEM.  Nothing here reads the route kernel's outputs.
   if (warp == 0 && lane < 13) {
-    const CUtensorMap* all = &maps.xs[0];  // xs[4], act[4], w1[3], w2, x are contiguous
-    tma_prefetch_desc(all + lane);
+    // bf16: xs[4], act[4], w1[3], w2, x; fp8: xq[4], actq[4], w1q[2], w2q (contiguous)
+    const CUtensorMap* all = kFp8 ? &maps.xq[0] : &maps.xs[0];
+    if (!kFp8 || lane < 11) tma_prefetch_desc(all + lane);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kMaxStages; ++s) {
@@ -252,21 +276,23 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   G.stripes = p.I / G.n_i;
   G.n_mtiles = n_post_pad / G.bm;
   G.n_hc = p.H / 128;
-  G.kbH = p.H / 64;
-  G.kbI = p.I / 64;
+  G.kbH = p.H / kKb;
+  G.kbI = p.I / kKb;
   G.group_m = p.table.group_m[cfg];
   G.sk = (G.mode == kModeSplit && p.table.split_k[cfg] > 1) ? p.table.split_k[cfg] : 1;
   G.nJobA = G.n_mtiles * G.stripes * G.sk;
   G.total = G.nJobA + (G.mode == kModeSplit ? G.n_mtiles * G.n_hc * G.sk : 0);
-  G.dbl = G.mode == kModeSplit && G.nA * G.bmN <= 256;
+  G.dbl = !kFp8 && G.mode == kModeSplit && G.nA * G.bmN <= 256;
   const int bmN = G.bmN, nA = G.nA;
-  const int sbytes = stage_bytes(G.bm, ttn);
+  const int sbytes = kFp8 ? stage_bytes_fp8(G.bm, ttn) : stage_bytes(G.bm, ttn);
   const uint32_t act_addr = ring_addr + stg * sbytes;
   unsigned char* act_ptr = base + kCtrlBytes + kStageBytesScatter + stg * sbytes;
-  const CUtensorMap* tm_xs = &maps.xs[bmn_index(bmN)];
-  const CUtensorMap* tm_act = &maps.act[bmn_index(bmN)];
-  const CUtensorMap* tm_w1 = &maps.w1[G.n_i == 256 ? 2 : G.n_i == 128 ? 1 : 0];
-  const CUtensorMap* tm_w2 = &maps.w2;
+  const CUtensorMap* tm_xs = kFp8 ? &maps.xq[bmn_index(bmN)] : &maps.xs[bmn_index(bmN)];
+  const CUtensorMap* tm_act = kFp8 ? &maps.actq[bmn_index(bmN)] : &maps.act[bmn_index(bmN)];
+  const CUtensorMap* tm_w1 =
+      kFp8 ? &maps.w1q[G.n_i == 256 ? 1 : 0] : &maps.w1[G.n_i == 256 ? 2 : G.n_i == 128 ? 1 : 0];
+  const CUtensorMap* tm_w2 = kFp8 ? &maps.w2q : &maps.w2;
+  const int sf_off = nA * kSubTileBytes + bmN * 128;  // FP8: scale atoms after the operand tiles
 
   // ---- phase 0: gather the token rows of every M-tile into expert-sorted
   // order (warps 2-7 of every CTA, 8 x 16-byte loads in flight per lane),
@@ -275,8 +301,54 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   // Token blocks of <= 16 rows skip phase 0: their producer gathers the rows
   // straight from x with TMA gather4 (4 rows per instruction), so decode-size
   // calls need no grid barrier before the first MMA.
-  const bool direct_x = bmN == 16;
-  if (warp >= 2 && !direct_x) {
+  const bool direct_x = !kFp8 && bmN == 16;
+  if (kFp8 && warp >= 2) {
+    // FP8: gather + quantise every row to MXFP8 (per-32 power-of-two scales)
+    // into x_q and the per-M-tile scale atoms x_sf.
+    constexpr int kGatherWarps = 6;
+    const int row_vec = p.H / 8;  // 8 bf16 per lane-chunk; 4 consecutive lanes = one 32-group
+    const int gw = blockIdx.x * kGatherWarps + (warp - 2), nw = gridDim.x * kGatherWarps;
+    const int4* xv = reinterpret_cast<const int4*>(p.x);
+    for (int r = gw; r < n_post_pad; r += nw) {
+      const int asg = p.sorted_ids[r];
+      const int m = r / G.bm, jr = r % G.bm;
+      const int4* src = xv + static_cast<int64_t>(asg < p.n_assign ? asg / p.top_k : 0) * row_vec;
+      for (int c = lane; c < row_vec; c += 32) {
+        int4 v = make_int4(0, 0, 0, 0);
+        if (asg < p.n_assign) v = __ldg(src + c);
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&v);
+        float f[8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float2 t = __bfloat1622float2(h2[u]);
+          f[2 * u] = t.x;
+          f[2 * u + 1] = t.y;
+        }
+        float amax = 0.f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) amax = fmaxf(amax, fabsf(f[u]));
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+        const int ex = amax > 0.f ? max(-127, min(127, (int)ceilf(log2f(amax / 448.0f)))) : -127;
+        const float inv = exp2f(static_cast<float>(-ex));
+        uint2 q;
+        q.x = static_cast<uint32_t>(e4m3x2_from_float(f[0] * inv, f[1] * inv)) |
+              (static_cast<uint32_t>(e4m3x2_from_float(f[2] * inv, f[3] * inv)) << 16);
+        q.y = static_cast<uint32_t>(e4m3x2_from_float(f[4] * inv, f[5] * inv)) |
+              (static_cast<uint32_t>(e4m3x2_from_float(f[6] * inv, f[7] * inv)) << 16);
+        *reinterpret_cast<uint2*>(p.x_q + static_cast<int64_t>(r) * p.H + c * 8) = q;
+        if ((lane & 3) == 0) {
+          const int g = c >> 2;  // 32-element group index along H
+          p.x_sf[(static_cast<int64_t>(m) * G.kbH + (g >> 2)) * 512 + (jr & 31) * 16 + (jr >> 5) * 4 + (g & 3)] =
+              static_cast<uint8_t>(ex + 127);
+        }
+      }
+    }
+    __threadfence();
+    named_bar_sync(2, 32 * kGatherWarps);
+    if (warp == 2 && lane == 0) atomicAdd(p.gbar, 1);
+  }
+  if (!kFp8 && warp >= 2 && !direct_x) {
     constexpr int kGatherWarps = 6, kUnroll = 8;
     const int row_vec = p.H / 8;  // 16-byte vectors per row
     const int gw = blockIdx.x * kGatherWarps + (warp - 2), nw = gridDim.x * kGatherWarps;
@@ -345,7 +417,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       const int e = warp_uniform(p.tile_expert[jb.m]);
       const int row0 = jb.m * G.bm;
       if (jb.kind == 0) {
-        const uint32_t tx1 = nA * kSubTileBytes + bmN * 128;
+        const uint32_t tx1 = nA * kSubTileBytes + bmN * 128 + (kFp8 ? (nA + 1) * 512 : 0);
         const int wrow = jb.s * G.n_i;
         const int kb0 = G.kb_lo(jb), kb1 = G.kb_hi(jb);
         int first_pending = 0, npend = 0;
@@ -359,20 +431,34 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
 #pragma unroll
           for (int q = 0; q < 16; ++q) trow[q] = __shfl_sync(0xffffffffu, mine, q);
         }
+        // token-side loads of one k-block (tile + FP8 scale atom), deferrable
+        auto load_tokens = [&](uint32_t sb, uint32_t full, int kb) {
+          tma_load_2d(sb + nA * kSubTileBytes, tm_xs, full, kb * kKb, row0, pol_x);
+          if constexpr (kFp8)
+            bulk_g2s(sb + sf_off + nA * 512, p.x_sf + (static_cast<int64_t>(jb.m) * G.kbH + kb) * 512, 512, full);
+        };
         for (int kb = kb0; kb < kb1; ++kb) {
           acquire();
           if (elect_one()) {
             const uint32_t full = smem_u32(&cs.full[stage]);
             const uint32_t sb = ring_addr + stage * u_sbytes;
             mbar_arrive_expect_tx(full, tx1);
-            tma_load_3d(sb, tm_w1, full, kb * 64, wrow, 2 * e, pol_w);
+            tma_load_3d(sb, tm_w1, full, kb * kKb, wrow, 2 * e, pol_w);
+            if constexpr (kFp8) {
+              for (int t = 0; t < nA; ++t) {
+                const int half = nA / 2;
+                const int64_t rb = (static_cast<int64_t>(e) * 2 * p.I + (t < half ? 0 : p.I) + wrow +
+                                    (t % half) * 128) / 128;
+                bulk_g2s(sb + sf_off + t * 512, p.w1_sf + (rb * G.kbH + kb) * 512, 512, full);
+              }
+            }
             if (direct_x) {
 #pragma unroll
               for (int q = 0; q < 16; q += 4)
                 tma_gather4(sb + nA * kSubTileBytes + q * 128, &maps.x, full, kb * 64, trow[q], trow[q + 1],
                             trow[q + 2], trow[q + 3], pol_x);
             } else if (gathered) {
-              tma_load_2d(sb + nA * kSubTileBytes, tm_xs, full, kb * 64, row0, pol_x);
+              load_tokens(sb, full, kb);
             }
           }
           __syncwarp();
@@ -391,8 +477,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
               if (elect_one()) {
                 for (int q = 0; q < npend; ++q) {
                   const uint32_t st = (stage + u_stg - (npend - 1) + q) % u_stg;
-                  tma_load_2d(ring_addr + st * u_sbytes + nA * kSubTileBytes, tm_xs, smem_u32(&cs.full[st]),
-                              (first_pending + q) * 64, row0, pol_x);
+                  load_tokens(ring_addr + st * u_sbytes, smem_u32(&cs.full[st]), first_pending + q);
                 }
               }
               __syncwarp();
@@ -418,7 +503,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       } else {
         // Split phase 3: weights stream immediately; the act rows wait for
         // every phase-1 job of this M-tile (release/acquire on done[m]).
-        const uint32_t tx = kSubTileBytes + bmN * 128;
+        const uint32_t tx = kSubTileBytes + bmN * 128 + (kFp8 ? 2 * 512 : 0);
         const int wrow = e * p.H + jb.hc * 128;
         const int kb0 = G.kb_lo(jb), kb1 = G.kb_hi(jb);
         int first_pending = 0, npend = 0;
@@ -427,17 +512,26 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         // still being produced by the phase-1 jobs, HBM keeps streaming weights,
         // and once the dependency resolves the slice arrives from L2.
         if (ld_acquire_gpu(p.done + jb.m) < G.stripes) {
-          for (int kb = kb0 + u_stg + lane; kb < kb1; kb += 32) tma_prefetch_2d(tm_w2, kb * 64, wrow);
+          for (int kb = kb0 + u_stg + lane; kb < kb1; kb += 32) tma_prefetch_2d(tm_w2, kb * kKb, wrow);
         }
         __syncwarp();
+        auto load_act = [&](uint32_t sb, uint32_t full, int kb) {
+          tma_load_2d(sb + kSubTileBytes, tm_act, full, kb * kKb, row0, pol_x);
+          if constexpr (kFp8)
+            bulk_g2s(sb + kSubTileBytes + bmN * 128 + 512, p.act_sf + (static_cast<int64_t>(jb.m) * G.kbI + kb) * 512,
+                     512, full);
+        };
         for (int kb = kb0; kb < kb1; ++kb) {
           acquire();
           if (elect_one()) {
             const uint32_t full = smem_u32(&cs.full[stage]);
             const uint32_t sb = ring_addr + stage * u_sbytes;
             mbar_arrive_expect_tx(full, tx);
-            tma_load_2d(sb, tm_w2, full, kb * 64, wrow, pol_w);
-            if (ready) tma_load_2d(sb + kSubTileBytes, tm_act, full, kb * 64, row0, pol_x);
+            tma_load_2d(sb, tm_w2, full, kb * kKb, wrow, pol_w);
+            if constexpr (kFp8)
+              bulk_g2s(sb + kSubTileBytes + bmN * 128, p.w2_sf + (static_cast<int64_t>(wrow / 128) * G.kbI + kb) * 512,
+                       512, full);
+            if (ready) load_act(sb, full, kb);
           }
           __syncwarp();
           if (!ready) {
@@ -453,8 +547,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
                 // the pending k-blocks sit in the npend stages ending at `stage`
                 for (int q = 0; q < npend; ++q) {
                   const uint32_t st = (stage + u_stg - (npend - 1) + q) % u_stg;
-                  tma_load_2d(ring_addr + st * u_sbytes + kSubTileBytes, tm_act, smem_u32(&cs.full[st]),
-                              (first_pending + q) * 64, row0, pol_x);
+                  load_act(ring_addr + st * u_sbytes, smem_u32(&cs.full[st]), first_pending + q);
                 }
               }
               __syncwarp();
@@ -528,11 +621,23 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           const uint64_t da = sw128_kmajor_desc(sb);
           const uint64_t db = sw128_kmajor_desc(sb + nA * kSubTileBytes);
           if (elect_one()) {
-            for (int t = 0; t < nA; ++t) {
+            if constexpr (kFp8) {
+              // scale atoms smem -> TMEM; in-order with the MMAs that read them
+              for (int t = 0; t <= nA; ++t) tmem_cp_sf(u_tmem + kSfCol + 4 * t, sf_atom_desc(sb + sf_off + t * 512));
+              for (int t = 0; t < nA; ++t) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                mma_bf16(acc + t * bmN, da + ((t * kSubTileBytes + k * 32) >> 4), db + ((k * 32) >> 4), idesc,
-                         ((kb - kb0) | k) != 0);
+                for (int k = 0; k < 4; ++k)
+                  mma_mxf8(acc + t * bmN, da + ((t * kSubTileBytes + k * 32) >> 4), db + ((k * 32) >> 4),
+                           idesc_mxf8(128, bmN, k), ((kb - kb0) | k) != 0,
+                           (uint32_t(k) << 30) | (u_tmem + kSfCol + 4 * t), (uint32_t(k) << 30) | (u_tmem + kSfCol + 4 * nA));
+              }
+            } else {
+              for (int t = 0; t < nA; ++t) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  mma_bf16(acc + t * bmN, da + ((t * kSubTileBytes + k * 32) >> 4), db + ((k * 32) >> 4), idesc,
+                           ((kb - kb0) | k) != 0);
+              }
             }
           }
           __syncwarp();
@@ -575,9 +680,19 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           const uint64_t da = sw128_kmajor_desc(sb);
           const uint64_t db = sw128_kmajor_desc(sb + kSubTileBytes);
           if (elect_one()) {
+            if constexpr (kFp8) {
+              const uint32_t sfs = sb + kSubTileBytes + bmN * 128;
+              tmem_cp_sf(u_tmem + kSfCol, sf_atom_desc(sfs));
+              tmem_cp_sf(u_tmem + kSfCol + 4, sf_atom_desc(sfs + 512));
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_bf16(acc, da + ((k * 32) >> 4), db + ((k * 32) >> 4), idesc, ((kb - kb0) | k) != 0);
+              for (int k = 0; k < 4; ++k)
+                mma_mxf8(acc, da + ((k * 32) >> 4), db + ((k * 32) >> 4), idesc_mxf8(128, bmN, k), ((kb - kb0) | k) != 0,
+                         (uint32_t(k) << 30) | (u_tmem + kSfCol), (uint32_t(k) << 30) | (u_tmem + kSfCol + 4));
+            } else {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_bf16(acc, da + ((k * 32) >> 4), db + ((k * 32) >> 4), idesc, ((kb - kb0) | k) != 0);
+            }
           }
           __syncwarp();
           release();
@@ -632,6 +747,27 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         // ---- phase 2: SwiGLU -> bf16 act (fused: SW128 K-major smem tile that
         // phase 3 reads; split: L2-resident global rows read by phase-3 jobs)
         auto store_act = [&](int f, int j0, const float (&g)[16], const float (&u)[16]) {
+          if constexpr (kFp8) {
+            // MXFP8 act for the FP8 phase-3 MMA: the warp's 32 lanes hold 32
+            // consecutive features = one scale group per token
+            const int col = jb.s * G.n_i + f;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const float a = silu_mul(g[q], u[q]);
+              float amax = fabsf(a);
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+              const int ex = amax > 0.f ? max(-127, min(127, (int)ceilf(log2f(amax / 448.0f)))) : -127;
+              const int jj = j0 + q;
+              if (jj < G.bm) {
+                p.act_q[static_cast<int64_t>(row0 + jj) * p.I + col] = e4m3_from_float(a * exp2f(static_cast<float>(-ex)));
+                if ((et & 31) == 0)
+                  p.act_sf[(static_cast<int64_t>(jb.m) * G.kbI + (col >> 7)) * 512 + (jj & 31) * 16 + (jj >> 5) * 4 +
+                           ((col >> 5) & 3)] = static_cast<uint8_t>(ex + 127);
+              }
+            }
+            return;
+          }
           if (G.mode == kModeFused) {
             unsigned char* kblk = act_ptr + (f >> 6) * bmN * 128;
             const int chunk = (f & 63) >> 3, within = (f & 7) * 2;

@@ -9,6 +9,7 @@
 namespace ramp {
 
 constexpr int kMaxBm = 128;  // largest token block the megakernel supports
+inline int bm_mma_host(int bm) { return bm <= 16 ? 16 : (bm + 15) / 16 * 16; }
 
 struct RouteArgs {
   const int32_t* topk_ids;
@@ -56,6 +57,13 @@ struct MoeLaunch {
   int* job_counter; // dynamic scheduler claim counter (zeroed by the route kernel)
   float* acc_a;     // [rows, 2I] split-K partial sums
   int* split_cnt;   // [rows] split-K arrival counters
+  bool fp8;         // MXFP8 path: w1/w2 are e4m3 with tiled UE8M0 scale atoms
+  const uint8_t* w1_sf;
+  const uint8_t* w2_sf;
+  void* x_q;        // [rows, H] e4m3
+  uint8_t* x_sf;    // [M-tiles][H/128][512]
+  void* act_q;      // [rows, I] e4m3
+  uint8_t* act_sf;  // [M-tiles][I/128][512]
   int64_t rows;     // capacity of x_sorted / act_g
   ramp_table_t table;
   int32_t S, H, I, E, top_k;
@@ -63,7 +71,7 @@ struct MoeLaunch {
 
 extern unsigned long long* g_prof_buffer;  // diagnostics, see ramp_set_profile_buffer
 
-cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const char** why);
-int64_t config_smem_bytes(int bm, int ttn, int stg, int mode);
+cudaError_t launch_fused_moe(const MoeLaunch& l, cudaStream_t stream, const char** why);
+int64_t config_smem_bytes(int bm, int ttn, int stg, int mode, bool fp8);
 
 }  // namespace ramp

@@ -31,10 +31,10 @@ static EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-// bf16 tensor map with a 128-byte swizzle; dims/strides innermost first
-// (strides in bytes for dims 1..rank-1).
+// Tensor map with a 128-byte swizzle; dims/strides innermost first (strides
+// in bytes for dims 1..rank-1); element type bf16 or raw bytes (e4m3).
 static bool make_map(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides,
-                     const uint32_t* box) {
+                     const uint32_t* box, bool bytes = false) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t d[3], st[2];
@@ -44,25 +44,27 @@ static bool make_map(CUtensorMap* map, const void* ptr, int rank, const uint64_t
     b[i] = box[i];
   }
   for (int i = 0; i < rank - 1; ++i) st[i] = strides[i];
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), d, st, b, e,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(map, bytes ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
+                   const_cast<void*>(ptr), d, st, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
-// Row-major [rows, cols] bf16 matrix, (box_rows x 64) boxes.
-static bool make_map_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+// Row-major [rows, cols] matrix, (box_rows x 128-byte) boxes.
+static bool make_map_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                        bool bytes = false) {
+  const uint64_t esz = bytes ? 1 : 2;
   const uint64_t dims[2] = {cols, rows};
-  const uint64_t strides[1] = {cols * 2};
-  const uint32_t box[2] = {64, box_rows};
-  return make_map(map, ptr, 2, dims, strides, box);
+  const uint64_t strides[1] = {cols * esz};
+  const uint32_t box[2] = {static_cast<uint32_t>(128 / esz), box_rows};
+  return make_map(map, ptr, 2, dims, strides, box, bytes);
 }
 
-int64_t config_smem_bytes(int bm, int ttn, int stg, int mode) {
+int64_t config_smem_bytes(int bm, int ttn, int stg, int mode, bool fp8) {
   if (bm < 1 || bm > kMaxBm || (ttn != 128 && ttn != 256 && ttn != 512) || stg < 1 || stg > kMaxStages)
     return 0;
   if (mode != kModeFused && mode != kModeSplit) return 0;
-  const int b = moe_smem_bytes(bm, ttn, stg, mode);
+  const int b = moe_smem_bytes(bm, ttn, stg, mode, fp8);
   return b <= kSmemLimit ? b : 0;
 }
 
@@ -77,49 +79,9 @@ static int sm_count_cached() {
   return n;
 }
 
-cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const char** why) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t err =
-        cudaFuncSetAttribute(fused_moe_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
-    if (err != cudaSuccess) return err;
-    err = cudaFuncSetAttribute(fused_moe_bf16_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (err != cudaSuccess) return err;
-    attr_set = true;
-  }
-  // Tensor maps depend only on pointers and shapes: encode once per
-  // (workspace, weights, shape) and reuse (the encoder costs ~1 us per map).
-  struct MapKey {
-    const void *xs, *act, *w1, *w2, *x;
-    int64_t rows;
-    int32_t S, H, I, E;
-    bool operator==(const MapKey& o) const {
-      return xs == o.xs && act == o.act && w1 == o.w1 && w2 == o.w2 && x == o.x && rows == o.rows && S == o.S &&
-             H == o.H && I == o.I && E == o.E;
-    }
-  };
-  struct MapEntry {
-    MapKey key;
-    alignas(64) MoeMaps maps;
-    bool used;
-  };
-  static MapEntry cache[16];
-  static int cache_next = 0;
-  static std::mutex cache_mu;
-  const MapKey key{l.x_sorted, l.act_g, l.w1, l.w2, l.x, l.rows, l.S, l.H, l.I, l.E};
-  alignas(64) MoeMaps maps;  // copied into the launch's parameter buffer
-  bool hit = false;
-  {
-    std::lock_guard<std::mutex> g(cache_mu);
-    for (auto& c : cache)
-      if (c.used && c.key == key) {
-        maps = c.maps;
-        hit = true;
-        break;
-      }
-  }
-  if (!hit) {
-    bool ok = true;
+static bool build_maps(const MoeLaunch& l, MoeMaps& maps) {
+  bool ok = true;
+  if (!l.fp8) {
     for (int i = 0; i < 4; ++i) {
       ok = ok && make_map_2d(&maps.xs[i], l.x_sorted, l.rows, l.H, 16u << i);
       ok = ok && make_map_2d(&maps.act[i], l.act_g, l.rows, l.I, 16u << i);
@@ -133,7 +95,72 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
     }
     ok = ok && make_map_2d(&maps.w2, l.w2, (uint64_t)l.E * l.H, l.I, 128);
     ok = ok && make_map_2d(&maps.x, l.x, (uint64_t)l.S, l.H, 1);
-    if (!ok) {
+  } else {
+    for (int i = 0; i < 4; ++i) {
+      ok = ok && make_map_2d(&maps.xq[i], l.x_q, l.rows, l.H, 16u << i, true);
+      ok = ok && make_map_2d(&maps.actq[i], l.act_q, l.rows, l.I, 16u << i, true);
+    }
+    for (int i = 0; i < 2; ++i) {
+      const uint64_t dims[3] = {(uint64_t)l.H, (uint64_t)l.I, 2ull * l.E};
+      const uint64_t strides[2] = {(uint64_t)l.H, (uint64_t)l.I * l.H};
+      const uint32_t box[3] = {128, 128u << i, 2};
+      ok = ok && ((l.I % (128 << i)) != 0 || make_map(&maps.w1q[i], l.w1, 3, dims, strides, box, true));
+    }
+    ok = ok && make_map_2d(&maps.w2q, l.w2, (uint64_t)l.E * l.H, l.I, 128, true);
+  }
+  return ok;
+}
+
+template <bool kFp8>
+static cudaError_t set_attrs() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  cudaError_t err =
+      cudaFuncSetAttribute(fused_moe_kernel<kFp8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+  if (err != cudaSuccess) return err;
+  err = cudaFuncSetAttribute(fused_moe_kernel<kFp8>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (err == cudaSuccess) done = true;
+  return err;
+}
+
+cudaError_t launch_fused_moe(const MoeLaunch& l, cudaStream_t stream, const char** why) {
+  cudaError_t err = l.fp8 ? set_attrs<true>() : set_attrs<false>();
+  if (err != cudaSuccess) return err;
+  // Tensor maps depend only on pointers and shapes: encode once per
+  // (workspace, weights, shape) and reuse (the encoder costs ~1 us per map).
+  struct MapKey {
+    const void *xs, *act, *w1, *w2, *x;
+    int64_t rows;
+    int32_t S, H, I, E;
+    bool fp8;
+    bool operator==(const MapKey& o) const {
+      return xs == o.xs && act == o.act && w1 == o.w1 && w2 == o.w2 && x == o.x && rows == o.rows && S == o.S &&
+             H == o.H && I == o.I && E == o.E && fp8 == o.fp8;
+    }
+  };
+  struct MapEntry {
+    MapKey key;
+    alignas(64) MoeMaps maps;
+    bool used;
+  };
+  static MapEntry cache[16];
+  static int cache_next = 0;
+  static std::mutex cache_mu;
+  const MapKey key{l.fp8 ? l.x_q : l.x_sorted, l.fp8 ? l.act_q : l.act_g, l.w1, l.w2, l.x, l.rows, l.S, l.H, l.I,
+                   l.E, l.fp8};
+  alignas(64) MoeMaps maps;  // copied into the launch's parameter buffer
+  bool hit = false;
+  {
+    std::lock_guard<std::mutex> g(cache_mu);
+    for (auto& c : cache)
+      if (c.used && c.key == key) {
+        maps = c.maps;
+        hit = true;
+        break;
+      }
+  }
+  if (!hit) {
+    if (!build_maps(l, maps)) {
       *why = "cuTensorMapEncodeTiled failed (alignment or driver entry point)";
       return cudaErrorInvalidValue;
     }
@@ -144,7 +171,7 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
     c.maps = maps;
     c.used = true;
   }
-  MoeParams p;
+  MoeParams p{};
   p.ctrl = l.ctrl;
   p.sorted_ids = l.sorted_ids;
   p.tile_expert = l.tile_expert;
@@ -159,6 +186,12 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
   p.x = static_cast<const __nv_bfloat16*>(l.x);
   p.x_sorted = static_cast<__nv_bfloat16*>(l.x_sorted);
   p.out = static_cast<__nv_bfloat16*>(l.out);
+  p.w1_sf = l.w1_sf;
+  p.w2_sf = l.w2_sf;
+  p.x_q = static_cast<uint8_t*>(l.x_q);
+  p.x_sf = l.x_sf;
+  p.act_q = static_cast<uint8_t*>(l.act_q);
+  p.act_sf = l.act_sf;
   p.table = l.table;
   p.S = l.S;
   p.H = l.H;
@@ -168,8 +201,7 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
   p.n_assign = l.S * l.top_k;
   p.prof = g_prof_buffer;
   // Programmatic dependent launch: the megakernel's prologue (barrier init,
-  // TMEM allocation, descriptor prefetch) overlaps the route kernel's tail,
-  // and the finalize kernel's launch overlaps the megakernel's tail.
+  // TMEM allocation, descriptor prefetch) may overlap the route kernel's tail.
   cudaLaunchAttribute pdl[1];
   pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   pdl[0].val.programmaticStreamSerializationAllowed = 1;
@@ -180,7 +212,8 @@ cudaError_t launch_fused_moe_bf16(const MoeLaunch& l, cudaStream_t stream, const
   cfg.stream = stream;
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
-  cudaError_t err = cudaLaunchKernelEx(&cfg, fused_moe_bf16_kernel, maps, p);
+  err = l.fp8 ? cudaLaunchKernelEx(&cfg, fused_moe_kernel<true>, maps, p)
+              : cudaLaunchKernelEx(&cfg, fused_moe_kernel<false>, maps, p);
   if (err != cudaSuccess) return err;
   return cudaGetLastError();
 }
