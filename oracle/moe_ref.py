@@ -78,3 +78,34 @@ def bf16_round(a: np.ndarray) -> np.ndarray:
     u = np.asarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
     r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
     return r.astype(np.uint32).view(np.float32)
+
+
+def e4m3_round(a: np.ndarray) -> np.ndarray:
+    """Round fp32 to the nearest OCP E4M3 value (ties to even, saturating at
+    +-448, subnormal step 2^-9), returned as fp32 -- cvt.rn.satfinite.e4m3x2."""
+    a = np.asarray(a, dtype=np.float32)
+    m = np.minimum(np.abs(a), np.float32(448.0)).astype(np.float64)
+    e = np.floor(np.log2(np.where(m > 0, m, 1.0)))
+    step = np.exp2(np.maximum(e, -6.0) - 3.0)
+    q = np.minimum(np.round(m / step) * step, 448.0)
+    return (np.sign(a) * q).astype(np.float32)
+
+
+def mx_fake_quant(v: np.ndarray, group: int = 32) -> np.ndarray:
+    """MXFP8 quantise-dequantise along the last axis: one power-of-two scale
+    2^ceil(log2(amax / 448)) per `group` elements (clamped to UE8M0's
+    [-127, 127]), elements rounded to E4M3.  The megakernel applies exactly
+    this to every gathered token row and every SwiGLU activation row."""
+    v = np.asarray(v, dtype=np.float32)
+    g = v.reshape(*v.shape[:-1], v.shape[-1] // group, group)
+    amax = np.abs(g).max(axis=-1, keepdims=True)
+    with np.errstate(divide="ignore"):
+        ex = np.where(amax > 0, np.ceil(np.log2(amax.astype(np.float64) / 448.0)), -127.0)
+    ex = np.clip(ex, -127, 127)
+    return (e4m3_round(g * np.exp2(-ex)) * np.exp2(ex)).astype(np.float32).reshape(v.shape)
+
+
+def fused_moe_ref_fp8(x, w1, w2, topk_w, topk_ids) -> np.ndarray:
+    """W8A8 MXFP8 layer semantics on already-dequantised expert weights:
+    tokens and activations go through mx_fake_quant, all math in fp32."""
+    return fused_moe_ref(mx_fake_quant(x), w1, w2, topk_w, topk_ids, act_dtype=mx_fake_quant)

@@ -96,6 +96,17 @@ class DeviceTable:
     def ref(self):
         return ctypes.byref(self.struct)
 
+    def fp8_compatible(self) -> bool:
+        """Every config runnable by the FP8 megakernel (split mode, no split-K,
+        bm >= 16, ttn >= 256, ramp_config_smem_bytes_fp8 > 0)."""
+        ok = getattr(self, "_fp8_ok", None)
+        if ok is not None:
+            return ok
+        lib = _lib.load()
+        self._fp8_ok = all(int(m) == 1 and int(sk) == 1 and lib.ramp_config_smem_bytes_fp8(int(bm), int(t), int(st)) > 0
+                           for bm, t, st, sk, m in zip(self.bm, self.ttn, self.stg, self.split_k, self.mode))
+        return self._fp8_ok
+
 
 def workspace_bytes(S: int, H: int, I: int, E: int, top_k: int) -> int:
     return int(_lib.load().ramp_fused_moe_workspace_size(S, H, I, E, top_k))
@@ -167,6 +178,65 @@ def fused_moe(
             hidden_states.data_ptr(), w1.data_ptr(), w2.data_ptr(), topk_weights.data_ptr(),
             topk_ids.data_ptr(), S, H, I, E, k, table.ref, int(forced_cfg), out.data_ptr(),
             workspace.sel.data_ptr(), workspace.buf.data_ptr(), workspace.buf.numel(), int(phases), _stream(),
+        )
+    )
+    return out
+
+
+def fused_moe_fp8(
+    hidden_states: torch.Tensor,
+    weights,
+    topk_weights: torch.Tensor,
+    topk_ids: torch.Tensor,
+    table: DeviceTable,
+    forced_cfg: int = -1,
+    out: torch.Tensor | None = None,
+    workspace: Workspace | None = None,
+    phases: int = 3,
+) -> torch.Tensor:
+    """Fused MoE layer forward, block-scaled FP8 (W8A8 MXFP8).
+
+    `weights` is a quant.MxFp8Weights (E4M3 experts + UE8M0 scale atoms, from
+    prepare_mxfp8_weights or prepare_block128_weights).  hidden_states stay
+    bf16 [S, H]; the megakernel quantises each gathered token row (one scale
+    per 32 features) and the SwiGLU activation the same way, multiplies with
+    kind::mxf8f6f4.block_scale MMAs and accumulates in fp32; the output is
+    bf16.  The table must be an FP8 pool (enumerate_b200_configs(...,
+    dtype="fp8")); `forced_cfg` / `phases` as in `fused_moe`.
+    """
+    lib = _lib.load()
+    S, H = hidden_states.shape
+    E, H1, I = weights.shape
+    k = topk_ids.shape[1]
+    if H1 != H:
+        raise ValueError(f"shape mismatch: x {tuple(hidden_states.shape)}, experts d_model {H1}")
+    for name, t, dt in (("hidden_states", hidden_states, torch.bfloat16),
+                        ("w1_q", weights.w1_q, torch.float8_e4m3fn), ("w2_q", weights.w2_q, torch.float8_e4m3fn),
+                        ("w1_sf", weights.w1_sf, torch.uint8), ("w2_sf", weights.w2_sf, torch.uint8),
+                        ("topk_weights", topk_weights, torch.float32), ("topk_ids", topk_ids, torch.int32)):
+        if t.dtype != dt:
+            raise ValueError(f"{name} must be {dt}, got {t.dtype}")
+        if not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+    if tuple(weights.w1_sf.shape) != (E * 2 * I // 128, H // 128, 512) or \
+            tuple(weights.w2_sf.shape) != (E * H // 128, I // 128, 512):
+        raise ValueError("scale atoms must be tiled [rows/128, K/128, 512] (quant.tile_scales)")
+    if tuple(topk_weights.shape) != (S, k):
+        raise ValueError("topk_weights must be [S, top_k]")
+    if not table.fp8_compatible():
+        raise ValueError("table holds configs the FP8 megakernel cannot run (use an FP8 pool)")
+    if out is None:
+        out = torch.empty(S, H, dtype=torch.bfloat16, device=hidden_states.device)
+    if workspace is None or not workspace.fits(S, H, I, E, k):
+        workspace = Workspace(S, H, I, E, k, device=hidden_states.device)
+    _lib.check(
+        lib.ramp_fused_moe_fp8(
+            hidden_states.data_ptr(), weights.w1_q.data_ptr(), weights.w1_sf.data_ptr(), weights.w2_q.data_ptr(),
+            weights.w2_sf.data_ptr(), topk_weights.data_ptr(), topk_ids.data_ptr(), S, H, I, E, k, table.ref,
+            int(forced_cfg), out.data_ptr(), workspace.sel.data_ptr(), workspace.buf.data_ptr(),
+            workspace.buf.numel(), int(phases), _stream(),
         )
     )
     return out

@@ -19,6 +19,8 @@ byte (r % 32) * 16 + (r // 32) * 4 + kg holds the scale of row r, K group kg
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import torch
 
 E4M3_MAX = 448.0
@@ -68,3 +70,71 @@ def tile_scales(sf: torch.Tensor) -> torch.Tensor:
     x = sf.reshape(*lead, R // 128, 4, 32, G // 4, 4)          # [.., rb, r1, r0, kb, kg]
     x = x.permute(*range(len(lead)), len(lead), len(lead) + 3, len(lead) + 2, len(lead) + 1, len(lead) + 4)
     return x.reshape(*lead, R // 128, G // 4, 512).contiguous()  # byte r0*16 + r1*4 + kg
+
+
+def untile_scales(tiled: torch.Tensor) -> torch.Tensor:
+    """Inverse of `tile_scales`: [..., R/128, K/128, 512] -> [..., R, K/32]."""
+    *lead, RB, KB, _ = tiled.shape
+    x = tiled.reshape(*lead, RB, KB, 32, 4, 4)                  # [.., rb, kb, r0, r1, kg]
+    n = len(lead)
+    x = x.permute(*range(n), n, n + 3, n + 2, n + 1, n + 4)     # [.., rb, r1, r0, kb, kg]
+    return x.reshape(*lead, RB * 128, KB * 4).contiguous()
+
+
+@dataclass
+class MxFp8Weights:
+    """Expert weights in the FP8 megakernel's operand format.
+
+    w1_q [E, 2I, H] / w2_q [E, H, I] float8_e4m3fn, and their UE8M0 scales as
+    canonical 512-byte atoms: w1_sf [E*2I/128, H/128, 512], w2_sf
+    [E*H/128, I/128, 512] (rows of all experts flattened, so the kernel
+    indexes a row block as (expert*rows + row) / 128)."""
+
+    w1_q: torch.Tensor
+    w1_sf: torch.Tensor
+    w2_q: torch.Tensor
+    w2_sf: torch.Tensor
+
+    @property
+    def shape(self):
+        E, two_i, H = self.w1_q.shape
+        return E, H, two_i // 2
+
+    def to(self, device) -> "MxFp8Weights":
+        return MxFp8Weights(*(t.to(device) for t in (self.w1_q, self.w1_sf, self.w2_q, self.w2_sf)))
+
+    def dequantize(self):
+        """fp32 (w1, w2) the FP8 MMAs multiply by -- the oracle's weights."""
+        E, H, I = self.shape
+        s1 = untile_scales(self.w1_sf).reshape(E, 2 * I, H // GROUP)
+        s2 = untile_scales(self.w2_sf).reshape(E, H, I // GROUP)
+        return mx_dequantize(self.w1_q, s1), mx_dequantize(self.w2_q, s2)
+
+
+def _pack(w1_q, s1, w2_q, s2) -> MxFp8Weights:
+    E, two_i, H = w1_q.shape
+    I = two_i // 2
+    return MxFp8Weights(w1_q.contiguous(), tile_scales(s1.reshape(E * two_i, H // GROUP)),
+                        w2_q.contiguous(), tile_scales(s2.reshape(E * H, I // GROUP)))
+
+
+def prepare_mxfp8_weights(w1: torch.Tensor, w2: torch.Tensor) -> MxFp8Weights:
+    """bf16 / fp32 expert weights (vLLM layout) -> MXFP8 operands."""
+    q1, s1 = mx_quantize(w1)
+    q2, s2 = mx_quantize(w2)
+    return _pack(q1, s1, q2, s2)
+
+
+def prepare_block128_weights(w1_q, w1_scale, w2_q, w2_scale) -> MxFp8Weights:
+    """A DeepSeek-style checkpoint (E4M3 + one fp32 scale per 128x128 block)
+    -> MXFP8 operands, once at load time."""
+    q1, s1 = requantize_block128(w1_q, w1_scale)
+    q2, s2 = requantize_block128(w2_q, w2_scale)
+    return _pack(q1, s1, q2, s2)
+
+
+def quantize_tokens_ref(x: torch.Tensor) -> torch.Tensor:
+    """What the megakernel's phase-0 gather does to every token row (per-token,
+    per-32 UE8M0 + E4M3), returned dequantised; for tests."""
+    q, s = mx_quantize(x)
+    return mx_dequantize(q, s)
