@@ -63,9 +63,15 @@ typedef struct ramp_table {
    * ntile[i]   work tiles per M-tile of config i, replacing ceil(N/ttn) in
    *            g = M-tiles * ntile * split_k -- the B200 megakernel's split
    *            mode runs I-stripe jobs AND H-chunk jobs per M-tile;
-   * omega_max  split-K gate threshold (reference: 0.2, ramp/dispatch.py:31). */
+   * omega_max  split-K gate threshold (reference: 0.2, ramp/dispatch.py:31);
+   * lam[i]     B200 L2-reuse factor of config i (variant "B4"): the traffic
+   *            terms c*g and d*ln(g+1) see the HBM-equivalent grid
+   *            g_l = ntile*split_k*(n_act + lam*(M-tiles - n_act)), n_act =
+   *            active experts, while the wave term keeps the job grid g.
+   *            null: g_l = g (the reference model). */
   const int32_t* ntile;
   double omega_max;
+  const double* lam;
 } ramp_table_t;
 
 /* Library version (major*10000 + minor*100 + patch) and sm_100a build flag. */

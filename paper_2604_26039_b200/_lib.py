@@ -75,6 +75,7 @@ class RampTable(ctypes.Structure):
         ("d", ctypes.c_void_p),
         ("ntile", ctypes.c_void_p),
         ("omega_max", ctypes.c_double),
+        ("lam", ctypes.c_void_p),
     ]
 
 

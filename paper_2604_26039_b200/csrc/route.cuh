@@ -146,7 +146,17 @@ __device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_tabl
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) mt_smem[u] = acc;
   }
+  // Active experts (only the B4 traffic grid needs them).
+  __shared__ int s_nact;
+  if (t.lam && warp == nwarps - 1) {
+    int na = 0;
+    for (int e = lane; e < E; e += 32) na += hist[e] > 0 ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) na += __shfl_xor_sync(0xffffffffu, na, o);
+    if (lane == 0) s_nact = na;
+  }
   __syncthreads();
+  const double nact = t.lam ? static_cast<double>(s_nact) : 0.0;
 
   const double sm = static_cast<double>(t.sm_count);
   const double omega_max = t.omega_max > 0.0 ? t.omega_max : 0.2;
@@ -159,9 +169,17 @@ __device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_tabl
     const double gd = static_cast<double>(g);
     bool keep = true;
     if (sk > 1) keep = t.kappa_ok && (__ddiv_rn(__ddiv_rn(gd, static_cast<double>(sk)), sm) < omega_max);
+    // B4: HBM-equivalent traffic grid (first M-tile of an expert streams its
+    // weights from HBM, later ones re-read them at lam x the cost from L2)
+    double gl = gd;
+    if (t.lam) {
+      const double mt = static_cast<double>(mt_smem[t.ubm_index[i]]);
+      const double u = __dadd_rn(nact, __dmul_rn(t.lam[i], __dadd_rn(mt, -nact)));
+      gl = __dmul_rn(static_cast<double>(stripes * sk), u);
+    }
     double p = __dadd_rn(t.a[i], __dmul_rn(t.b[i], ceil(__ddiv_rn(gd, sm))));
-    p = __dadd_rn(p, __dmul_rn(t.c[i], gd));
-    p = __dadd_rn(p, __dmul_rn(t.d[i], log(__dadd_rn(gd, 1.0))));
+    p = __dadd_rn(p, __dmul_rn(t.c[i], gl));
+    p = __dadd_rn(p, __dmul_rn(t.d[i], log(__dadd_rn(gl, 1.0))));
     if (grid_out) grid_out[i] = g;
     if (!keep) p = CUDART_INF;
     if (pred_out) pred_out[i] = p;

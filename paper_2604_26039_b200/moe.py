@@ -49,6 +49,7 @@ class DeviceTable:
     device: torch.device | str = "cuda"
     ntile: np.ndarray | None = None   # work tiles per M-tile (default ceil(N/ttn))
     omega_max: float = 0.0            # split-K gate threshold (<= 0: the reference's 0.2)
+    lam: np.ndarray | None = None     # B4 L2-reuse factor per config (None: the reference model)
     _tensors: dict = field(default_factory=dict, repr=False)
     struct: _lib.RampTable | None = field(default=None, repr=False)
 
@@ -87,6 +88,11 @@ class DeviceTable:
             setattr(s, name, t[name].data_ptr())
         s.ntile = t["ntile"].data_ptr() if "ntile" in t else None
         s.omega_max = float(self.omega_max)
+        if self.lam is not None:
+            if len(self.lam) != n:
+                raise ValueError("lam must have one entry per config")
+            t["lam"] = torch.as_tensor(np.asarray(self.lam, dtype=np.float64), **f64)
+        s.lam = t["lam"].data_ptr() if "lam" in t else None
         self.struct = s
 
     def __len__(self) -> int:

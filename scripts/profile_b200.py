@@ -9,8 +9,10 @@ pool is launched and timed (sweep.MeasuredTimer), the samples are written in
 ramp's trace CSV schema (loadable by ramp.load_trace), and each config's four
 coefficients are fitted with the reference's OLS (cost_model.fit).  The model
 variant (P2 / P3 / P4, the reference's ablation ladder) is chosen by held-out
-dispatch regret on the sweep itself (choose_variant): on the persistent,
-dynamically scheduled megakernel the wave staircase is weak and P2 wins.
+dispatch regret on the sweep itself (choose_variant), together with the B200
+variant B4 (cost_model.py: waves on the job grid, traffic terms on the
+HBM-equivalent grid with a fitted per-config L2-reuse factor).
+`--refit` skips the GPU sweep and refits from an existing trace.
 Outputs (under paper_2604_26039_b200/data/ unless --out is given):
     trace_<model>_b200.csv, coeffs_<model>_b200.json, fit_<model>_b200.json
 Then it evaluates the fitted table against an exhaustive on-GPU sweep over the
@@ -33,38 +35,60 @@ sys.path.insert(0, str(ROOT))
 
 from paper_2604_26039_b200.catalog import BASELINE_MODELS  # noqa: E402
 from paper_2604_26039_b200.config_space import HardwareModel, enumerate_b200_configs  # noqa: E402
-from paper_2604_26039_b200.cost_model import coeff_store_dict, fit, profiling_plan, write_coeff_store  # noqa: E402
+from paper_2604_26039_b200.cost_model import (b4_features, coeff_store_dict, fit, fit_b4, profiling_plan,  # noqa: E402
+                                              write_coeff_store)
+from paper_2604_26039_b200.routing import sample_histogram  # noqa: E402
 from paper_2604_26039_b200.dispatch import DispatchTable, evaluate_regret, speedup_ra_vs_static  # noqa: E402
 from paper_2604_26039_b200.moe import DeviceTable  # noqa: E402
 from paper_2604_26039_b200.sweep import MeasuredTimer  # noqa: E402
-from paper_2604_26039_b200.trace import profile  # noqa: E402
+from paper_2604_26039_b200.trace import load_trace, profile  # noqa: E402
 
 
-def choose_variant(pool, trace, hw):
-    """Pick the cost-model variant (P2 / P3 / P4, ramp/cost_model.py:163-196)
-    with the lowest held-out dispatch regret: fit on routing seeds 0-1 of every
-    plan point, select on seed 2, compare with the measured best there."""
-    from paper_2604_26039_b200.cost_model import predict_batch
+def _fit_all(pool, by_cfg, hw, variant, geom):
+    cols = pool.columns()
+    out = {}
+    for cid, ss in by_cfg.items():
+        if variant == "B4":
+            jpm = int(cols["ntile"][cid] * cols["split_k"][cid])
+            out[cid] = fit_b4(ss, b4_features(ss, geom, int(cols["bm"][cid]), jpm), hw)
+        else:
+            out[cid] = fit(ss, hw, variant)
+    return out
 
+
+def choose_variant(pool, trace, hw, geom):
+    """Pick the cost-model variant (the reference's P2 / P3 / P4,
+    ramp/cost_model.py:163-196, or the B200 "B4") with the lowest held-out
+    dispatch regret: for every routing seed of every plan point, fit on the
+    other seeds, select on it with the table's own host predictor, compare
+    with the measured best there; mean over all folds."""
     points: dict = {}
     for s in trace.samples:
         points.setdefault((s.S, s.beta_target), {}).setdefault(s.seed, {})[s.config_id] = s
-    train, test = [], []
-    for _, by_seed in sorted(points.items()):
-        seeds = sorted(by_seed)
-        train += [by_seed[x] for x in seeds[:-1]]
-        test += [by_seed[seeds[-1]]]
+    n_seeds = min(len(v) for v in points.values())
     ids = [c.id for c in pool]
     out = {}
-    for variant in ("P2", "P3", "P4"):
-        co = [fit([pt[c] for pt in train], hw, variant).coefficients for c in ids]
-        a, b, c_, d = (np.array([getattr(x, f) for x in co]) for f in "abcd")
+    for variant in ("P2", "P3", "P4", "B4"):
         regs = []
-        for pt in test:
-            g = np.array([pt[c].g for c in ids])
-            t = np.array([pt[c].time_us for c in ids])
-            sel = int(np.argmin(predict_batch(a, b, c_, d, g, hw.sm_count)))
-            regs.append(t[sel] / t.min() - 1.0)
+        for hold in range(n_seeds):
+            train: dict[int, list] = {c: [] for c in ids}
+            test = []
+            for _, by_seed in sorted(points.items()):
+                seeds = sorted(by_seed)
+                for j, sd in enumerate(seeds):
+                    if j == hold:
+                        test.append(by_seed[sd])
+                    else:
+                        for c in ids:
+                            train[c].append(by_seed[sd][c])
+            reports = _fit_all(pool, train, hw, variant, geom)
+            table = DispatchTable(model="cv", pool=pool, coefficients={c: r.coefficients for c, r in reports.items()},
+                                  sm_count=hw.sm_count)
+            for pt in test:
+                s0 = pt[ids[0]]
+                hist = sample_histogram(geom.E, s0.S, geom.top_k, s0.beta_target, s0.seed).histogram
+                t = np.array([pt[c].time_us for c in ids])
+                regs.append(t[table.host_select(hist)] / t.min() - 1.0)
         out[variant] = float(np.mean(regs))
     return min(out, key=out.get), out
 
@@ -78,6 +102,7 @@ def main() -> None:
     ap.add_argument("--out", default=str(ROOT / "paper_2604_26039_b200" / "data"))
     ap.add_argument("--skip-eval", action="store_true")
     ap.add_argument("--eval-iters", type=int, default=7)
+    ap.add_argument("--refit", action="store_true", help="reuse the existing trace (no profiling sweep)")
     a = ap.parse_args()
     out = Path(a.out)
     out.mkdir(parents=True, exist_ok=True)
@@ -86,24 +111,31 @@ def main() -> None:
     pool = enumerate_b200_configs(geom, hw)
     cols = pool.columns()
     n = len(pool)
-    flat = DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
-                       group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], a=np.ones(n),
-                       b=np.zeros(n), c=np.zeros(n), d=np.zeros(n), N=geom.N, kappa_ok=False,
-                       sm_count=hw.sm_count)
-    timer = MeasuredTimer(geom, flat, iters=a.iters)
     plan = profiling_plan(geom)
     tag = f"{a.model}_b200"
     trace_path = out / f"trace_{tag}.csv"
-    if trace_path.exists():
-        trace_path.unlink()
     t0 = time.time()
-    trace = profile(pool, geom, plan, timer, seeds_per_point=a.plan_reps, trace_path=trace_path)
+    def make_timer():
+        flat = DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
+                           group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], a=np.ones(n),
+                           b=np.zeros(n), c=np.zeros(n), d=np.zeros(n), N=geom.N, kappa_ok=False,
+                           sm_count=hw.sm_count)
+        return MeasuredTimer(geom, flat, iters=a.iters)
+
+    timer = None
+    if a.refit:
+        trace = load_trace(trace_path, pool)
+    else:
+        timer = make_timer()
+        if trace_path.exists():
+            trace_path.unlink()
+        trace = profile(pool, geom, plan, timer, seeds_per_point=a.plan_reps, trace_path=trace_path)
     t_prof = time.time() - t0
     by_cfg: dict[int, list] = {}
     for s in trace.samples:
         by_cfg.setdefault(s.config_id, []).append(s)
-    variant, validation = choose_variant(pool, trace, hw)
-    reports = {cid: fit(ss, hw, variant) for cid, ss in by_cfg.items()}
+    variant, validation = choose_variant(pool, trace, hw, geom)
+    reports = _fit_all(pool, by_cfg, hw, variant, geom)
     write_coeff_store(out / f"coeffs_{tag}.json", coeff_store_dict(a.model, hw.sm_count, reports))
     r2 = np.array([r.r_squared for r in reports.values()])
     summary = {"model": a.model, "pool": n, "plan_points": len(plan), "samples": len(trace.samples),
@@ -115,6 +147,7 @@ def main() -> None:
                               coefficients={c: r.coefficients for c, r in reports.items()},
                               sm_count=hw.sm_count)
         t0 = time.time()
+        timer = timer or make_timer()
         timer.iters = a.eval_iters
         reg = evaluate_regret(table, pool, geom, timer, seeds_per_point=a.eval_reps)
         spd = speedup_ra_vs_static(table, pool, geom, timer, seeds_per_point=a.eval_reps)

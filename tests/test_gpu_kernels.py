@@ -346,3 +346,24 @@ def test_fused_moe_fp8_block128_checkpoint():
     q2, s2 = block128_quantize(torch.from_numpy(w2).cuda())
     weights = prepare_block128_weights(q1, s1, q2, s2)
     _fp8_case(x, None, None, w, ids, table, [-1, pool.configs[0].id, pool.configs[-1].id], weights=weights)
+
+
+def test_b4_device_dispatch_matches_oracle():
+    """B4 tables (per-config L2-reuse factor): device selection and
+    evaluation count equal the oracle's on random histograms."""
+    from oracle import ramp_ref as R
+    from tests.test_host_mirror import _b4_table
+
+    g, pool, co, table = _b4_table(seed=4)
+    M = _M()
+    cols = pool.columns()
+    cfgs = [dict(bm=c.bm, ttn=c.ttn, split_k=c.split_k) for c in pool]
+    coeffs = [[co[i].a, co[i].b, co[i].c, co[i].d] for i in range(len(pool))]
+    lam = [co[i].lam for i in range(len(pool))]
+    rng = np.random.default_rng(8)
+    for _ in range(200):
+        counts = rng.multinomial(int(rng.integers(1, 4096)), rng.dirichlet(np.full(64, 0.3))).astype(np.int32)
+        cfg, n_eval, _, _ = M.dispatch_select(torch.from_numpy(counts).cuda(), table.device_table())
+        want = R.select(cfgs, coeffs, counts.tolist(), g.N, 148, True, ntile=cols["ntile"].tolist(),
+                        omega_max=float("inf"), lam=lam)
+        assert (int(cfg.item()), int(n_eval.item())) == want

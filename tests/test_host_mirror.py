@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import hashlib
 import json
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -205,3 +206,89 @@ def test_b200_pool_is_kernel_admissible():
             assert CS.b200_smem_bytes(c.bm, c.ttn, c.stg, c.mode) <= CS.B200_SMEM_LIMIT
             assert (g.N // 2) % (c.ttn // 2) == 0
         assert [c.id for c in pool] == list(range(len(pool)))
+
+
+# ------------------------------------------------------------- B4 variant
+def _b4_table(seed=0):
+    from paper_2604_26039_b200.catalog import BASELINE_MODELS
+    from paper_2604_26039_b200.config_space import enumerate_b200_configs
+    from paper_2604_26039_b200.cost_model import CostCoefficients
+    from paper_2604_26039_b200.dispatch import DispatchTable
+
+    g = BASELINE_MODELS["OLMoE-1B-7B"]
+    pool = enumerate_b200_configs(g)
+    rng = np.random.default_rng(seed)
+    co = {c.id: CostCoefficients(a=float(rng.uniform(10, 40)), b=float(rng.uniform(0, 20)),
+                                 c=float(rng.uniform(0, 0.3)), d=float(rng.uniform(-2, 5)), uses_log=True,
+                                 variant="B4", lam=float(rng.choice(np.linspace(0, 1, 21)))) for c in pool}
+    return g, pool, co, DispatchTable(model="t", pool=pool, coefficients=co, sm_count=148)
+
+
+def test_b4_host_select_matches_oracle():
+    """The host mirror of the B4 dispatcher and the oracle restatement pick
+    the same config on random histograms (the device path is held to the
+    same oracle in test_gpu_kernels)."""
+    from oracle import ramp_ref as R
+    from paper_2604_26039_b200.routing import ExpertHistogram
+
+    g, pool, co, table = _b4_table()
+    cols = pool.columns()
+    cfgs = [dict(bm=c.bm, ttn=c.ttn, split_k=c.split_k) for c in pool]
+    coeffs = [[co[i].a, co[i].b, co[i].c, co[i].d] for i in range(len(pool))]
+    lam = [co[i].lam for i in range(len(pool))]
+    rng = np.random.default_rng(1)
+    for _ in range(60):
+        counts = rng.multinomial(int(rng.integers(1, 4096)), rng.dirichlet(np.full(64, 0.3)))
+        want, _ = R.select(cfgs, coeffs, counts.tolist(), g.N, 148, True, ntile=cols["ntile"].tolist(),
+                           omega_max=float("inf"), lam=lam)
+        assert table.host_select(ExpertHistogram(tuple(int(c) for c in counts))) == want
+
+
+def test_b4_fit_recovers_planted_model():
+    from paper_2604_26039_b200.config_space import HardwareModel
+    from paper_2604_26039_b200.cost_model import B4Features, ProfilingSample, fit_b4, traffic_grid
+
+    hw = HardwareModel.b200()
+    rng = np.random.default_rng(2)
+    n = 60
+    n_act = rng.integers(1, 65, n)
+    mt = n_act + rng.integers(0, 200, n)
+    jpm = 24
+    g = mt * jpm
+    lam = 0.35
+    gl = traffic_grid(jpm, n_act, mt, lam)
+    t = 20.0 + 3.0 * np.ceil(g / 148) + 0.05 * gl + 1.5 * np.log(gl + 1.0)
+    samples = [ProfilingSample(config_id=0, S=8, beta_target=0.5, seed=i, g=int(g[i]), time_us=float(t[i]))
+               for i in range(n)]
+    r = fit_b4(samples, B4Features(g=g, n_act=n_act, m_tiles=mt, jobs_per_mtile=jpm), hw)
+    c = r.coefficients
+    assert c.variant == "B4" and abs(c.lam - lam) < 1e-9
+    assert np.allclose([c.a, c.b, c.c, c.d], [20.0, 3.0, 0.05, 1.5], rtol=1e-6, atol=1e-6)
+    assert r.r_squared > 1 - 1e-9
+
+
+def test_b4_coeff_store_round_trip_and_validation():
+    from paper_2604_26039_b200.cost_model import CostCoefficients, FitReport, coeff_store_dict, parse_coeff_store
+
+    co = CostCoefficients(a=1.0, b=2.0, c=0.1, d=0.5, uses_log=True, variant="B4", lam=0.25)
+    rep = FitReport(coefficients=co, r_squared=0.99, n_samples=10, median_grid=100.0, condition_flag=False)
+    _, _, back = parse_coeff_store(coeff_store_dict("m", 148, {0: rep}))
+    assert back[0] == co
+    with pytest.raises(ValueError):
+        CostCoefficients(a=1.0, b=0.0, c=0.1, d=0.0, uses_log=False, variant="P2", lam=0.5)
+    with pytest.raises(ValueError):
+        CostCoefficients(a=1.0, b=0.0, c=0.1, d=0.0, uses_log=True, variant="B4", lam=1.5)
+
+
+def test_shipped_olmoe_coeffs_load_into_the_table():
+    """The committed coefficient store matches the current B200 pool."""
+    from paper_2604_26039_b200.catalog import BASELINE_MODELS
+    from paper_2604_26039_b200.config_space import enumerate_b200_configs
+    from paper_2604_26039_b200.cost_model import parse_coeff_store, read_coeff_store
+    from paper_2604_26039_b200.dispatch import DispatchTable
+
+    g = BASELINE_MODELS["OLMoE-1B-7B"]
+    pool = enumerate_b200_configs(g)
+    path = Path(__file__).resolve().parents[1] / "paper_2604_26039_b200" / "data" / "coeffs_OLMoE-1B-7B_b200.json"
+    _, sm, co = parse_coeff_store(read_coeff_store(path))
+    DispatchTable(model=g.name, pool=pool, coefficients=co, sm_count=sm)
