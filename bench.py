@@ -74,47 +74,67 @@ def layer_bytes(geom, hist, S):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: an NVML
+    polling thread (2 ms period; the timed region can be only tens of ms,
+    shorter than nvidia-smi's start-up), nvidia-smi as the fallback."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, gpu: int):
-        self.gpu, self.rows, self.proc = gpu, [], None
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [v.strip() for v in vis.split(",") if v.strip()]
+        self.gpu = int(ids[gpu]) if gpu < len(ids) and ids[gpu].isdigit() else gpu
+        self.rows, self.max_mhz, self.stop, self.thread, self.err = [], None, threading.Event(), None, None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            bits = (N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                    N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap)
+
+            def poll():
+                while True:
+                    r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)),
+                                      tuple(n for n, b in zip(self.NAMES, bits) if r & b)))
+                    if self.stop.wait(0.002):
+                        break
+
+            self.thread = threading.Thread(target=poll, daemon=True)
             self.thread.start()
-        except (FileNotFoundError, OSError):
-            self.proc = None
+        except Exception as e:  # no NVML: fall back to one nvidia-smi read after the region
+            self.err = repr(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([f.strip() for f in line.split(",")])
-
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        elif not self.rows:
+            self._smi()
+
+    def _smi(self):
+        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+            "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=20).stdout
+            f = [x.strip() for x in out.strip().split(",")]
+            self.max_mhz = float(f[1])
+            self.rows.append((float(f[0]), tuple(n for n, v in zip(self.NAMES, f[2:]) if v == "Active")))
+        except Exception as e:
+            self.err = (self.err or "") + " / nvidia-smi: " + repr(e)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [f"no clock samples ({self.err})"]}
+        return {"sm_mhz": float(np.median([r[0] for r in self.rows])), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted({n for r in self.rows for n in r[1]}), "samples": len(self.rows),
+                "source": "nvml" if self.thread is not None else "nvidia-smi"}
 
 
 # ------------------------------------------------------------------ CPU oracle
@@ -328,12 +348,14 @@ def ours(args, geom):
     # ---------------- routing-aware vs static and regret against an exhaustive on-GPU sweep
     ra = None
     if not args.no_sweep:
-        timer = MeasuredTimer(geom, dtab, w1=copies[0][0], w2=copies[0][1], iters=3, device=dev)
+        timer = MeasuredTimer(geom, dtab, w1=copies[0][0], w2=copies[0][1], iters=5, device=dev)
         points = [(pt["S"], pt["beta"]) for pt in pts]
         spd = speedup_ra_vs_static(table, pool, geom, timer, points=points, seeds_per_point=1)
         reg = evaluate_regret(table, pool, geom, timer, test_points=points, seeds_per_point=1)
         ra = {"ra_vs_static_geomean": spd.geomean, "per_beta": spd.aggregate()["per_beta_geomean"],
-              "regret_mean_pct": reg.mean * 100, "regret_max_pct": reg.max * 100, "points": len(points)}
+              "regret_mean_pct": reg.mean * 100, "regret_max_pct": reg.max * 100, "points": len(points),
+              "worst": [{"S": r.S, "beta": r.beta, "regret_pct": round(r.regret * 100, 2), "sel": r.selected_id,
+                         "best": r.best_id} for r in sorted(reg.records, key=lambda r: -r.regret)[:4]]}
 
     # ---------------- e2e through the public API with host buffers
     pinned = []

@@ -35,7 +35,7 @@ sys.path.insert(0, str(ROOT))
 
 from paper_2604_26039_b200.catalog import BASELINE_MODELS  # noqa: E402
 from paper_2604_26039_b200.config_space import HardwareModel, enumerate_b200_configs  # noqa: E402
-from paper_2604_26039_b200.cost_model import (b4_features, coeff_store_dict, fit, fit_b4, profiling_plan,  # noqa: E402
+from paper_2604_26039_b200.cost_model import (B200_BATCH_SIZES, b4_features, coeff_store_dict, fit, fit_b4, profiling_plan,  # noqa: E402
                                               write_coeff_store)
 from paper_2604_26039_b200.routing import sample_histogram  # noqa: E402
 from paper_2604_26039_b200.dispatch import DispatchTable, evaluate_regret, speedup_ra_vs_static  # noqa: E402
@@ -111,7 +111,7 @@ def main() -> None:
     pool = enumerate_b200_configs(geom, hw)
     cols = pool.columns()
     n = len(pool)
-    plan = profiling_plan(geom)
+    plan = profiling_plan(geom, batch_sizes=B200_BATCH_SIZES)
     tag = f"{a.model}_b200"
     trace_path = out / f"trace_{tag}.csv"
     t0 = time.time()
