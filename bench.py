@@ -208,6 +208,78 @@ def reference_arm(args, geom):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ FP8 leg
+FP8_MODEL = "Qwen3-30B-A3B"
+FP8_BATCHES = (1, 8, 32, 128, 512, 2048)
+FP8_BETAS = (0.5, 0.55)  # 12 / 15 of 128 experts active: BASELINE configs[2]'s 8-14% skew
+FP8_COPIES = 4
+
+
+def fp8_leg(dev):
+    """BASELINE configs[2]: Qwen3-30B-A3B MoE layer, MXFP8 block-scaled, skewed
+    routing, on-device dispatch over the FP8 pool with its own fitted table.
+    Untimed by the step contract; reported as a side object of the line."""
+    import torch
+
+    from paper_2604_26039_b200 import moe
+    from paper_2604_26039_b200.catalog import BASELINE_MODELS
+    from paper_2604_26039_b200.config_space import HardwareModel, enumerate_b200_configs
+    from paper_2604_26039_b200.cost_model import parse_coeff_store, read_coeff_store
+    from paper_2604_26039_b200.dispatch import EVAL_HIST_DOMAIN, DispatchTable, derive_seed
+    from paper_2604_26039_b200.routing import sample_histogram
+    from paper_2604_26039_b200.sweep import make_fp8_weights, make_inputs
+
+    geom = BASELINE_MODELS[FP8_MODEL]
+    path = ROOT / "paper_2604_26039_b200" / "data" / f"coeffs_{FP8_MODEL}_b200_fp8.json"
+    if not path.exists():
+        return {"skipped": f"{path.name} missing (scripts/profile_b200.py --model {FP8_MODEL} --dtype fp8)"}
+    pool = enumerate_b200_configs(geom, HardwareModel.b200(), dtype="fp8")
+    _, sm, co = parse_coeff_store(read_coeff_store(path))
+    dtab = DispatchTable(model=FP8_MODEL, pool=pool, coefficients=co, sm_count=sm).device_table(device=dev)
+    copies = [make_fp8_weights(geom, seed=100 + c, device=dev) for c in range(FP8_COPIES)]
+    H, I, E, k = geom.K, geom.N // 2, geom.E, geom.top_k
+    side = torch.cuda.Stream(device=dev)
+    rows = []
+    for S in FP8_BATCHES:
+        for beta in FP8_BETAS:
+            hs = derive_seed(42, EVAL_HIST_DOMAIN, S, round(beta * 1000), 0)
+            hist = sample_histogram(E, S, k, beta, hs).histogram
+            x, ids, w = make_inputs(geom, hist, hs, dev)
+            ws = moe.Workspace(S, H, I, E, k, device=dev)
+            out = torch.empty(S, H, dtype=torch.bfloat16, device=dev)
+            graphs = []
+            with torch.cuda.stream(side):
+                for c in range(FP8_COPIES):
+                    moe.fused_moe_fp8(x, copies[c], w, ids, dtab, -1, out=out, workspace=ws)
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=side):
+                        moe.fused_moe_fp8(x, copies[c], w, ids, dtab, -1, out=out, workspace=ws)
+                    graphs.append(g)
+            torch.cuda.synchronize()
+            ts = []
+            for r in range(12):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                graphs[r % FP8_COPIES].replay()
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e3)
+            us = float(np.median(ts[FP8_COPIES:]))
+            a = hist.active_experts
+            nbytes = a * 3 * H * I * (1 + 1 / 32) + S * H * 4 + 8 * S * k
+            c = pool.by_id(int(ws.sel[0].item()))
+            rows.append({"S": S, "beta": beta, "active": a, "us": round(us, 2),
+                         "tflops": round(6 * S * k * H * I / us / 1e6, 2), "gbs": round(nbytes / us / 1e3, 1),
+                         "cfg": {"id": c.id, "bm": c.bm, "ttn": c.ttn, "stg": c.stg, "group_m": int(c.group_m)}})
+    del copies
+    torch.cuda.empty_cache()
+    return {"workload": f"{FP8_MODEL} MoE layer (E=128, top-8, d=2048, d_ff=768) MXFP8 W8A8, skewed routing "
+                        f"beta in {FP8_BETAS} (12/15 of 128 experts active), on-device dispatch over the FP8 pool",
+            "dtype": "e4m3 x e4m3 (UE8M0 per 32) -> fp32", "l2": f"{FP8_COPIES} rotating weight copies",
+            "us_geomean": float(np.exp(np.mean([np.log(r["us"]) for r in rows]))), "points": rows,
+            "coeffs": path.name}
+
+
 # ------------------------------------------------------------------ GPU arm
 def load_table(geom, pool, hw):
     from paper_2604_26039_b200.cost_model import parse_coeff_store, read_coeff_store
@@ -396,6 +468,8 @@ def ours(args, geom):
         cpu = {"value": f / t / 1e12, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
                "sample": f"first {n} of {len(pts)} sweep points (fp32 numpy oracle, oracle/moe_ref.py)"}
 
+    fp8 = None if args.no_fp8 else fp8_leg(dev)
+
     peaks = {}
     pk_path = ROOT / "MEASURED_PEAKS.json"
     if pk_path.exists():
@@ -425,6 +499,7 @@ def ours(args, geom):
         "cpu_baseline": cpu,
         "dispatch": ra,
         "per_point": per_point,
+        "fp8": fp8,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -439,6 +514,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-sweep", action="store_true", help="skip the exhaustive RA/static/regret sweep")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    ap.add_argument("--no-fp8", action="store_true", help="skip the Qwen3 FP8 side measurement")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

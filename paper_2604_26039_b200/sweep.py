@@ -22,7 +22,7 @@ import torch
 from .catalog import MoeGeometry
 from .config_space import ConfigPool
 from .dispatch import derive_seed
-from .moe import DeviceTable, Workspace, fused_moe
+from .moe import DeviceTable, Workspace, fused_moe, fused_moe_fp8
 from .routing import ExpertHistogram, topk_from_histogram
 
 TOPK_DOMAIN = 6      # seed domains for the concrete inputs of a histogram
@@ -41,6 +41,16 @@ def make_weights(geom: MoeGeometry, seed: int = 42, device="cuda"):
         w1[e] = (torch.randn(2 * I, H, generator=g, device=device) * H ** -0.5).to(torch.bfloat16)
         w2[e] = (torch.randn(H, I, generator=g, device=device) * I ** -0.5).to(torch.bfloat16)
     return w1, w2
+
+
+def make_fp8_weights(geom: MoeGeometry, seed: int = 42, device="cuda"):
+    """make_weights, quantised to MXFP8 operands expert by expert."""
+    from .quant import MxFp8Weights, prepare_mxfp8_weights
+
+    w1, w2 = make_weights(geom, seed, device)
+    parts = [prepare_mxfp8_weights(w1[e:e + 1], w2[e:e + 1]) for e in range(geom.E)]
+    del w1, w2
+    return MxFp8Weights(*(torch.cat([getattr(p, f) for p in parts]) for f in ("w1_q", "w1_sf", "w2_q", "w2_sf")))
 
 
 def make_inputs(geom: MoeGeometry, hist: ExpertHistogram, seed: int, device="cuda"):
@@ -63,12 +73,14 @@ class MeasuredTimer:
     """Times every config of a pool on one histogram with the real megakernel."""
 
     def __init__(self, geom: MoeGeometry, table: DeviceTable, w1=None, w2=None, iters: int = 5,
-                 flush_mb: int = 256, device="cuda"):
+                 flush_mb: int = 256, device="cuda", fp8_weights=None):
+        """`fp8_weights` (quant.MxFp8Weights): time the FP8 megakernel instead."""
         self.geom = geom
         self.table = table
         self.iters = iters
         self.device = device
-        if w1 is None:
+        self.fp8 = fp8_weights
+        if w1 is None and fp8_weights is None:
             w1, w2 = make_weights(geom, device=device)
         self.w1, self.w2 = w1, w2
         self.flush = torch.empty(flush_mb << 20, dtype=torch.uint8, device=device)
@@ -79,14 +91,18 @@ class MeasuredTimer:
 
     def time_configs(self, x, ids, w, config_ids) -> np.ndarray:
         S, H = x.shape
-        I = self.w2.shape[2]
+        I = self.geom.N // 2
         ws = Workspace(S, H, I, self.geom.E, self.geom.top_k, device=self.device)
         out = torch.empty(S, H, dtype=torch.bfloat16, device=self.device)
         res = np.empty(len(config_ids))
         stream = torch.cuda.Stream()
         for n, cid in enumerate(config_ids):
-            call = lambda: fused_moe(x, self.w1, self.w2, w, ids, self.table, int(cid), out=out,  # noqa: E731
-                                     workspace=ws)
+            if self.fp8 is not None:
+                call = lambda: fused_moe_fp8(x, self.fp8, w, ids, self.table, int(cid), out=out,  # noqa: E731
+                                             workspace=ws)
+            else:
+                call = lambda: fused_moe(x, self.w1, self.w2, w, ids, self.table, int(cid), out=out,  # noqa: E731
+                                         workspace=ws)
             with torch.cuda.stream(stream):
                 call()  # warm-up (also encodes the cached tensor maps)
                 graph = torch.cuda.CUDAGraph()

@@ -40,7 +40,7 @@ from paper_2604_26039_b200.cost_model import (B200_BATCH_SIZES, b4_features, coe
 from paper_2604_26039_b200.routing import sample_histogram  # noqa: E402
 from paper_2604_26039_b200.dispatch import DispatchTable, evaluate_regret, speedup_ra_vs_static  # noqa: E402
 from paper_2604_26039_b200.moe import DeviceTable  # noqa: E402
-from paper_2604_26039_b200.sweep import MeasuredTimer  # noqa: E402
+from paper_2604_26039_b200.sweep import MeasuredTimer, make_fp8_weights  # noqa: E402
 from paper_2604_26039_b200.trace import load_trace, profile  # noqa: E402
 
 
@@ -102,17 +102,18 @@ def main() -> None:
     ap.add_argument("--out", default=str(ROOT / "paper_2604_26039_b200" / "data"))
     ap.add_argument("--skip-eval", action="store_true")
     ap.add_argument("--eval-iters", type=int, default=7)
+    ap.add_argument("--dtype", default="bf16", choices=("bf16", "fp8"))
     ap.add_argument("--refit", action="store_true", help="reuse the existing trace (no profiling sweep)")
     a = ap.parse_args()
     out = Path(a.out)
     out.mkdir(parents=True, exist_ok=True)
     geom = BASELINE_MODELS[a.model]
     hw = HardwareModel.b200()
-    pool = enumerate_b200_configs(geom, hw)
+    pool = enumerate_b200_configs(geom, hw, dtype=a.dtype)
     cols = pool.columns()
     n = len(pool)
     plan = profiling_plan(geom, batch_sizes=B200_BATCH_SIZES)
-    tag = f"{a.model}_b200"
+    tag = f"{a.model}_b200" + ("_fp8" if a.dtype == "fp8" else "")
     trace_path = out / f"trace_{tag}.csv"
     t0 = time.time()
     def make_timer():
@@ -120,6 +121,8 @@ def main() -> None:
                            group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], a=np.ones(n),
                            b=np.zeros(n), c=np.zeros(n), d=np.zeros(n), N=geom.N, kappa_ok=False,
                            sm_count=hw.sm_count)
+        if a.dtype == "fp8":
+            return MeasuredTimer(geom, flat, iters=a.iters, fp8_weights=make_fp8_weights(geom))
         return MeasuredTimer(geom, flat, iters=a.iters)
 
     timer = None
