@@ -72,6 +72,10 @@ typedef struct ramp_table {
   const int32_t* ntile;
   double omega_max;
   const double* lam;
+  /* kps[i]     k-blocks (64 K-elements each) per pipeline stage of config i,
+   *            1, 2 or 4 (BF16 megakernel; null = 1).  Larger stages raise the
+   *            per-CTA weight-streaming rate of the decode configs. */
+  const int32_t* kps;
 } ramp_table_t;
 
 /* Library version (major*10000 + minor*100 + patch) and sm_100a build flag. */
@@ -142,6 +146,22 @@ int ramp_fused_moe_bf16_ex(const void* x, const void* w1, const void* w2, const 
                            int32_t* sel_out, void* workspace, size_t workspace_bytes, int32_t phases,
                            void* stream);
 
+/* Router fusion: the BF16 layer straight from the router's
+ * logits, vLLM's fused_moe(hidden_states, w1, w2, gating_output, topk,
+ * renormalize) contract.  The route kernel first takes the softmax top-k of
+ * router_logits[S,E] (fp32, or bf16 when logits_bf16) per token: the k
+ * highest probabilities, ties to the lower expert id; weights = the softmax
+ * probabilities (fp32), divided by their sum over the k picks when
+ * renormalize.  It writes them to topk_w_out[S,k] / topk_ids_out[S,k]
+ * (device) and continues exactly as ramp_fused_moe_bf16 on them -- the
+ * routing decision never round-trips through another kernel.
+ * Needs top_k <= 32 and S * top_k <= 16384. */
+int ramp_fused_moe_gating_bf16(const void* x, const void* w1, const void* w2, const void* router_logits,
+                               int32_t logits_bf16, int32_t renormalize, float* topk_w_out, int32_t* topk_ids_out,
+                               int32_t S, int32_t H, int32_t I, int32_t E, int32_t top_k, const ramp_table_t* table,
+                               int32_t forced_cfg, void* out, int32_t* sel_out, void* workspace,
+                               size_t workspace_bytes, void* stream);
+
 /* Fused MoE layer forward, block-scaled FP8 (MXFP8: E4M3 operands with one
  * UE8M0 scale per 32 K elements, kind::mxf8f6f4.block_scale MMAs).
  * w1_q [E,2I,H] / w2_q [E,H,I] e4m3; w1_sf / w2_sf their scale atoms tiled as
@@ -161,13 +181,17 @@ int64_t ramp_config_smem_bytes_fp8(int32_t bm, int32_t ttn, int32_t stg);
  * configuration is not realisable on this part (pool admissibility test,
  * the B200 counterpart of smem_usage/is_valid, ramp/config_space.py:122-138). */
 int64_t ramp_config_smem_bytes(int32_t bm, int32_t ttn, int32_t stg, int32_t mode);
+/* Same with kps k-blocks per stage (1, 2 or 4); 0 if not realisable. */
+int64_t ramp_config_smem_bytes_kps(int32_t bm, int32_t ttn, int32_t stg, int32_t mode, int32_t kps);
 
 /* Diagnostics: when dev_buf is non-null, every later megakernel launch writes
  * 32 per-CTA slots (cycle counters of the producer / MMA / epilogue roles and
  * globaltimer stamps of the kernel's phases, see ProfSlot in
  * csrc/fused_moe.cuh) to dev_buf[blockIdx * 32 + slot], and the route kernel
- * writes globaltimer stamps to dev_buf[148 * 32 + 0..15]
- * (buffer: >= 149 * 32 entries).
+ * writes globaltimer stamps to dev_buf[148 * 32 + 0..15]; from
+ * dev_buf[149 * 32] on, each CTA logs its first 16 jobs as
+ * {job id, claimed, loads issued, epilogue done} (4 entries per job)
+ * (buffer: >= 149 * 32 + 148 * 16 * 4 entries).
  * Pass null to switch it off.  Not used on the timed path. */
 void ramp_set_profile_buffer(unsigned long long* dev_buf);
 

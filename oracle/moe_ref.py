@@ -35,6 +35,8 @@ def fused_moe_ref(x: np.ndarray, w1: np.ndarray, w2: np.ndarray, topk_w: np.ndar
     flat_w = np.asarray(topk_w, dtype=np.float32).reshape(-1)
     tok = np.repeat(np.arange(S), k)
     for e in np.unique(flat_ids):
+        if e == -1:
+            continue  # non-local slot (expert-parallel convention): no work
         sel = np.nonzero(flat_ids == e)[0]
         xe = x[tok[sel]]                                   # gather  [n, H]
         h = xe @ np.asarray(w1[e], dtype=np.float32).T     # phase 1 [n, 2I]
@@ -46,9 +48,26 @@ def fused_moe_ref(x: np.ndarray, w1: np.ndarray, w2: np.ndarray, topk_w: np.ndar
     return out
 
 
+def topk_softmax_ref(logits: np.ndarray, k: int, renormalize: bool):
+    """Router top-k (vLLM fused_topk semantics, the contract of
+    ramp_fused_moe_gating_bf16): fp32 softmax over the experts, the k highest
+    probabilities per token (ties to the lower expert id), weights = those
+    probabilities, divided by their sum when `renormalize`.
+    Returns (weights [S, k] fp32, ids [S, k] int32)."""
+    z = np.asarray(logits, dtype=np.float32)
+    p = np.exp(z - z.max(axis=1, keepdims=True))
+    p = p / p.sum(axis=1, keepdims=True)
+    ids = np.argsort(-z, axis=1, kind="stable")[:, :k]   # stable: ties keep the lower id first
+    w = np.take_along_axis(p, ids, axis=1)
+    if renormalize:
+        w = w / w.sum(axis=1, keepdims=True)
+    return w.astype(np.float32), ids.astype(np.int32)
+
+
 def moe_align_ref(topk_ids: np.ndarray, E: int, bm: int):
     """Histogram + stable alignment (the contract of ramp_moe_align).
 
+    Slots holding -1 (an expert owned by another rank) are skipped.
     Returns (hist[E], sorted_ids[n_post_pad], tile_expert[n_post_pad/bm], n_post_pad):
     flat assignment indices grouped by expert in ascending order, each
     expert's run padded with the sentinel n = topk_ids.size up to a multiple
@@ -57,11 +76,13 @@ def moe_align_ref(topk_ids: np.ndarray, E: int, bm: int):
     """
     flat = np.asarray(topk_ids, dtype=np.int64).reshape(-1)
     n = flat.size
-    if n and (flat.min() < 0 or flat.max() >= E):
+    valid = flat != -1  # -1 = non-local slot (expert-parallel convention): skipped
+    if n and valid.any() and (flat[valid].min() < 0 or flat[valid].max() >= E):
         raise ValueError("expert id out of range")
-    hist = np.bincount(flat, minlength=E).astype(np.int64)
+    hist = np.bincount(flat[valid], minlength=E).astype(np.int64)
     padded = -(-hist // bm) * bm
-    order = np.argsort(flat, kind="stable")
+    key = np.where(valid, flat, E)  # skipped slots sort after every expert
+    order = np.argsort(key, kind="stable")
     sorted_ids = np.full(int(padded.sum()), n, dtype=np.int64)
     tile_expert = np.repeat(np.arange(E), padded // bm)
     starts = np.concatenate(([0], np.cumsum(padded)[:-1]))

@@ -43,6 +43,12 @@ SIGNATURES = {
     ),
 }
 SIGNATURES["ramp_config_smem_bytes_fp8"] = (ctypes.c_int64, [ctypes.c_int32] * 3)
+SIGNATURES["ramp_config_smem_bytes_kps"] = (ctypes.c_int64, [ctypes.c_int32] * 5)
+SIGNATURES["ramp_fused_moe_gating_bf16"] = (
+    ctypes.c_int,
+    [ctypes.c_void_p] * 4 + [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
+    + [ctypes.c_int32] * 5 + [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                              ctypes.c_size_t, ctypes.c_void_p])
 SIGNATURES["ramp_fused_moe_fp8"] = (
     ctypes.c_int,
     [ctypes.c_void_p] * 7 + [ctypes.c_int32] * 5 + [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
@@ -76,6 +82,7 @@ class RampTable(ctypes.Structure):
         ("ntile", ctypes.c_void_p),
         ("omega_max", ctypes.c_double),
         ("lam", ctypes.c_void_p),
+        ("kps", ctypes.c_void_p),
     ]
 
 

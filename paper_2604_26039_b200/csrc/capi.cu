@@ -106,6 +106,10 @@ int64_t ramp_config_smem_bytes(int32_t bm, int32_t ttn, int32_t stg, int32_t mod
   return ramp::config_smem_bytes(bm, ttn, stg, mode, false);
 }
 
+int64_t ramp_config_smem_bytes_kps(int32_t bm, int32_t ttn, int32_t stg, int32_t mode, int32_t kps) {
+  return ramp::config_smem_bytes(bm, ttn, stg, mode, false, kps);
+}
+
 int64_t ramp_config_smem_bytes_fp8(int32_t bm, int32_t ttn, int32_t stg) {
   if (bm < 16 || ttn < 256 || (ttn / 128) * ramp::bm_mma_host(bm) > 448) return 0;
   return ramp::config_smem_bytes(bm, ttn, stg, 1, true);
@@ -144,7 +148,9 @@ size_t ramp_fused_moe_workspace_size(int32_t S, int32_t H, int32_t I, int32_t E,
 static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const void* w2, const uint8_t* w2_sf,
                       const float* topk_w, const int32_t* topk_ids, int32_t S, int32_t H, int32_t I, int32_t E,
                       int32_t top_k, const ramp_table_t* table, int32_t forced_cfg, void* out, int32_t* sel_out,
-                      void* workspace, size_t workspace_bytes, int32_t phases, void* stream, bool fp8) {
+                      void* workspace, size_t workspace_bytes, int32_t phases, void* stream, bool fp8,
+                      const void* logits = nullptr, int32_t logits_bf16 = 0, int32_t renorm = 0,
+                      float* w_out = nullptr) {
   if (phases < 1 || phases > 3) return fail(RAMP_EINVAL, "phases must be 1 (route), 2 (megakernel) or 3");
   if (int rc = check_table(table)) return rc;
   if (S < 0) return fail(RAMP_EINVAL, "S must be >= 0");
@@ -194,6 +200,11 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   ra.S = S;
   ra.H = H;
   ra.top_k = top_k;
+  ra.pdl_early = ramp::pdl_mode() == 1;
+  ra.logits = logits;
+  ra.logits_bf16 = logits_bf16;
+  ra.renorm = renorm;
+  ra.w_out = w_out;
   const int zero_blocks = 0;
   cudaError_t err = cudaSuccess;
   if (phases & 1) {
@@ -252,6 +263,20 @@ int ramp_fused_moe_bf16(const void* x, const void* w1, const void* w2, const flo
                         void* workspace, size_t workspace_bytes, void* stream) {
   return ramp_fused_moe_bf16_ex(x, w1, w2, topk_w, topk_ids, S, H, I, E, top_k, table, forced_cfg, out, sel_out,
                                 workspace, workspace_bytes, 3, stream);
+}
+
+int ramp_fused_moe_gating_bf16(const void* x, const void* w1, const void* w2, const void* router_logits,
+                               int32_t logits_bf16, int32_t renormalize, float* topk_w_out, int32_t* topk_ids_out,
+                               int32_t S, int32_t H, int32_t I, int32_t E, int32_t top_k, const ramp_table_t* table,
+                               int32_t forced_cfg, void* out, int32_t* sel_out, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  if (top_k < 1 || top_k > ramp::kMaxTopK) return fail(RAMP_EINVAL, "router fusion needs 1 <= top_k <= 32");
+  if ((int64_t)S * top_k > ramp::kIdCache)
+    return fail(RAMP_EINVAL, "router fusion needs S * top_k <= 16384 (the ids stay in shared memory)");
+  if (S > 0 && (!router_logits || !topk_w_out || !topk_ids_out)) return fail(RAMP_EINVAL, "null router buffer");
+  return fused_impl(x, w1, nullptr, w2, nullptr, topk_w_out, topk_ids_out, S, H, I, E, top_k, table, forced_cfg, out,
+                    sel_out, workspace, workspace_bytes, 3, stream, false, router_logits, logits_bf16, renormalize,
+                    topk_w_out);
 }
 
 int ramp_fused_moe_fp8(const void* x, const void* w1_q, const uint8_t* w1_sf, const void* w2_q,

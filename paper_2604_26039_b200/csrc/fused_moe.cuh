@@ -50,8 +50,13 @@ constexpr int kModeFused = 0;
 constexpr int kModeSplit = 1;
 
 __host__ __device__ inline int bm_mma(int bm) { return bm <= 16 ? 16 : (bm + 15) / 16 * 16; }
-__host__ __device__ inline int stage_bytes(int bm, int ttn) {
-  const int raw = (ttn >= 256 ? ttn / 128 : 1) * kSubTileBytes + bm_mma(bm) * 128;
+// One ring stage holds kps consecutive k-blocks: kps x (ttn/128 weight boxes
+// of 16 KB) followed by kps token tiles of bm_mma rows x 128 B.  Bigger stages
+// raise the per-CTA streaming rate (a CTA completes roughly one stage per
+// 0.25 us however small the stage, scripts/hbm_probe.cu), which is what the
+// few-CTA decode regime is bound by.
+__host__ __device__ inline int stage_bytes(int bm, int ttn, int kps = 1) {
+  const int raw = kps * ((ttn >= 256 ? ttn / 128 : 1) * kSubTileBytes + bm_mma(bm) * 128);
   return (raw + 1023) / 1024 * 1024;
 }
 // FP8 (MXFP8) stages also carry the 512-byte scale-factor atoms of the nA
@@ -67,8 +72,8 @@ __host__ __device__ inline int act_bytes(int bm, int ttn, int mode) {
 // Dynamic shared memory of one config (the B200 counterpart of smem_usage(),
 // ramp/config_space.py:122-124): 1 KB alignment slack, control block,
 // scatter transpose buffer, stg ring stages, fused mode's bf16 act tile.
-__host__ __device__ inline int moe_smem_bytes(int bm, int ttn, int stg, int mode, bool fp8 = false) {
-  return 1024 + kCtrlBytes + kStageBytesScatter + stg * (fp8 ? stage_bytes_fp8(bm, ttn) : stage_bytes(bm, ttn)) +
+__host__ __device__ inline int moe_smem_bytes(int bm, int ttn, int stg, int mode, bool fp8 = false, int kps = 1) {
+  return 1024 + kCtrlBytes + kStageBytesScatter + stg * (fp8 ? stage_bytes_fp8(bm, ttn) : stage_bytes(bm, ttn, kps)) +
          (fp8 ? 0 : act_bytes(bm, ttn, mode));
 }
 constexpr int kSfCol = 480;  // TMEM columns 480.. hold the scale factors of the FP8 MMAs
@@ -112,7 +117,9 @@ struct MoeParams {
   ramp_table_t table;
   int32_t S, H, I, E, top_k, n_assign;
   unsigned long long* prof;    // optional per-CTA cycle counters [gridDim][16] (diagnostics)
+  unsigned long long* jlog;    // optional per-CTA job log [gridDim][kJobLog][4] (diagnostics)
 };
+constexpr int kJobLog = 16;  // jobs logged per CTA: {job id, claimed, loads issued, epilogue done} (ns)
 
 // Diagnostic counters (cycles, per CTA) written when MoeParams::prof != null.
 enum ProfSlot {
@@ -153,6 +160,11 @@ struct CtrlSmem {
 static_assert(sizeof(CtrlSmem) <= kCtrlBytes, "control block overflow");
 
 // Job decoding, identical in every role.
+template <int N>
+struct KpsC {
+  static constexpr int value = N;
+};
+
 struct Job {
   int kind;  // 0 = phase 1(+2) of (m, s) [fused: +phase 3], 1 = split phase 3 of (m, hc)
   int m, s, hc;
@@ -160,7 +172,7 @@ struct Job {
 };
 
 struct Geometry {
-  int mode, bm, bmN, nA, n_i, stripes, n_mtiles, n_hc, kbH, kbI, nJobA, total, group_m, sk;
+  int mode, bm, bmN, nA, n_i, stripes, n_mtiles, n_hc, kbH, kbI, nJobA, total, group_m, sk, kps;
   bool dbl;  // TMEM double buffering across jobs (split mode, fits in 256 columns)
   __device__ __forceinline__ Job job(int j) const {
     Job r;
@@ -283,8 +295,13 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   G.nJobA = G.n_mtiles * G.stripes * G.sk;
   G.total = G.nJobA + (G.mode == kModeSplit ? G.n_mtiles * G.n_hc * G.sk : 0);
   G.dbl = !kFp8 && G.mode == kModeSplit && G.nA * G.bmN <= 256;
-  const int bmN = G.bmN, nA = G.nA;
-  const int sbytes = kFp8 ? stage_bytes_fp8(G.bm, ttn) : stage_bytes(G.bm, ttn);
+  // k-blocks per stage (BF16 only); every job's k-range must split into whole stages
+  G.kps = (!kFp8 && p.table.kps) ? p.table.kps[cfg] : 1;
+  if (G.kps != 2 && G.kps != 4) G.kps = 1;
+  if ((G.kbH / G.sk) % G.kps != 0 || (G.mode == kModeSplit && (G.kbI / G.sk) % G.kps != 0)) G.kps = 1;
+  const int bmN = G.bmN, nA = G.nA, kps = G.kps;
+  const int sbytes = kFp8 ? stage_bytes_fp8(G.bm, ttn) : stage_bytes(G.bm, ttn, kps);
+  const int tok_off = kps * nA * kSubTileBytes;  // token tiles follow the stage's weight boxes
   const uint32_t act_addr = ring_addr + stg * sbytes;
   unsigned char* act_ptr = base + kCtrlBytes + kStageBytesScatter + stg * sbytes;
   const CUtensorMap* tm_xs = kFp8 ? &maps.xq[bmn_index(bmN)] : &maps.xs[bmn_index(bmN)];
@@ -376,12 +393,15 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   }
 
   if (warp == 0) {
+    auto role = [&](auto kc) {
     // ============================ TMA producer ============================
     // The whole warp walks the schedule (so every operand is warp-uniform and
     // stays on the uniform datapath); one elected lane issues each TMA.
     const uint64_t pol_w = policy_evict_first();
     const uint64_t pol_x = policy_evict_last();
     const int u_stg = warp_uniform(stg), u_sbytes = warp_uniform(sbytes);
+    constexpr int u_kps = decltype(kc)::value;  // compile-time: runtime trip counts slow the issue loops
+    const int u_tok = warp_uniform(tok_off);
     uint32_t stage = 0, phase = 0;
     unsigned long long c_wait = 0, c_issue = 0, c_dep = 0, t_begin = clock64();
     ProfClock pc;
@@ -398,6 +418,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       c_wait += pc.lap();
     };
     uint32_t js = 0, jph = 0;
+    int n_claimed = 0;
     bool gathered = direct_x;
     while (true) {
       // claim the next job (dynamic, in global order) and publish it to the ring
@@ -413,11 +434,18 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       __syncwarp();
       if (++js == 4) { js = 0; jph ^= 1; }
       if (j < 0) break;
+      unsigned long long* jl_row =
+          (p.jlog && n_claimed < kJobLog) ? p.jlog + (static_cast<size_t>(blockIdx.x) * kJobLog + n_claimed) * 4 : nullptr;
+      ++n_claimed;
+      if (jl_row && lane == 0) {
+        jl_row[0] = static_cast<unsigned long long>(j);
+        jl_row[1] = globaltimer();
+      }
       const Job jb = G.job(j);
       const int e = warp_uniform(p.tile_expert[jb.m]);
       const int row0 = jb.m * G.bm;
       if (jb.kind == 0) {
-        const uint32_t tx1 = nA * kSubTileBytes + bmN * 128 + (kFp8 ? (nA + 1) * 512 : 0);
+        const uint32_t tx1 = u_kps * (nA * kSubTileBytes + bmN * 128) + (kFp8 ? (nA + 1) * 512 : 0);
         const int wrow = jb.s * G.n_i;
         const int kb0 = G.kb_lo(jb), kb1 = G.kb_hi(jb);
         int first_pending = 0, npend = 0;
@@ -431,19 +459,21 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
 #pragma unroll
           for (int q = 0; q < 16; ++q) trow[q] = __shfl_sync(0xffffffffu, mine, q);
         }
-        // token-side loads of one k-block (tile + FP8 scale atom), deferrable
+        // token-side loads of one stage (tiles + FP8 scale atom), deferrable
         auto load_tokens = [&](uint32_t sb, uint32_t full, int kb) {
-          tma_load_2d(sb + nA * kSubTileBytes, tm_xs, full, kb * kKb, row0, pol_x);
+          for (int q = 0; q < u_kps; ++q)
+            tma_load_2d(sb + u_tok + q * bmN * 128, tm_xs, full, (kb + q) * kKb, row0, pol_x);
           if constexpr (kFp8)
             bulk_g2s(sb + sf_off + nA * 512, p.x_sf + (static_cast<int64_t>(jb.m) * G.kbH + kb) * 512, 512, full);
         };
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; kb += u_kps) {
           acquire();
           if (elect_one()) {
             const uint32_t full = smem_u32(&cs.full[stage]);
             const uint32_t sb = ring_addr + stage * u_sbytes;
             mbar_arrive_expect_tx(full, tx1);
-            tma_load_3d(sb, tm_w1, full, kb * kKb, wrow, 2 * e, pol_w);
+            for (int q = 0; q < u_kps; ++q)
+              tma_load_3d(sb + q * nA * kSubTileBytes, tm_w1, full, (kb + q) * kKb, wrow, 2 * e, pol_w);
             if constexpr (kFp8) {
               for (int t = 0; t < nA; ++t) {
                 const int half = nA / 2;
@@ -453,10 +483,12 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
               }
             }
             if (direct_x) {
+              for (int u = 0; u < u_kps; ++u) {
 #pragma unroll
-              for (int q = 0; q < 16; q += 4)
-                tma_gather4(sb + nA * kSubTileBytes + q * 128, &maps.x, full, kb * 64, trow[q], trow[q + 1],
-                            trow[q + 2], trow[q + 3], pol_x);
+                for (int q = 0; q < 16; q += 4)
+                  tma_gather4(sb + u_tok + u * 16 * 128 + q * 128, &maps.x, full, (kb + u) * 64, trow[q], trow[q + 1],
+                              trow[q + 2], trow[q + 3], pol_x);
+              }
             } else if (gathered) {
               load_tokens(sb, full, kb);
             }
@@ -467,7 +499,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             // every CTA has published its slice of x_sorted
             if (npend == 0) first_pending = kb;
             ++npend;
-            if (npend == u_stg || kb == kb1 - 1) {
+            if (npend == u_stg || kb + u_kps >= kb1) {
               pc.lap();
               while (ld_acquire_gpu(p.gbar) < (int)gridDim.x) __nanosleep(32);
               fence_proxy_async_global();
@@ -477,7 +509,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
               if (elect_one()) {
                 for (int q = 0; q < npend; ++q) {
                   const uint32_t st = (stage + u_stg - (npend - 1) + q) % u_stg;
-                  load_tokens(ring_addr + st * u_sbytes, smem_u32(&cs.full[st]), first_pending + q);
+                  load_tokens(ring_addr + st * u_sbytes, smem_u32(&cs.full[st]), first_pending + q * u_kps);
                 }
               }
               __syncwarp();
@@ -503,31 +535,34 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       } else {
         // Split phase 3: weights stream immediately; the act rows wait for
         // every phase-1 job of this M-tile (release/acquire on done[m]).
-        const uint32_t tx = kSubTileBytes + bmN * 128 + (kFp8 ? 2 * 512 : 0);
+        const uint32_t tx = u_kps * (kSubTileBytes + bmN * 128) + (kFp8 ? 2 * 512 : 0);
         const int wrow = e * p.H + jb.hc * 128;
         const int kb0 = G.kb_lo(jb), kb1 = G.kb_hi(jb);
+        // act tiles sit after the stage's weight area (FP8: right after the one W2 box)
+        const int a_off = kFp8 ? kSubTileBytes : u_tok;
         int first_pending = 0, npend = 0;
         bool ready = false;
         // Pull this job's whole W2 slice toward L2 now: while the act rows are
         // still being produced by the phase-1 jobs, HBM keeps streaming weights,
         // and once the dependency resolves the slice arrives from L2.
         if (ld_acquire_gpu(p.done + jb.m) < G.stripes) {
-          for (int kb = kb0 + u_stg + lane; kb < kb1; kb += 32) tma_prefetch_2d(tm_w2, kb * kKb, wrow);
+          for (int kb = kb0 + u_stg * u_kps + lane; kb < kb1; kb += 32) tma_prefetch_2d(tm_w2, kb * kKb, wrow);
         }
         __syncwarp();
         auto load_act = [&](uint32_t sb, uint32_t full, int kb) {
-          tma_load_2d(sb + kSubTileBytes, tm_act, full, kb * kKb, row0, pol_x);
+          for (int q = 0; q < u_kps; ++q)
+            tma_load_2d(sb + a_off + q * bmN * 128, tm_act, full, (kb + q) * kKb, row0, pol_x);
           if constexpr (kFp8)
             bulk_g2s(sb + kSubTileBytes + bmN * 128 + 512, p.act_sf + (static_cast<int64_t>(jb.m) * G.kbI + kb) * 512,
                      512, full);
         };
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; kb += u_kps) {
           acquire();
           if (elect_one()) {
             const uint32_t full = smem_u32(&cs.full[stage]);
             const uint32_t sb = ring_addr + stage * u_sbytes;
             mbar_arrive_expect_tx(full, tx);
-            tma_load_2d(sb, tm_w2, full, kb * kKb, wrow, pol_w);
+            for (int q = 0; q < u_kps; ++q) tma_load_2d(sb + q * kSubTileBytes, tm_w2, full, (kb + q) * kKb, wrow, pol_w);
             if constexpr (kFp8)
               bulk_g2s(sb + kSubTileBytes + bmN * 128, p.w2_sf + (static_cast<int64_t>(wrow / 128) * G.kbI + kb) * 512,
                        512, full);
@@ -537,7 +572,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           if (!ready) {
             if (npend == 0) first_pending = kb;
             ++npend;
-            if (npend == u_stg || kb == kb1 - 1) {
+            if (npend == u_stg || kb + u_kps >= kb1) {
               pc.lap();
               while (ld_acquire_gpu(p.done + jb.m) < G.stripes) __nanosleep(64);
               fence_proxy_async_global();
@@ -547,7 +582,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
                 // the pending k-blocks sit in the npend stages ending at `stage`
                 for (int q = 0; q < npend; ++q) {
                   const uint32_t st = (stage + u_stg - (npend - 1) + q) % u_stg;
-                  load_act(ring_addr + st * u_sbytes, smem_u32(&cs.full[st]), first_pending + q);
+                  load_act(ring_addr + st * u_sbytes, smem_u32(&cs.full[st]), first_pending + q * u_kps);
                 }
               }
               __syncwarp();
@@ -556,6 +591,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           next();
         }
       }
+      if (jl_row && lane == 0) jl_row[2] = globaltimer();
     }
     if (p.prof && lane == 0) {
       unsigned long long* pr = p.prof + blockIdx.x * kNumProf;
@@ -565,11 +601,26 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       pr[kPrWaitDep] = c_dep;
       pr[kTotal] = clock64() - t_begin;
     }
+    };
+    // kps is chosen on the device per call: one compiled copy of the role per
+    // value (a runtime trip count in these loops costs ~30 % of the issue rate)
+    if constexpr (kFp8) {
+      role(KpsC<1>{});
+    } else if (kps == 4) {
+      role(KpsC<4>{});
+    } else if (kps == 2) {
+      role(KpsC<2>{});
+    } else {
+      role(KpsC<1>{});
+    }
   } else if (warp == 1) {
+    auto role = [&](auto kc) {
     // ============================ MMA issuer =============================
     // Whole warp iterates; one elected lane issues the tcgen05 instructions.
     const uint32_t idesc = idesc_bf16(128, warp_uniform(bmN));
     const int u_stg = warp_uniform(stg), u_sbytes = warp_uniform(sbytes);
+    constexpr int u_kps = decltype(kc)::value;  // compile-time: runtime trip counts slow the issue loops
+    const int u_tok = warp_uniform(tok_off);
     const uint32_t u_tmem = warp_uniform(tmem);
     const uint64_t act_desc = sw128_kmajor_desc(act_addr);
     const int a_step = warp_uniform(bmN) * 128 >> 4;  // act K-block stride in descriptor units
@@ -616,10 +667,10 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       tc_fence_after();
       const int kb0 = G.kb_lo(jb), kb1 = G.kb_hi(jb);
       if (jb.kind == 0) {
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; kb += u_kps) {
           const uint32_t sb = wait_full();
           const uint64_t da = sw128_kmajor_desc(sb);
-          const uint64_t db = sw128_kmajor_desc(sb + nA * kSubTileBytes);
+          const uint64_t db = sw128_kmajor_desc(sb + (kFp8 ? nA * kSubTileBytes : u_tok));
           if (elect_one()) {
             if constexpr (kFp8) {
               // scale atoms smem -> TMEM; in-order with the MMAs that read them
@@ -632,12 +683,13 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
                            (uint32_t(k) << 30) | (u_tmem + kSfCol + 4 * t), (uint32_t(k) << 30) | (u_tmem + kSfCol + 4 * nA));
               }
             } else {
-              for (int t = 0; t < nA; ++t) {
+              for (int q = 0; q < u_kps; ++q)
+                for (int t = 0; t < nA; ++t) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                  mma_bf16(acc + t * bmN, da + ((t * kSubTileBytes + k * 32) >> 4), db + ((k * 32) >> 4), idesc,
-                           ((kb - kb0) | k) != 0);
-              }
+                  for (int k = 0; k < 4; ++k)
+                    mma_bf16(acc + t * bmN, da + ((((q * nA + t) * kSubTileBytes) + k * 32) >> 4),
+                             db + ((q * bmN * 128 + k * 32) >> 4), idesc, ((kb - kb0) | q | k) != 0);
+                }
             }
           }
           __syncwarp();
@@ -675,10 +727,10 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           }
         }
       } else {
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; kb += u_kps) {
           const uint32_t sb = wait_full();
           const uint64_t da = sw128_kmajor_desc(sb);
-          const uint64_t db = sw128_kmajor_desc(sb + kSubTileBytes);
+          const uint64_t db = sw128_kmajor_desc(sb + (kFp8 ? kSubTileBytes : u_tok));
           if (elect_one()) {
             if constexpr (kFp8) {
               const uint32_t sfs = sb + kSubTileBytes + bmN * 128;
@@ -689,9 +741,12 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
                 mma_mxf8(acc, da + ((k * 32) >> 4), db + ((k * 32) >> 4), idesc_mxf8(128, bmN, k), ((kb - kb0) | k) != 0,
                          (uint32_t(k) << 30) | (u_tmem + kSfCol), (uint32_t(k) << 30) | (u_tmem + kSfCol + 4));
             } else {
+              for (int q = 0; q < u_kps; ++q) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                mma_bf16(acc, da + ((k * 32) >> 4), db + ((k * 32) >> 4), idesc, ((kb - kb0) | k) != 0);
+                for (int k = 0; k < 4; ++k)
+                  mma_bf16(acc, da + ((q * kSubTileBytes + k * 32) >> 4), db + ((q * bmN * 128 + k * 32) >> 4), idesc,
+                           ((kb - kb0) | q | k) != 0);
+              }
             }
           }
           __syncwarp();
@@ -708,6 +763,18 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       pr[kMmaWaitAcc] = c_acc;
       pr[kMmaWaitAct] = c_act;
       pr[kItems] = items;
+    }
+    };
+    // kps is chosen on the device per call: one compiled copy of the role per
+    // value (a runtime trip count in these loops costs ~30 % of the issue rate)
+    if constexpr (kFp8) {
+      role(KpsC<1>{});
+    } else if (kps == 4) {
+      role(KpsC<4>{});
+    } else if (kps == 2) {
+      role(KpsC<2>{});
+    } else {
+      role(KpsC<1>{});
     }
   } else if (warp >= 4) {
     // ============================ epilogue ===============================
@@ -942,6 +1009,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         }
         c_scatter += pc.lap();
       }
+      if (p.jlog && et == 0 && jl < (uint32_t)kJobLog)
+        p.jlog[(static_cast<size_t>(blockIdx.x) * kJobLog + jl) * 4 + 3] = globaltimer();
     }
     if (p.prof && et == 0) {
       unsigned long long* pr = p.prof + blockIdx.x * kNumProf;

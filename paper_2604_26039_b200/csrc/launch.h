@@ -32,7 +32,15 @@ struct RouteArgs {
   const void* x;         // [S, H] bf16 tokens
   void* x_sorted;        // [rows, H] bf16, gathered by the helper blocks (null: skip)
   int32_t S, H, top_k;
+  int32_t pdl_early;     // trigger the dependent launch at entry (1) or after the alignment (0)
+  // router fusion: when logits != null the route kernel first computes the
+  // softmax top-k into topk_ids (== ids_out) and w_out
+  const void* logits;    // [S, E] fp32 or bf16
+  int32_t logits_bf16, renorm;
+  float* w_out;          // [S, top_k]
 };
+
+int pdl_mode();  // RAMP_PDL: 0 off, 1 trigger at route entry (default), 2 trigger at route exit
 
 cudaError_t launch_route(const RouteArgs& a, int zero_blocks, cudaStream_t stream);
 cudaError_t launch_align(const int32_t* ids, int64_t n, int E, int bm, int32_t* hist, int32_t* sorted_ids,
@@ -72,6 +80,6 @@ struct MoeLaunch {
 extern unsigned long long* g_prof_buffer;  // diagnostics, see ramp_set_profile_buffer
 
 cudaError_t launch_fused_moe(const MoeLaunch& l, cudaStream_t stream, const char** why);
-int64_t config_smem_bytes(int bm, int ttn, int stg, int mode, bool fp8);
+int64_t config_smem_bytes(int bm, int ttn, int stg, int mode, bool fp8, int kps = 1);
 
 }  // namespace ramp

@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "fused_moe.cuh"
@@ -11,6 +12,14 @@
 namespace ramp {
 
 unsigned long long* g_prof_buffer = nullptr;
+
+int pdl_mode() {
+  static int mode = [] {
+    const char* v = getenv("RAMP_PDL");
+    return v ? atoi(v) : 1;
+  }();
+  return mode;
+}
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
@@ -60,11 +69,12 @@ static bool make_map_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64
   return make_map(map, ptr, 2, dims, strides, box, bytes);
 }
 
-int64_t config_smem_bytes(int bm, int ttn, int stg, int mode, bool fp8) {
+int64_t config_smem_bytes(int bm, int ttn, int stg, int mode, bool fp8, int kps) {
   if (bm < 1 || bm > kMaxBm || (ttn != 128 && ttn != 256 && ttn != 512) || stg < 1 || stg > kMaxStages)
     return 0;
   if (mode != kModeFused && mode != kModeSplit) return 0;
-  const int b = moe_smem_bytes(bm, ttn, stg, mode, fp8);
+  if (kps != 1 && (fp8 || (kps != 2 && kps != 4))) return 0;
+  const int b = moe_smem_bytes(bm, ttn, stg, mode, fp8, kps);
   return b <= kSmemLimit ? b : 0;
 }
 
@@ -200,6 +210,7 @@ cudaError_t launch_fused_moe(const MoeLaunch& l, cudaStream_t stream, const char
   p.top_k = l.top_k;
   p.n_assign = l.S * l.top_k;
   p.prof = g_prof_buffer;
+  p.jlog = g_prof_buffer ? g_prof_buffer + 149 * 32 : nullptr;
   // Programmatic dependent launch: the megakernel's prologue (barrier init,
   // TMEM allocation, descriptor prefetch) may overlap the route kernel's tail.
   cudaLaunchAttribute pdl[1];
@@ -211,7 +222,7 @@ cudaError_t launch_fused_moe(const MoeLaunch& l, cudaStream_t stream, const char
   cfg.dynamicSmemBytes = kSmemLimit;
   cfg.stream = stream;
   cfg.attrs = pdl;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_mode() ? 1 : 0;
   err = l.fp8 ? cudaLaunchKernelEx(&cfg, fused_moe_kernel<true>, maps, p)
               : cudaLaunchKernelEx(&cfg, fused_moe_kernel<false>, maps, p);
   if (err != cudaSuccess) return err;

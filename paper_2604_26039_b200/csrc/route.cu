@@ -18,7 +18,7 @@ struct RouteStatic {
 
 __global__ void __launch_bounds__(kRouteThreads, 1)
     route_kernel(const RouteArgs a) {
-  pdl_launch_dependents();  // let the megakernel's prologue start on idle SMs
+  if (a.pdl_early) pdl_launch_dependents();  // let the megakernel's prologue start on idle SMs
   auto stamp = [&](int slot) {
     if (a.prof && threadIdx.x == 0) a.prof[slot] = globaltimer();
   };
@@ -71,22 +71,51 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   __shared__ RouteStatic st;
   RouteSmem s = carve_route_smem(dyn, a.E, a.n_assign);
   stamp(0);
+  if (a.prof && threadIdx.x == 0) a.prof[6] = clock64();
+  // the dispatch table is constant: start loading this thread's config now
+  const CfgRegs pre = a.forced_cfg < 0 ? dispatch_prefetch(a.table) : CfgRegs{};
   if (threadIdx.x == 0) st.bad = 0;
+  if (a.logits) {
+    // router fusion: the top-k is computed here (host checked n <= kIdCache)
+    block_topk(a.logits, a.logits_bf16 != 0, a.S, a.E, a.top_k, a.renorm != 0, s.ids,
+               const_cast<int32_t*>(a.topk_ids), a.w_out);
+  }
   __syncthreads();
-  block_count(a.topk_ids, a.n_assign, a.E, s, &st.bad);
+  block_count(a.topk_ids, a.n_assign, a.E, s, &st.bad, a.logits != nullptr);
   stamp(1);
   int sel = a.forced_cfg;
   int n_eval = 0;
+  // Warp specialisation: the dispatcher needs one thread per config; the
+  // remaining warps walk the (bm-independent) alignment ranks meanwhile.
+  const int cfg_warps = (a.table.n_cfg + 31) >> 5;
+  const bool overlap = s.cached && sel < 0 && cfg_warps <= kRouteWarps - 8;
   if (sel < 0) {
-    sel = block_dispatch(s.hist, a.E, a.table, a.grid_out, a.pred_out, a.n_eval_out, st.mt, st.red,
-                         st.cnt);
-    n_eval = st.cnt[0];
+    if (!overlap) {
+      sel = block_dispatch(s.hist, a.E, a.table, pre, a.grid_out, a.pred_out, a.n_eval_out, st.mt, st.red,
+                           st.cnt, a.prof);
+      n_eval = st.cnt[0];
+    } else if (static_cast<int>(threadIdx.x >> 5) < cfg_warps) {
+      block_dispatch(s.hist, a.E, a.table, pre, a.grid_out, a.pred_out, a.n_eval_out, st.mt, st.red, st.cnt,
+                     a.prof, cfg_warps);
+    } else {
+      block_walk_ranks(a.n_assign, a.E, s, cfg_warps, kRouteWarps - cfg_warps);
+    }
+    if (overlap) {
+      __syncthreads();
+      sel = st.red[0].i;
+      n_eval = st.cnt[0];
+    }
   }
   stamp(2);
+  if (a.prof && threadIdx.x == 0) a.prof[7] = clock64();
   const int bm = a.table.bm[sel];
   int32_t* n_post_pad = a.ctrl + 1;
-  block_align(a.topk_ids, a.n_assign, a.E, bm, s, st.warp_tot, a.sorted_ids, a.tile_expert,
-              n_post_pad, a.prof);
+  if (overlap) {
+    block_place(a.n_assign, a.E, bm, s, st.warp_tot, a.sorted_ids, a.tile_expert, n_post_pad, a.prof);
+  } else {
+    block_align(a.topk_ids, a.n_assign, a.E, bm, s, st.warp_tot, a.sorted_ids, a.tile_expert, n_post_pad,
+                a.prof);
+  }
   stamp(3);
   const int npp = s.off[a.E];
   for (int e = threadIdx.x; e < a.E; e += blockDim.x)
@@ -114,6 +143,7 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
     st_release_gpu(a.ctrl + 5, 1);
   }
   stamp(4);
+  if (!a.pdl_early) pdl_launch_dependents();
 }
 
 __global__ void __launch_bounds__(kRouteThreads, 1)
@@ -135,10 +165,11 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
                   int64_t* grid_out, double* pred_out) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ RouteStatic st;
+  const CfgRegs pre = dispatch_prefetch(t);
   int32_t* h = reinterpret_cast<int32_t*>(dyn);
   for (int e = threadIdx.x; e < E; e += blockDim.x) h[e] = hist[e];
   __syncthreads();
-  const int sel = block_dispatch(h, E, t, grid_out, pred_out, n_eval_out, st.mt, st.red, st.cnt);
+  const int sel = block_dispatch(h, E, t, pre, grid_out, pred_out, n_eval_out, st.mt, st.red, st.cnt);
   if (threadIdx.x == 0) *cfg_out = sel;
 }
 

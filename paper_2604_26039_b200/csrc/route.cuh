@@ -5,6 +5,7 @@
 // alignment the megakernel consumes).
 #pragma once
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <math_constants.h>
 
 #include "../../include/ramp_b200.h"
@@ -16,23 +17,34 @@ constexpr int kRouteWarps = kRouteThreads / 32;
 constexpr int kMaxExperts = 512;
 constexpr int kMaxUbm = 128;
 constexpr int kIdCache = 16384;  // topk ids kept in shared memory between the two passes
+constexpr int kStageMax = 20480; // sorted ids staged in shared memory, then copied out coalesced
+constexpr int kAlignMaxBm = 128;
 
 // Dynamic shared memory layout of the route block (sized by E and n).
 //   hist[E]       bincount
 //   off[E+1]      exclusive scan of the padded counts
 //   cnt[E][32]    per-(expert, warp) counts, then exclusive prefixes over warps
 //   ids[min(n, kIdCache)]
+//   stage[stage_cap]  sorted ids built here (scattered shared stores), then
+//                     written to global memory with coalesced 16-byte stores
 struct RouteSmem {
   int32_t* hist;
   int32_t* off;
   int32_t* cnt;
   int32_t* ids;
+  int32_t* stage;
+  int stage_cap;
   bool cached;
 };
 
+__host__ __device__ inline int route_stage_cap(int E, int64_t n) {
+  const int64_t want = n + (int64_t)E * (kAlignMaxBm - 1);
+  return static_cast<int>(want < kStageMax ? want : kStageMax);
+}
+
 __host__ __device__ inline size_t route_smem_bytes(int E, int64_t n) {
   const int64_t cache = n <= kIdCache ? n : 0;
-  return sizeof(int32_t) * ((size_t)E * 34 + 1 + (size_t)cache) + 64;
+  return sizeof(int32_t) * ((size_t)E * 34 + 1 + (size_t)cache + 4 + (size_t)route_stage_cap(E, n)) + 64;
 }
 
 __device__ inline RouteSmem carve_route_smem(unsigned char* base, int E, int64_t n) {
@@ -42,6 +54,9 @@ __device__ inline RouteSmem carve_route_smem(unsigned char* base, int E, int64_t
   s.cnt = s.off + E + 1;
   s.ids = s.cnt + 32 * E;
   s.cached = n <= kIdCache;
+  const uintptr_t st = reinterpret_cast<uintptr_t>(s.ids + (s.cached ? n : 0));
+  s.stage = reinterpret_cast<int32_t*>((st + 15) & ~static_cast<uintptr_t>(15));
+  s.stage_cap = route_stage_cap(E, n);
   return s;
 }
 
@@ -65,17 +80,89 @@ __host__ __device__ inline int bits_for(int E) {
   return b;
 }
 
+// --------------------------------------------------------------- router
+// Router fusion: softmax top-k of the router logits, one
+// warp per token.  Lane l holds experts l, l+32, ...; the k picks are k
+// rounds of a warp arg-max (higher probability first, ties to the lower
+// expert id); weights are the softmax probabilities (fp32, expf), divided by
+// their sum over the picks when `renorm` (vLLM's fused_topk semantics).  The
+// ids land in shared memory (the histogram pass reads them there) and, with
+// the weights, in global memory for the megakernel and the caller.
+constexpr int kMaxTopK = 32;
+__device__ inline void block_topk(const void* __restrict__ logits, bool bf16, int S, int E, int k, bool renorm,
+                                  int32_t* ids_smem, int32_t* __restrict__ ids_out, float* __restrict__ w_out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int per = (E + 31) >> 5;  // <= 16 for E <= 512
+  for (int t = warp; t < S; t += nwarps) {
+    float v[kMaxExperts / 32];
+    float mx = -CUDART_INF_F;
+#pragma unroll
+    for (int j = 0; j < kMaxExperts / 32; ++j) {
+      v[j] = -CUDART_INF_F;
+      const int e = lane + 32 * j;
+      if (j < per && e < E) {
+        const size_t at = static_cast<size_t>(t) * E + e;
+        v[j] = bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(logits)[at])
+                    : reinterpret_cast<const float*>(logits)[at];
+        mx = fmaxf(mx, v[j]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxExperts / 32; ++j)
+      if (j < per && lane + 32 * j < E) sum += expf(v[j] - mx);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    unsigned taken = 0;
+    float mine = 0.f, picked = 0.f;
+    for (int r = 0; r < k; ++r) {
+      float bv = -CUDART_INF_F;
+      int be = 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < kMaxExperts / 32; ++j) {
+        const int e = lane + 32 * j;
+        if (j < per && e < E && !((taken >> j) & 1) && (v[j] > bv || (v[j] == bv && e < be))) {
+          bv = v[j];
+          be = e;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+        if (ov > bv || (ov == bv && oe < be)) {
+          bv = ov;
+          be = oe;
+        }
+      }
+      if ((be & 31) == lane) taken |= 1u << (be >> 5);
+      const float pr = expf(bv - mx) / sum;
+      picked += pr;
+      if (lane == r) mine = pr;
+      if (lane == 0) {
+        ids_smem[t * k + r] = be;
+        ids_out[t * k + r] = be;
+      }
+    }
+    if (lane < k) w_out[t * k + lane] = renorm ? mine / picked : mine;
+  }
+}
+
 // --------------------------------------------------------------- histogram
 // Pass 1 of the stable counting sort.  The n flat assignments are cut into 32
 // contiguous segments, one per warp; each warp counts its segment per expert
 // (warp-aggregated with match.any, no atomics: the warp owns column w of
 // cnt), then one warp scan per expert turns the 32 counts into exclusive
 // prefixes and the total, i.e. bincount(topk_ids, minlength=E).
-// Ids outside [0, E) set *bad (ExpertHistogram rejects them, ramp/routing.py:45-50).
+// Ids outside [0, E) set *bad (ExpertHistogram rejects them, ramp/routing.py:45-50),
+// except -1: a slot whose expert lives on another rank (vLLM's expert-parallel
+// convention) -- skipped, it is neither counted nor aligned.
 __device__ inline void block_count(const int32_t* __restrict__ ids, int64_t n, int E, RouteSmem& s,
-                                   int* bad) {
+                                   int* bad, bool ids_in_smem = false) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (s.cached)
+  if (s.cached && !ids_in_smem)
     for (int64_t i = tid; i < n; i += blockDim.x) s.ids[i] = __ldg(ids + i);
   for (int x = tid; x < 32 * E; x += blockDim.x) s.cnt[x] = 0;
   __syncthreads();
@@ -86,7 +173,7 @@ __device__ inline void block_count(const int32_t* __restrict__ ids, int64_t n, i
     int e = -1;
     if (i < hi) {
       e = s.cached ? s.ids[i] : __ldg(ids + i);
-      if (e < 0 || e >= E) {
+      if (e != -1 && (e < 0 || e >= E)) {
         *bad = 1;
         e = -1;
       }
@@ -122,21 +209,75 @@ __device__ inline bool argmin_better(const ArgMin& x, const ArgMin& y) {
   return x.i < y.i;
 }
 
+// Static fields of one config, loaded into registers at kernel entry so their
+// global-memory latency overlaps the histogram pass (the table is constant;
+// only g depends on the routing).
+struct CfgRegs {
+  long long stripes;  // work tiles per M-tile (ntile, or ceil(N/ttn))
+  int sk, ubm_idx;
+  int ubm_w;          // distinct bm value number (warp index), for the M-tile counts
+  double a, b, c, d, lam;
+};
+
+__device__ __forceinline__ CfgRegs load_cfg(const ramp_table_t& t, int i) {
+  CfgRegs r;
+  r.sk = __ldg(t.split_k + i);
+  r.ubm_idx = __ldg(t.ubm_index + i);
+  r.stripes = t.ntile ? __ldg(t.ntile + i) : (static_cast<long long>(t.N) + __ldg(t.ttn + i) - 1) / __ldg(t.ttn + i);
+  r.a = __ldg(t.a + i);
+  r.b = __ldg(t.b + i);
+  r.c = __ldg(t.c + i);
+  r.d = __ldg(t.d + i);
+  r.lam = t.lam ? __ldg(t.lam + i) : 0.0;
+  return r;
+}
+
+// Config handled first by this thread (index threadIdx.x), prefetched.
+__device__ __forceinline__ CfgRegs dispatch_prefetch(const ramp_table_t& t) {
+  CfgRegs r{};
+  if (static_cast<int>(threadIdx.x) < t.n_cfg) r = load_cfg(t, threadIdx.x);
+  const int w = threadIdx.x >> 5;
+  r.ubm_w = w < t.n_ubm ? __ldg(t.ubm + w) : 1;
+  return r;
+}
+
 // Evaluates every config of the table on the histogram in shared memory and
 // returns (in every thread) the selected id.  fp64 arithmetic follows
 // predict_batch exactly: ((a + b*ceil(g/sm)) + c*g) + d*log(g+1)
 // (ramp/cost_model.py:104-114), gate (g/split_k)/sm < 0.2 (ramp/dispatch.py:107-114),
-// first argmin over +inf-masked predictions (:118-119).
-__device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_table_t& t,
+// first argmin over +inf-masked predictions (:118-119).  `pre` holds the
+// prefetched fields of config threadIdx.x (dispatch_prefetch).
+//
+// Runs on warps [0, nwarps) of the block; with nwarps < blockDim/32 the group
+// synchronises on named barrier 3 only, so the other warps can walk the
+// alignment ranks meanwhile (route_kernel).  Threads outside the group must
+// not call it.
+__device__ __forceinline__ void group_sync(int nwarps) {
+  if (nwarps * 32 == static_cast<int>(blockDim.x)) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync 3, %0;" ::"r"(nwarps * 32) : "memory");
+  }
+}
+
+__device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_table_t& t, const CfgRegs& pre,
                                      int64_t* grid_out, double* pred_out, int* n_eval_out,
                                      int64_t* mt_smem /*[kMaxUbm]*/, ArgMin* red_smem /*[32]*/,
-                                     int* cnt_smem /*[32]*/) {
+                                     int* cnt_smem /*[32]*/, unsigned long long* stamps = nullptr,
+                                     int nwarps = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = blockDim.x >> 5;
+  if (nwarps <= 0) nwarps = blockDim.x >> 5;
+  auto stamp = [&](int slot) {
+    if (stamps && threadIdx.x == 0) {
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+      stamps[slot] = tt;
+    }
+  };
   // M-tiles per distinct bm: sum over active experts of ceil(c_e / bm)
   // (m_tile_counts, ramp/routing.py:197-203).
   for (int u = warp; u < t.n_ubm; u += nwarps) {
-    const int bm = t.ubm[u];
+    const int bm = u == warp ? pre.ubm_w : t.ubm[u];
     long long acc = 0;
     for (int e = lane; e < E; e += 32) {
       const int c = hist[e];
@@ -155,31 +296,43 @@ __device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_tabl
     for (int o = 16; o > 0; o >>= 1) na += __shfl_xor_sync(0xffffffffu, na, o);
     if (lane == 0) s_nact = na;
   }
-  __syncthreads();
+  group_sync(nwarps);
+  stamp(12);
   const double nact = t.lam ? static_cast<double>(s_nact) : 0.0;
 
   const double sm = static_cast<double>(t.sm_count);
   const double omega_max = t.omega_max > 0.0 ? t.omega_max : 0.2;
   ArgMin best{CUDART_INF, 0x7fffffff};
   int kept = 0;
-  for (int i = threadIdx.x; i < t.n_cfg; i += blockDim.x) {
-    const int ttn = t.ttn[i], sk = t.split_k[i];
-    const long long stripes = t.ntile ? t.ntile[i] : (static_cast<long long>(t.N) + ttn - 1) / ttn;
-    const long long g = mt_smem[t.ubm_index[i]] * stripes * sk;
+  const long long smi = t.sm_count;
+  for (int i = threadIdx.x; i < t.n_cfg; i += nwarps * 32) {
+    const CfgRegs r = i == static_cast<int>(threadIdx.x) ? pre : load_cfg(t, i);
+    const int sk = r.sk;
+    const long long stripes = r.stripes;
+    const long long g = mt_smem[r.ubm_idx] * stripes * sk;
     const double gd = static_cast<double>(g);
     bool keep = true;
-    if (sk > 1) keep = t.kappa_ok && (__ddiv_rn(__ddiv_rn(gd, static_cast<double>(sk)), sm) < omega_max);
+    // (an infinite threshold keeps every finite ratio: skip the divisions)
+    if (sk > 1)
+      keep = t.kappa_ok && (isinf(omega_max) || __ddiv_rn(__ddiv_rn(gd, static_cast<double>(sk)), sm) < omega_max);
     // B4: HBM-equivalent traffic grid (first M-tile of an expert streams its
     // weights from HBM, later ones re-read them at lam x the cost from L2)
     double gl = gd;
     if (t.lam) {
-      const double mt = static_cast<double>(mt_smem[t.ubm_index[i]]);
-      const double u = __dadd_rn(nact, __dmul_rn(t.lam[i], __dadd_rn(mt, -nact)));
+      const double mt = static_cast<double>(mt_smem[r.ubm_idx]);
+      const double u = __dadd_rn(nact, __dmul_rn(r.lam, __dadd_rn(mt, -nact)));
       gl = __dmul_rn(static_cast<double>(stripes * sk), u);
     }
-    double p = __dadd_rn(t.a[i], __dmul_rn(t.b[i], ceil(__ddiv_rn(gd, sm))));
-    p = __dadd_rn(p, __dmul_rn(t.c[i], gl));
-    p = __dadd_rn(p, __dmul_rn(t.d[i], log(__dadd_rn(gl, 1.0))));
+    // ceil(g / sm) as an integer division: the fp64 quotient of two integers
+    // below 2^40 rounds to within far less than 1/sm of the true value, so
+    // numpy's np.ceil(g / sm) is exactly this integer.
+    const double waves = static_cast<double>(
+        g < (1ll << 31) ? static_cast<long long>((static_cast<unsigned>(g) + static_cast<unsigned>(smi) - 1u) /
+                                                 static_cast<unsigned>(smi))
+                        : (g + smi - 1) / smi);
+    double p = __dadd_rn(r.a, __dmul_rn(r.b, waves));
+    p = __dadd_rn(p, __dmul_rn(r.c, gl));
+    p = __dadd_rn(p, __dmul_rn(r.d, log(__dadd_rn(gl, 1.0))));
     if (grid_out) grid_out[i] = g;
     if (!keep) p = CUDART_INF;
     if (pred_out) pred_out[i] = p;
@@ -187,20 +340,25 @@ __device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_tabl
     const ArgMin cand{p, i};
     if (argmin_better(cand, best)) best = cand;
   }
+  stamp(13);
+  // only warps that evaluated a config take part in the reduction
+  const int cfg_warps = min(nwarps, (t.n_cfg + 31) >> 5);
+  if (warp < cfg_warps) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    ArgMin other{__shfl_xor_sync(0xffffffffu, best.v, o), __shfl_xor_sync(0xffffffffu, best.i, o)};
-    if (argmin_better(other, best)) best = other;
-    kept += __shfl_xor_sync(0xffffffffu, kept, o);
+    for (int o = 16; o > 0; o >>= 1) {
+      ArgMin other{__shfl_xor_sync(0xffffffffu, best.v, o), __shfl_xor_sync(0xffffffffu, best.i, o)};
+      if (argmin_better(other, best)) best = other;
+      kept += __shfl_xor_sync(0xffffffffu, kept, o);
+    }
+    if (lane == 0) {
+      red_smem[warp] = best;
+      cnt_smem[warp] = kept;
+    }
   }
-  if (lane == 0) {
-    red_smem[warp] = best;
-    cnt_smem[warp] = kept;
-  }
-  __syncthreads();
+  group_sync(nwarps);
   if (warp == 0) {
-    ArgMin b = lane < nwarps ? red_smem[lane] : ArgMin{CUDART_INF, 0x7fffffff};
-    int k = lane < nwarps ? cnt_smem[lane] : 0;
+    ArgMin b = lane < cfg_warps ? red_smem[lane] : ArgMin{CUDART_INF, 0x7fffffff};
+    int k = lane < cfg_warps ? cnt_smem[lane] : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       ArgMin other{__shfl_xor_sync(0xffffffffu, b.v, o), __shfl_xor_sync(0xffffffffu, b.i, o)};
@@ -213,9 +371,10 @@ __device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_tabl
       if (n_eval_out) *n_eval_out = k;
     }
   }
-  __syncthreads();
+  group_sync(nwarps);
+  stamp(14);
   const int sel = red_smem[0].i;
-  __syncthreads();
+  group_sync(nwarps);
   return sel;
 }
 
@@ -251,7 +410,103 @@ __device__ inline int block_exclusive_scan(int v, int* warp_tot /*[32]*/, int* t
 // indices grouped by expert, ascending within an expert, each expert's run
 // padded to a multiple of bm with the sentinel n (== S*top_k).  (The
 // reference has no alignment code; this order is our contract.)
+//
+// Split in two so the bm-independent half can overlap the dispatcher:
+//   block_walk_ranks  each of the 32 segments of pass 1 is walked in order;
+//                     an assignment's rank within its expert = earlier
+//                     segments' count of that expert + its running count in
+//                     the segment + its rank within the 32-chunk (ballot-per-
+//                     bit match).  The rank is packed into the cached id
+//                     (id | rank << 10), so ids must be cached (n <= kIdCache).
+//   block_place       with the selected bm: padded exclusive scan, padding /
+//                     tile experts, then every assignment lands at
+//                     off[e] + rank (shared-memory staged, coalesced copy-out).
 // Requires blockDim.x == 1024, E <= kMaxExperts and block_count() first.
+constexpr int kRankShift = 10;  // E <= 512 fits below it; rank < 16384 above
+
+__device__ inline void block_walk_ranks(int64_t n, int E, RouteSmem& s, int first_warp, int n_walkers) {
+  const int warp = (threadIdx.x >> 5) - first_warp, lane = threadIdx.x & 31;
+  const int nbits = bits_for(E);
+  const int64_t seg = (n + kRouteWarps - 1) / kRouteWarps;
+  for (int sg = warp; sg < kRouteWarps; sg += n_walkers) {
+    const int64_t lo = sg * seg, hi = lo + seg < n ? lo + seg : n;
+    for (int64_t c0 = lo; c0 < hi; c0 += 32) {
+      const int64_t i = c0 + lane;
+      int e = -1;
+      if (i < hi) {
+        e = s.ids[i];
+        if (e < 0 || e >= E) {
+          e = -1;
+          s.ids[i] = -1;  // skipped (or rejected) slots never reach block_place
+        }
+      }
+      const unsigned peers = match_peers(e, nbits);
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      int base = 0;
+      if (e >= 0) {
+        base = s.cnt[e * 32 + sg];
+        s.ids[i] = e | ((base + rank) << kRankShift);
+      }
+      __syncwarp();
+      if (e >= 0 && rank == 0) s.cnt[e * 32 + sg] = base + __popc(peers);
+      __syncwarp();
+    }
+  }
+}
+
+__device__ inline void block_place(int64_t n, int E, int bm, RouteSmem& s, int* warp_tot,
+                                   int32_t* __restrict__ sorted_ids, int32_t* __restrict__ tile_expert,
+                                   int32_t* n_post_pad_out, unsigned long long* stamps = nullptr) {
+  auto stamp = [&](int slot) {
+    if (stamps && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      stamps[slot] = t;
+    }
+  };
+  const int tid = threadIdx.x;
+  int padded = 0, c = 0;
+  if (tid < E) {
+    c = s.hist[tid];
+    padded = (c + bm - 1) / bm * bm;
+  }
+  int total = 0;
+  const int off = block_exclusive_scan(padded, warp_tot, &total);
+  // stage in shared memory when the list is long enough for scattered global
+  // stores to cost more than the copy-out, and fits (total is block-uniform)
+  const bool staged = n >= 2048 && total <= s.stage_cap;
+  int32_t* const dst = staged ? s.stage : sorted_ids;
+  if (tid < E) {
+    s.off[tid] = off;
+    for (int q = off + c; q < off + padded; ++q) dst[q] = static_cast<int32_t>(n);
+    for (int tt = off / bm; tt < (off + padded) / bm; ++tt) tile_expert[tt] = tid;
+  }
+  if (tid == 0) {
+    s.off[E] = total;
+    if (n_post_pad_out) *n_post_pad_out = total;
+  }
+  __syncthreads();
+  stamp(5);
+  for (int64_t i = tid; i < n; i += blockDim.x) {
+    const int v = s.ids[i];
+    if (v >= 0) dst[s.off[v & ((1 << kRankShift) - 1)] + (v >> kRankShift)] = static_cast<int32_t>(i);
+  }
+  __syncthreads();
+  if (staged) {
+    // coalesced copy-out (sorted_ids is 16-byte aligned in the workspace)
+    const bool vec = (reinterpret_cast<uintptr_t>(sorted_ids) & 15) == 0;
+    const int n4 = vec ? total / 4 : 0;
+    const int4* src4 = reinterpret_cast<const int4*>(s.stage);
+    int4* dst4 = reinterpret_cast<int4*>(sorted_ids);
+    for (int q = tid; q < n4; q += blockDim.x) dst4[q] = src4[q];
+    for (int q = n4 * 4 + tid; q < total; q += blockDim.x) sorted_ids[q] = s.stage[q];
+    __syncthreads();
+  }
+}
+
+// Single pass (no dispatch to overlap with): padded scan first, then one walk
+// that writes every position straight to global memory.  Ids come from the
+// shared-memory cache when n <= kIdCache, else from global memory.
 __device__ inline void block_align(const int32_t* __restrict__ ids, int64_t n, int E, int bm,
                                    RouteSmem& s, int* warp_tot, int32_t* __restrict__ sorted_ids,
                                    int32_t* __restrict__ tile_expert, int32_t* n_post_pad_out,
@@ -282,8 +537,6 @@ __device__ inline void block_align(const int32_t* __restrict__ ids, int64_t n, i
   }
   __syncthreads();
   stamp(5);
-  // each warp walks its segment again in order; position = expert base +
-  // earlier warps' count + this warp's running count + rank within the chunk
   const int nbits = bits_for(E);
   const int64_t seg = (n + kRouteWarps - 1) / kRouteWarps;
   const int64_t lo = warp * seg, hi = lo + seg < n ? lo + seg : n;

@@ -9,7 +9,8 @@ Rank r of a P-rank group owns experts [r*E/P, (r+1)*E/P).  One MoE layer:
      (token, rank) pairs -- the "pre-reduce per (token, rank)" of SURVEY §8e.
   2. the owner runs the fused-MoE megakernel on its local experts: the
      received rows are its tokens, their local expert ids / weights its top-k
-     (unused slots carry weight 0 and expert 0);
+     (slots of other ranks' experts carry expert -1 and weight 0; the route
+     kernel skips them, so they cost no work);
   3. combine: the per-(token, rank) partial outputs travel back and are
      summed into the origin tokens.
 
@@ -64,7 +65,8 @@ def dispatch(x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor, E: i
     # per sent row: the token's assignments that live on that rank (others -> weight 0)
     row_owner = owner[pair_token]                                        # [P, k]
     hit = row_owner == pair_rank[:, None]
-    row_ids = torch.where(hit, topk_ids[pair_token].long() - pair_rank[:, None] * per, 0)
+    # slots of other ranks' experts carry -1: the route kernel skips them
+    row_ids = torch.where(hit, topk_ids[pair_token].long() - pair_rank[:, None] * per, -1)
     row_w = torch.where(hit, topk_w[pair_token], torch.zeros((), dtype=topk_w.dtype, device=dev))
     send_x = x[pair_token].contiguous()
     R = sum(rc)
@@ -94,20 +96,31 @@ def ep_moe_layer(x, topk_ids, topk_w, E: int, local_fn, group=None):
     return combine(plan, partial, x.shape[0], group)
 
 
-def make_local_megakernel(w1_local, w2_local, table, workspace_cache: dict | None = None):
-    """local_fn running the B200 megakernel on this rank's experts."""
-    from .moe import Workspace, fused_moe
+def make_local_megakernel(weights, table, workspace_cache: dict | None = None):
+    """local_fn running the B200 megakernel on this rank's experts.
+    `weights` is (w1_local, w2_local) bf16 or a quant.MxFp8Weights of the
+    local experts (then `table` must be an FP8 pool's)."""
+    from .moe import Workspace, fused_moe, fused_moe_fp8
 
     cache = workspace_cache if workspace_cache is not None else {}
+    fp8 = not isinstance(weights, tuple)
+    if fp8:
+        E_l, H, I = weights.shape
+    else:
+        w1_local, w2_local = weights
+        E_l, two_i, H = w1_local.shape
+        I = two_i // 2
 
     def run(rx, rids, rw):
         if rx.shape[0] == 0:
             return torch.zeros(0, rx.shape[1], dtype=rx.dtype, device=rx.device)
-        E_l, two_i, H = w1_local.shape
         key = (rx.shape[0], rids.shape[1])
         ws = cache.get(key)
         if ws is None:
-            ws = cache[key] = Workspace(rx.shape[0], H, two_i // 2, E_l, rids.shape[1], device=rx.device)
+            ws = cache[key] = Workspace(rx.shape[0], H, I, E_l, rids.shape[1], device=rx.device)
+        if fp8:
+            return fused_moe_fp8(rx.contiguous(), weights, rw.float().contiguous(), rids.contiguous(), table,
+                                 workspace=ws)
         return fused_moe(rx.contiguous(), w1_local, w2_local, rw.float().contiguous(), rids.contiguous(), table,
                          workspace=ws)
 

@@ -50,6 +50,7 @@ class DeviceTable:
     ntile: np.ndarray | None = None   # work tiles per M-tile (default ceil(N/ttn))
     omega_max: float = 0.0            # split-K gate threshold (<= 0: the reference's 0.2)
     lam: np.ndarray | None = None     # B4 L2-reuse factor per config (None: the reference model)
+    kps: np.ndarray | None = None     # k-blocks per pipeline stage per config (None: 1)
     _tensors: dict = field(default_factory=dict, repr=False)
     struct: _lib.RampTable | None = field(default=None, repr=False)
 
@@ -93,6 +94,14 @@ class DeviceTable:
                 raise ValueError("lam must have one entry per config")
             t["lam"] = torch.as_tensor(np.asarray(self.lam, dtype=np.float64), **f64)
         s.lam = t["lam"].data_ptr() if "lam" in t else None
+        if self.kps is not None:
+            kps = np.asarray(self.kps, dtype=np.int64)
+            if len(kps) != n:
+                raise ValueError("kps must have one entry per config")
+            if not np.isin(kps, (1, 2, 4)).all():
+                raise ValueError("kps values must be 1, 2 or 4")
+            t["kps"] = torch.as_tensor(kps.astype(np.int32), **i32)
+        s.kps = t["kps"].data_ptr() if "kps" in t else None
         self.struct = s
 
     def __len__(self) -> int:
@@ -187,6 +196,64 @@ def fused_moe(
         )
     )
     return out
+
+
+def fused_moe_gating(
+    hidden_states: torch.Tensor,
+    w1: torch.Tensor,
+    w2: torch.Tensor,
+    gating_output: torch.Tensor,
+    topk: int,
+    renormalize: bool,
+    table: DeviceTable,
+    forced_cfg: int = -1,
+    out: torch.Tensor | None = None,
+    workspace: Workspace | None = None,
+    return_topk: bool = False,
+):
+    """The BF16 layer from the router's logits (router fusion),
+    vLLM's `fused_moe(hidden_states, w1, w2, gating_output, topk, renormalize)`
+    contract: per token the softmax top-k of `gating_output` [S, E] (fp32 or
+    bf16) -- highest probabilities first, ties to the lower expert id; weights
+    are the fp32 softmax probabilities, renormalised over the k picks when
+    `renormalize` -- computed inside the route kernel, which then dispatches,
+    aligns and launches the megakernel as `fused_moe` does.  With
+    `return_topk` the (topk_weights, topk_ids) it chose are returned too."""
+    lib = _lib.load()
+    S, H = hidden_states.shape
+    E, two_i, H1 = w1.shape
+    I = two_i // 2
+    k = int(topk)
+    if H1 != H or tuple(w2.shape) != (E, H, I):
+        raise ValueError(f"shape mismatch: x {tuple(hidden_states.shape)}, w1 {tuple(w1.shape)}, w2 {tuple(w2.shape)}")
+    if tuple(gating_output.shape) != (S, E):
+        raise ValueError(f"gating_output must be [S, E] = {(S, E)}, got {tuple(gating_output.shape)}")
+    if gating_output.dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError(f"gating_output must be float32 or bfloat16, got {gating_output.dtype}")
+    for name, t, dt in (("hidden_states", hidden_states, torch.bfloat16), ("w1", w1, torch.bfloat16),
+                        ("w2", w2, torch.bfloat16), ("gating_output", gating_output, gating_output.dtype)):
+        if t.dtype != dt:
+            raise ValueError(f"{name} must be {dt}, got {t.dtype}")
+        if not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+    dev = hidden_states.device
+    topk_w = torch.empty(S, k, dtype=torch.float32, device=dev)
+    topk_ids = torch.empty(S, k, dtype=torch.int32, device=dev)
+    if out is None:
+        out = torch.empty(S, H, dtype=torch.bfloat16, device=dev)
+    if workspace is None or not workspace.fits(S, H, I, E, k):
+        workspace = Workspace(S, H, I, E, k, device=dev)
+    _lib.check(
+        lib.ramp_fused_moe_gating_bf16(
+            hidden_states.data_ptr(), w1.data_ptr(), w2.data_ptr(), gating_output.data_ptr(),
+            int(gating_output.dtype == torch.bfloat16), int(bool(renormalize)), topk_w.data_ptr(),
+            topk_ids.data_ptr(), S, H, I, E, k, table.ref, int(forced_cfg), out.data_ptr(),
+            workspace.sel.data_ptr(), workspace.buf.data_ptr(), workspace.buf.numel(), _stream(),
+        )
+    )
+    return (out, topk_w, topk_ids) if return_topk else out
 
 
 def fused_moe_fp8(

@@ -49,6 +49,15 @@ def test_smem_formula_matches_python(lib):
                     got = lib.ramp_config_smem_bytes(bm, ttn, stg, mode)
                     assert got == (want if want <= B200_SMEM_LIMIT else 0), (bm, ttn, stg, mode)
     assert lib.ramp_config_smem_bytes(4, 384, 2, 0) == 0
+    for bm in (4, 16, 32):
+        for ttn in (128, 256):
+            for stg in range(1, 13):
+                for mode in (0, 1):
+                    for kps in (1, 2, 4):
+                        want = b200_smem_bytes(bm, ttn, stg, mode, kps)
+                        got = lib.ramp_config_smem_bytes_kps(bm, ttn, stg, mode, kps)
+                        assert got == (want if want <= B200_SMEM_LIMIT else 0), (bm, ttn, stg, mode, kps)
+    assert lib.ramp_config_smem_bytes_kps(16, 128, 2, 1, 3) == 0
 
 
 def test_argument_validation_without_gpu(lib):

@@ -60,3 +60,25 @@ def test_bf16_round():
     r = bf16_round(x)
     assert r[0] == 1.0 and r[2] == -2.5
     assert abs(r[3] - 3.140625) < 1e-7
+
+
+def test_nonlocal_slots_are_skipped():
+    """-1 (expert-parallel: owned by another rank) == the slot removed."""
+    from oracle.moe_ref import fused_moe_ref, moe_align_ref
+
+    rng = np.random.default_rng(0)
+    S, H, I, E, k = 9, 16, 8, 4, 3
+    x = rng.standard_normal((S, H)).astype(np.float32)
+    w1 = rng.standard_normal((E, 2 * I, H)).astype(np.float32)
+    w2 = rng.standard_normal((E, H, I)).astype(np.float32)
+    ids = rng.integers(0, E, size=(S, k)).astype(np.int32)
+    w = rng.random((S, k)).astype(np.float32)
+    mask = rng.random((S, k)) < 0.4
+    ids_m = np.where(mask, -1, ids)
+    w_zero = np.where(mask, 0.0, w).astype(np.float32)
+    np.testing.assert_allclose(fused_moe_ref(x, w1, w2, w, ids_m), fused_moe_ref(x, w1, w2, w_zero, ids),
+                               rtol=1e-5, atol=1e-5)
+    hist, sorted_ids, tiles, npp = moe_align_ref(ids_m, E, 2)
+    assert hist.sum() == (~mask).sum()
+    flat = ids_m.reshape(-1)
+    assert all(flat[a] >= 0 for a in sorted_ids if a < flat.size)
