@@ -201,6 +201,12 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   ra.H = H;
   ra.top_k = top_k;
   ra.pdl_early = ramp::pdl_mode() == 1;
+  // speculative weight prefetch (BF16): only when this call also runs the
+  // route kernel, which publishes the histogram early
+  // (decode sizes only: at prefill sizes the prefetch competes with the token
+  // gather for HBM and costs more than it hides, measured at S*k = 4096)
+  const bool prefetch = !fp8 && (phases & 1) && ramp::prefetch_cap() > 0 && (int64_t)S * top_k <= 256;
+  ra.publish_hist = prefetch ? 1 : 0;
   ra.logits = logits;
   ra.logits_bf16 = logits_bf16;
   ra.renorm = renorm;
@@ -243,6 +249,9 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   ml.I = I;
   ml.E = E;
   ml.top_k = top_k;
+  ml.hist = ra.hist_out;
+  ml.pf_flag = ra.ctrl + 11;
+  ml.pf_cap = prefetch ? ramp::prefetch_cap() : 0;
   const char* why = nullptr;
   err = ramp::launch_fused_moe(ml, st, &why);
   if (err != cudaSuccess) return why ? fail(RAMP_ECUDA, why) : cuda_fail(err, "fused_moe kernel");

@@ -118,7 +118,16 @@ struct MoeParams {
   int32_t S, H, I, E, top_k, n_assign;
   unsigned long long* prof;    // optional per-CTA cycle counters [gridDim][16] (diagnostics)
   unsigned long long* jlog;    // optional per-CTA job log [gridDim][kJobLog][4] (diagnostics)
+  // Speculative weight prefetch: the route kernel publishes the histogram
+  // (hist) and raises *pf_flag long before it finishes; the CTAs, already
+  // resident under PDL, pull the active experts' weights toward L2 meanwhile.
+  const int32_t* hist;         // [E]
+  const void* w1_base;         // raw expert weights (the TMA maps hold the same pointers)
+  const void* w2_base;
+  int32_t* pf_flag;            // raised by the route kernel, cleared at the end of this kernel
+  int64_t pf_cap;              // bytes to prefetch at most (0: off)
 };
+constexpr int64_t kPrefetchCap = 64ll << 20;  // half the 126 MB L2
 constexpr int kJobLog = 16;  // jobs logged per CTA: {job id, claimed, loads issued, epilogue done} (ns)
 
 // Diagnostic counters (cycles, per CTA) written when MoeParams::prof != null.
@@ -156,6 +165,7 @@ struct CtrlSmem {
   int32_t fin;  // split-K: this CTA completed the (m, s) reduction
   int32_t epi_tok[128];
   float epi_w[128];
+  int16_t pf_act[512];  // active experts of the speculative prefetch (E <= 512)
 };
 static_assert(sizeof(CtrlSmem) <= kCtrlBytes, "control block overflow");
 
@@ -271,6 +281,49 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = cs.tmem_base;
+  if (!kFp8 && p.pf_cap > 0 && warp == 3) {
+    // Speculative L2 prefetch of the active experts' weights (W1 of every
+    // active expert in id order -- the order the first wave of phase-1 jobs
+    // reads them -- then W2), capped at pf_cap bytes and split evenly over
+    // the CTAs.  Starts as soon as the histogram is published, i.e. while the
+    // route kernel is still dispatching and aligning.
+    int spins = 0;
+    while (ld_acquire_gpu(p.pf_flag) == 0 && ++spins < (1 << 16)) __nanosleep(32);
+    if (spins < (1 << 16)) {
+      int16_t* act = cs.pf_act;
+      int n_act = 0;
+      for (int e0 = 0; e0 < p.E; e0 += 32) {
+        const int e = e0 + lane;
+        const bool a = e < p.E && __ldcg(p.hist + e) > 0;
+        const unsigned m = __ballot_sync(0xffffffffu, a);
+        if (a) act[n_act + __popc(m & ((1u << lane) - 1u))] = static_cast<int16_t>(e);
+        n_act += __popc(m);
+      }
+      __syncwarp();
+      const int64_t l1 = 2ll * p.I * p.H * 2, l2 = static_cast<int64_t>(p.H) * p.I * 2;
+      const int64_t total = static_cast<int64_t>(n_act) * (l1 + l2);
+      const int64_t cap = total < p.pf_cap ? total : p.pf_cap;
+      const int64_t per = (cap / gridDim.x + 4095) & ~4095ll;
+      const int64_t v0 = per * blockIdx.x, v1 = v0 + per < cap ? v0 + per : cap;
+      constexpr int64_t kChunk = 32 << 10;
+      const char* w1b = static_cast<const char*>(p.w1_base);
+      const char* w2b = static_cast<const char*>(p.w2_base);
+      for (int64_t v = v0 + lane * kChunk; v < v1; v += 32 * kChunk) {
+        int64_t len = v1 - v < kChunk ? v1 - v : kChunk;
+        const char* src;
+        if (v < n_act * l1) {
+          const int64_t k = v / l1, o = v % l1;
+          if (o + len > l1) len = l1 - o;
+          src = w1b + act[k] * l1 + o;
+        } else {
+          const int64_t w = v - n_act * l1, k = w / l2, o = w % l2;
+          if (o + len > l2) len = l2 - o;
+          src = w2b + act[k] * l2 + o;
+        }
+        bulk_prefetch_l2(src, static_cast<uint32_t>(len) & ~15u);
+      }
+    }
+  }
   pdl_wait();  // the route kernel's selection, alignment and gathered rows are now visible
   if (ts && threadIdx.x == 0) ts[kTsStart] = globaltimer();
 
@@ -1034,6 +1087,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     if (ts) ts[kTsEndArrive] = globaltimer();
     atomicAdd(p.gbar + 1, 1);
     while (ld_acquire_gpu(p.gbar + 1) < (int)gridDim.x) __nanosleep(64);
+    // every CTA is past its prologue: re-arm the prefetch flag for the next call
+    if (blockIdx.x == 0 && p.pf_flag) *p.pf_flag = 0;
     if (ts) ts[kTsEndPass] = globaltimer();
   }
   __syncthreads();

@@ -32,6 +32,7 @@ struct RouteArgs {
   const void* x;         // [S, H] bf16 tokens
   void* x_sorted;        // [rows, H] bf16, gathered by the helper blocks (null: skip)
   int32_t S, H, top_k;
+  int32_t publish_hist;  // write hist_out and raise ctrl[11] right after the histogram pass
   int32_t pdl_early;     // trigger the dependent launch at entry (1) or after the alignment (0)
   // router fusion: when logits != null the route kernel first computes the
   // softmax top-k into topk_ids (== ids_out) and w_out
@@ -40,7 +41,8 @@ struct RouteArgs {
   float* w_out;          // [S, top_k]
 };
 
-int pdl_mode();  // RAMP_PDL: 0 off, 1 trigger at route entry (default), 2 trigger at route exit
+int pdl_mode();
+int64_t prefetch_cap();  // RAMP_PREFETCH_MB (default 64; 0 disables the speculative weight prefetch)  // RAMP_PDL: 0 off, 1 trigger at route entry (default), 2 trigger at route exit
 
 cudaError_t launch_route(const RouteArgs& a, int zero_blocks, cudaStream_t stream);
 cudaError_t launch_align(const int32_t* ids, int64_t n, int E, int bm, int32_t* hist, int32_t* sorted_ids,
@@ -75,6 +77,9 @@ struct MoeLaunch {
   int64_t rows;     // capacity of x_sorted / act_g
   ramp_table_t table;
   int32_t S, H, I, E, top_k;
+  const int32_t* hist;  // speculative prefetch: published histogram, flag, byte cap (0 = off)
+  int32_t* pf_flag;
+  int64_t pf_cap;
 };
 
 extern unsigned long long* g_prof_buffer;  // diagnostics, see ramp_set_profile_buffer

@@ -13,6 +13,14 @@ namespace ramp {
 
 unsigned long long* g_prof_buffer = nullptr;
 
+int64_t prefetch_cap() {
+  static int64_t cap = [] {
+    const char* v = getenv("RAMP_PREFETCH_MB");
+    return (v ? atoll(v) : 64ll) << 20;
+  }();
+  return cap;
+}
+
 int pdl_mode() {
   static int mode = [] {
     const char* v = getenv("RAMP_PDL");
@@ -211,6 +219,11 @@ cudaError_t launch_fused_moe(const MoeLaunch& l, cudaStream_t stream, const char
   p.n_assign = l.S * l.top_k;
   p.prof = g_prof_buffer;
   p.jlog = g_prof_buffer ? g_prof_buffer + 149 * 32 : nullptr;
+  p.hist = l.hist;
+  p.w1_base = l.w1;
+  p.w2_base = l.w2;
+  p.pf_flag = l.pf_flag;
+  p.pf_cap = l.pf_cap;
   // Programmatic dependent launch: the megakernel's prologue (barrier init,
   // TMEM allocation, descriptor prefetch) may overlap the route kernel's tail.
   cudaLaunchAttribute pdl[1];

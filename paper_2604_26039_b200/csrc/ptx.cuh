@@ -179,6 +179,11 @@ __device__ __forceinline__ uint64_t sf_atom_desc(uint32_t smem_addr) {
   return d;
 }
 // 1D bulk copy global -> shared, completion on an mbarrier (transaction bytes).
+// Fire-and-forget L2 prefetch of a contiguous global range (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(bar)

@@ -83,6 +83,16 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   __syncthreads();
   block_count(a.topk_ids, a.n_assign, a.E, s, &st.bad, a.logits != nullptr);
   stamp(1);
+  if (a.publish_hist && a.hist_out && (threadIdx.x >> 5) == kRouteWarps - 1) {
+    // publish the histogram now: the megakernel CTAs (already resident under
+    // PDL) start prefetching the active experts' weights while we dispatch
+    for (int e = threadIdx.x & 31; e < a.E; e += 32) a.hist_out[e] = s.hist[e];
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      __threadfence();
+      st_release_gpu(a.ctrl + 11, 1);
+    }
+  }
   int sel = a.forced_cfg;
   int n_eval = 0;
   // Warp specialisation: the dispatcher needs one thread per config; the

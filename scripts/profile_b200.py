@@ -48,9 +48,9 @@ def _fit_all(pool, by_cfg, hw, variant, geom):
     cols = pool.columns()
     out = {}
     for cid, ss in by_cfg.items():
-        if variant == "B4":
+        if variant in ("B4", "B4r"):
             jpm = int(cols["ntile"][cid] * cols["split_k"][cid])
-            out[cid] = fit_b4(ss, b4_features(ss, geom, int(cols["bm"][cid]), jpm), hw)
+            out[cid] = fit_b4(ss, b4_features(ss, geom, int(cols["bm"][cid]), jpm), hw, relative=variant == "B4r")
         else:
             out[cid] = fit(ss, hw, variant)
     return out
@@ -68,7 +68,7 @@ def choose_variant(pool, trace, hw, geom):
     n_seeds = min(len(v) for v in points.values())
     ids = [c.id for c in pool]
     out = {}
-    for variant in ("P2", "P3", "P4", "B4"):
+    for variant in ("P2", "P3", "P4", "B4", "B4r"):
         regs = []
         for hold in range(n_seeds):
             train: dict[int, list] = {c: [] for c in ids}
