@@ -128,7 +128,9 @@ struct MoeParams {
   int64_t pf_cap;              // bytes to prefetch at most (0: off)
 };
 constexpr int64_t kPrefetchCap = 64ll << 20;  // half the 126 MB L2
-constexpr int kJobLog = 16;  // jobs logged per CTA: {job id, claimed, loads issued, epilogue done} (ns)
+// jobs logged per CTA: {job id, claimed, loads issued, epilogue done} (ns);
+// compiled in only with -DRAMP_JOBLOG (diagnostic build)
+constexpr int kJobLog = 16;
 
 // Diagnostic counters (cycles, per CTA) written when MoeParams::prof != null.
 enum ProfSlot {
@@ -424,6 +426,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     const int gw = blockIdx.x * kGatherWarps + (warp - 2), nw = gridDim.x * kGatherWarps;
     const int4* xv = reinterpret_cast<const int4*>(p.x);
     int4* dv = reinterpret_cast<int4*>(p.x_sorted);
+#ifdef RAMP_AB_OLD_GATHER
     for (int r = gw; r < n_post_pad; r += nw) {
       const int asg = p.sorted_ids[r];
       int4* d = dv + static_cast<int64_t>(r) * row_vec;
@@ -440,6 +443,42 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           if (c0 + 32 * u < row_vec) d[c0 + 32 * u] = v[u];
       }
     }
+#else
+    // This warp's rows are gw, gw + nw, ...: one coalesced load fetches the
+    // assignments of the next 32 of them (no per-row dependent load), and two
+    // rows move per iteration (16 x 16 B in flight per lane).
+    for (int r0 = gw; r0 < n_post_pad; r0 += 32 * nw) {
+      const int rl = r0 + lane * nw;
+      const int asg_l = rl < n_post_pad ? __ldcg(p.sorted_ids + rl) : p.n_assign;
+      const int nrows = min(32, (n_post_pad - r0 + nw - 1) / nw);
+      for (int q = 0; q < nrows; q += 2) {
+        const int a0 = __shfl_sync(0xffffffffu, asg_l, q);
+        const int a1 = __shfl_sync(0xffffffffu, asg_l, (q + 1) & 31);
+        const bool two = q + 1 < nrows;
+        const int4* s0 = xv + static_cast<int64_t>(a0 < p.n_assign ? a0 / p.top_k : 0) * row_vec;
+        const int4* s1 = xv + static_cast<int64_t>(a1 < p.n_assign ? a1 / p.top_k : 0) * row_vec;
+        int4* d0 = dv + static_cast<int64_t>(r0 + q * nw) * row_vec;
+        int4* d1 = dv + static_cast<int64_t>(r0 + (q + 1) * nw) * row_vec;
+        for (int c0 = lane; c0 < row_vec; c0 += 32 * kUnroll) {
+          int4 v0[kUnroll], v1[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const bool in = c0 + 32 * u < row_vec;
+            v0[u] = v1[u] = make_int4(0, 0, 0, 0);
+            if (in && a0 < p.n_assign) v0[u] = __ldg(s0 + c0 + 32 * u);
+            if (in && two && a1 < p.n_assign) v1[u] = __ldg(s1 + c0 + 32 * u);
+          }
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            if (c0 + 32 * u < row_vec) {
+              d0[c0 + 32 * u] = v0[u];
+              if (two) d1[c0 + 32 * u] = v1[u];
+            }
+          }
+        }
+      }
+    }
+#endif
     __threadfence();
     named_bar_sync(2, 32 * kGatherWarps);
     if (warp == 2 && lane == 0) atomicAdd(p.gbar, 1);
@@ -471,7 +510,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       c_wait += pc.lap();
     };
     uint32_t js = 0, jph = 0;
+#ifdef RAMP_JOBLOG
     int n_claimed = 0;
+#endif
     bool gathered = direct_x;
     while (true) {
       // claim the next job (dynamic, in global order) and publish it to the ring
@@ -487,6 +528,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       __syncwarp();
       if (++js == 4) { js = 0; jph ^= 1; }
       if (j < 0) break;
+#ifdef RAMP_JOBLOG
       unsigned long long* jl_row =
           (p.jlog && n_claimed < kJobLog) ? p.jlog + (static_cast<size_t>(blockIdx.x) * kJobLog + n_claimed) * 4 : nullptr;
       ++n_claimed;
@@ -494,6 +536,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         jl_row[0] = static_cast<unsigned long long>(j);
         jl_row[1] = globaltimer();
       }
+#endif
       const Job jb = G.job(j);
       const int e = warp_uniform(p.tile_expert[jb.m]);
       const int row0 = jb.m * G.bm;
@@ -644,7 +687,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           next();
         }
       }
+#ifdef RAMP_JOBLOG
       if (jl_row && lane == 0) jl_row[2] = globaltimer();
+#endif
     }
     if (p.prof && lane == 0) {
       unsigned long long* pr = p.prof + blockIdx.x * kNumProf;
@@ -657,7 +702,11 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     };
     // kps is chosen on the device per call: one compiled copy of the role per
     // value (a runtime trip count in these loops costs ~30 % of the issue rate)
+#ifdef RAMP_AB_ONE_ROLE
+    if constexpr (true) {
+#else
     if constexpr (kFp8) {
+#endif
       role(KpsC<1>{});
     } else if (kps == 4) {
       role(KpsC<4>{});
@@ -820,7 +869,11 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     };
     // kps is chosen on the device per call: one compiled copy of the role per
     // value (a runtime trip count in these loops costs ~30 % of the issue rate)
+#ifdef RAMP_AB_ONE_ROLE
+    if constexpr (true) {
+#else
     if constexpr (kFp8) {
+#endif
       role(KpsC<1>{});
     } else if (kps == 4) {
       role(KpsC<4>{});
@@ -1062,8 +1115,10 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         }
         c_scatter += pc.lap();
       }
+#ifdef RAMP_JOBLOG
       if (p.jlog && et == 0 && jl < (uint32_t)kJobLog)
         p.jlog[(static_cast<size_t>(blockIdx.x) * kJobLog + jl) * 4 + 3] = globaltimer();
+#endif
     }
     if (p.prof && et == 0) {
       unsigned long long* pr = p.prof + blockIdx.x * kNumProf;

@@ -42,7 +42,7 @@ struct RouteArgs {
 };
 
 int pdl_mode();
-int64_t prefetch_cap();  // RAMP_PREFETCH_MB (default 64; 0 disables the speculative weight prefetch)  // RAMP_PDL: 0 off, 1 trigger at route entry (default), 2 trigger at route exit
+int64_t prefetch_cap();  // RAMP_PREFETCH_MB (default 0 = off; e.g. 64 enables the speculative weight prefetch)  // RAMP_PDL: 0 off, 1 trigger at route entry (default), 2 trigger at route exit
 
 cudaError_t launch_route(const RouteArgs& a, int zero_blocks, cudaStream_t stream);
 cudaError_t launch_align(const int32_t* ids, int64_t n, int E, int bm, int32_t* hist, int32_t* sorted_ids,

@@ -16,7 +16,7 @@ unsigned long long* g_prof_buffer = nullptr;
 int64_t prefetch_cap() {
   static int64_t cap = [] {
     const char* v = getenv("RAMP_PREFETCH_MB");
-    return (v ? atoll(v) : 64ll) << 20;
+    return (v ? atoll(v) : 0ll) << 20;
   }();
   return cap;
 }

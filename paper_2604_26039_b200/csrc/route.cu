@@ -16,72 +16,32 @@ struct RouteStatic {
   int bad;
 };
 
+// One route block.  Specialised at compile time on router fusion (kGating)
+// and on device dispatch (kDispatch; false = forced config, the profiling
+// sweep): the kernel runs once per layer on one cold SM, so every byte of
+// code it does not need costs instruction-cache misses.
+template <bool kGating, bool kDispatch>
 __global__ void __launch_bounds__(kRouteThreads, 1)
     route_kernel(const RouteArgs a) {
   if (a.pdl_early) pdl_launch_dependents();  // let the megakernel's prologue start on idle SMs
   auto stamp = [&](int slot) {
     if (a.prof && threadIdx.x == 0) a.prof[slot] = globaltimer();
   };
-  if (blockIdx.x > 0) {
-    if (blockIdx.x == 1) stamp(8);
-    // Helper blocks: clear the fp32 output accumulator, then (once block 0
-    // has published the alignment) gather the token rows into expert-sorted
-    // order so the megakernel can fetch a whole M-tile with one TMA box.
-    const int nh = gridDim.x - 1, hb = blockIdx.x - 1;
-    float4* acc4 = reinterpret_cast<float4*>(a.acc_clear);
-    const int64_t n4 = a.acc_clear_n / 4;
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int64_t i = hb * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)nh * blockDim.x) acc4[i] = z;
-    for (int64_t i = n4 * 4 + hb * (int64_t)blockDim.x + threadIdx.x; i < a.acc_clear_n;
-         i += (int64_t)nh * blockDim.x)
-      a.acc_clear[i] = 0.f;
-    if (a.x_sorted == nullptr) return;
-    if (blockIdx.x == 1) stamp(9);
-    if (threadIdx.x == 0)
-      while (ld_acquire_gpu(a.ctrl + 5) == 0) __nanosleep(64);
-    __syncthreads();
-    if (blockIdx.x == 1) stamp(10);
-    const int npp = __ldcg(a.ctrl + 1);
-    const int row_vec = a.H / 8;  // 16-byte vectors per row
-    const int4* xv = reinterpret_cast<const int4*>(a.x);
-    int4* dv = reinterpret_cast<int4*>(a.x_sorted);
-    const int gw = hb * kRouteWarps + (threadIdx.x >> 5), nw = nh * kRouteWarps, lane = threadIdx.x & 31;
-    for (int r = gw; r < npp; r += nw) {
-      const int asg = __ldcg(a.sorted_ids + r);
-      int4* d = dv + static_cast<int64_t>(r) * row_vec;
-      if (asg < a.n_assign) {
-        const int4* s = xv + static_cast<int64_t>(asg / a.top_k) * row_vec;
-        for (int c = lane; c < row_vec; c += 32) d[c] = __ldg(s + c);
-      } else {
-        for (int c = lane; c < row_vec; c += 32) d[c] = make_int4(0, 0, 0, 0);
-      }
-    }
-    __syncthreads();
-    if (blockIdx.x == 1) stamp(11);
-    if (threadIdx.x == 0) {
-      // the last helper through resets the flag for the next call
-      if (atomicAdd(a.ctrl + 6, 1) == nh - 1) {
-        a.ctrl[6] = 0;
-        a.ctrl[5] = 0;
-      }
-    }
-    return;
-  }
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ RouteStatic st;
-  RouteSmem s = carve_route_smem(dyn, a.E, a.n_assign);
+  RouteSmem s = carve_route_smem(dyn, a.E, a.n_assign, kDispatch ? a.table.n_cfg : 0);
   stamp(0);
   if (a.prof && threadIdx.x == 0) a.prof[6] = clock64();
-  // the dispatch table is constant: start loading this thread's config now
-  const CfgRegs pre = a.forced_cfg < 0 ? dispatch_prefetch(a.table) : CfgRegs{};
+  // the dispatch table is constant: start copying it to shared memory now
+  if constexpr (kDispatch) stage_table(a.table, s);
   if (threadIdx.x == 0) st.bad = 0;
-  if (a.logits) {
+  if constexpr (kGating) {
     // router fusion: the top-k is computed here (host checked n <= kIdCache)
     block_topk(a.logits, a.logits_bf16 != 0, a.S, a.E, a.top_k, a.renorm != 0, s.ids,
                const_cast<int32_t*>(a.topk_ids), a.w_out);
   }
   __syncthreads();
-  block_count(a.topk_ids, a.n_assign, a.E, s, &st.bad, a.logits != nullptr);
+  block_count(a.topk_ids, a.n_assign, a.E, s, &st.bad, kGating);
   stamp(1);
   if (a.publish_hist && a.hist_out && (threadIdx.x >> 5) == kRouteWarps - 1) {
     // publish the histogram now: the megakernel CTAs (already resident under
@@ -98,14 +58,14 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   // Warp specialisation: the dispatcher needs one thread per config; the
   // remaining warps walk the (bm-independent) alignment ranks meanwhile.
   const int cfg_warps = (a.table.n_cfg + 31) >> 5;
-  const bool overlap = s.cached && sel < 0 && cfg_warps <= kRouteWarps - 8;
-  if (sel < 0) {
+  const bool overlap = kDispatch && s.cached && cfg_warps <= kRouteWarps - 8;
+  if constexpr (kDispatch) {
     if (!overlap) {
-      sel = block_dispatch(s.hist, a.E, a.table, pre, a.grid_out, a.pred_out, a.n_eval_out, st.mt, st.red,
+      sel = block_dispatch(s.hist, a.E, a.table, &s, a.grid_out, a.pred_out, a.n_eval_out, st.mt, st.red,
                            st.cnt, a.prof);
       n_eval = st.cnt[0];
     } else if (static_cast<int>(threadIdx.x >> 5) < cfg_warps) {
-      block_dispatch(s.hist, a.E, a.table, pre, a.grid_out, a.pred_out, a.n_eval_out, st.mt, st.red, st.cnt,
+      block_dispatch(s.hist, a.E, a.table, &s, a.grid_out, a.pred_out, a.n_eval_out, st.mt, st.red, st.cnt,
                      a.prof, cfg_warps);
     } else {
       block_walk_ranks(a.n_assign, a.E, s, cfg_warps, kRouteWarps - cfg_warps);
@@ -120,7 +80,7 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   if (a.prof && threadIdx.x == 0) a.prof[7] = clock64();
   const int bm = a.table.bm[sel];
   int32_t* n_post_pad = a.ctrl + 1;
-  if (overlap) {
+  if (kDispatch && overlap) {
     block_place(a.n_assign, a.E, bm, s, st.warp_tot, a.sorted_ids, a.tile_expert, n_post_pad, a.prof);
   } else {
     block_align(a.topk_ids, a.n_assign, a.E, bm, s, st.warp_tot, a.sorted_ids, a.tile_expert, n_post_pad,
@@ -175,29 +135,36 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
                   int64_t* grid_out, double* pred_out) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ RouteStatic st;
-  const CfgRegs pre = dispatch_prefetch(t);
   int32_t* h = reinterpret_cast<int32_t*>(dyn);
   for (int e = threadIdx.x; e < E; e += blockDim.x) h[e] = hist[e];
   __syncthreads();
-  const int sel = block_dispatch(h, E, t, pre, grid_out, pred_out, n_eval_out, st.mt, st.red, st.cnt);
+  const int sel = block_dispatch(h, E, t, nullptr, grid_out, pred_out, n_eval_out, st.mt, st.red, st.cnt);
   if (threadIdx.x == 0) *cfg_out = sel;
 }
 
-cudaError_t launch_route(const RouteArgs& a, int zero_blocks, cudaStream_t stream) {
-  const size_t smem = route_smem_bytes(a.E, a.n_assign);
+template <bool kGating, bool kDispatch>
+static cudaError_t launch_route_t(const RouteArgs& a, cudaStream_t stream) {
+  const size_t smem = route_smem_bytes(a.E, a.n_assign, kDispatch ? a.table.n_cfg : 0);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t err = cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)route_smem_bytes(kMaxExperts, kIdCache));
+    cudaError_t err = cudaFuncSetAttribute(route_kernel<kGating, kDispatch>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRouteSmemLimit);
     if (err != cudaSuccess) return err;
     // same shared-memory carveout as the megakernel, so SMs need no
     // reconfiguration when the megakernel launches behind it (PDL overlap)
-    err = cudaFuncSetAttribute(route_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    err = cudaFuncSetAttribute(route_kernel<kGating, kDispatch>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               100);
     if (err != cudaSuccess) return err;
     attr_set = true;
   }
-  route_kernel<<<1 + zero_blocks, kRouteThreads, smem, stream>>>(a);
+  route_kernel<kGating, kDispatch><<<1, kRouteThreads, smem, stream>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_route(const RouteArgs& a, int /*zero_blocks*/, cudaStream_t stream) {
+  const bool dispatch = a.forced_cfg < 0;
+  if (a.logits) return dispatch ? launch_route_t<true, true>(a, stream) : launch_route_t<true, false>(a, stream);
+  return dispatch ? launch_route_t<false, true>(a, stream) : launch_route_t<false, false>(a, stream);
 }
 
 cudaError_t launch_align(const int32_t* ids, int64_t n, int E, int bm, int32_t* hist, int32_t* sorted_ids,
@@ -205,7 +172,7 @@ cudaError_t launch_align(const int32_t* ids, int64_t n, int E, int bm, int32_t* 
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t err = cudaFuncSetAttribute(align_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)route_smem_bytes(kMaxExperts, kIdCache));
+                                           (int)kRouteSmemLimit);
     if (err != cudaSuccess) return err;
     attr_set = true;
   }

@@ -19,6 +19,8 @@ constexpr int kMaxUbm = 128;
 constexpr int kIdCache = 16384;  // topk ids kept in shared memory between the two passes
 constexpr int kStageMax = 20480; // sorted ids staged in shared memory, then copied out coalesced
 constexpr int kAlignMaxBm = 128;
+constexpr int kCfgStageMax = 1024;      // configs whose static fields are staged in shared memory
+constexpr size_t kRouteSmemLimit = 220 * 1024;
 
 // Dynamic shared memory layout of the route block (sized by E and n).
 //   hist[E]       bincount
@@ -35,6 +37,9 @@ struct RouteSmem {
   int32_t* stage;
   int stage_cap;
   bool cached;
+  // dispatch table staged by cp.async at kernel entry (null: read from global)
+  double *ca, *cb, *cc, *cd, *clam;
+  int32_t *csk, *cubm_idx, *ctiles, *cubm;
 };
 
 __host__ __device__ inline int route_stage_cap(int E, int64_t n) {
@@ -42,12 +47,22 @@ __host__ __device__ inline int route_stage_cap(int E, int64_t n) {
   return static_cast<int>(want < kStageMax ? want : kStageMax);
 }
 
-__host__ __device__ inline size_t route_smem_bytes(int E, int64_t n) {
+__host__ __device__ inline size_t route_smem_base(int E, int64_t n) {
   const int64_t cache = n <= kIdCache ? n : 0;
   return sizeof(int32_t) * ((size_t)E * 34 + 1 + (size_t)cache + 4 + (size_t)route_stage_cap(E, n)) + 64;
 }
+__host__ __device__ inline size_t cfg_stage_bytes(int n_cfg) {
+  return (size_t)n_cfg * (5 * 8 + 3 * 4) + kMaxUbm * 4 + 16;
+}
+// Stage the table in shared memory when it is small enough and fits.
+__host__ __device__ inline bool route_cfg_staged(int E, int64_t n, int n_cfg) {
+  return n_cfg > 0 && n_cfg <= kCfgStageMax && route_smem_base(E, n) + cfg_stage_bytes(n_cfg) <= kRouteSmemLimit;
+}
+__host__ __device__ inline size_t route_smem_bytes(int E, int64_t n, int n_cfg = 0) {
+  return route_smem_base(E, n) + (route_cfg_staged(E, n, n_cfg) ? cfg_stage_bytes(n_cfg) : 0);
+}
 
-__device__ inline RouteSmem carve_route_smem(unsigned char* base, int E, int64_t n) {
+__device__ inline RouteSmem carve_route_smem(unsigned char* base, int E, int64_t n, int n_cfg = 0) {
   RouteSmem s;
   s.hist = reinterpret_cast<int32_t*>(base);
   s.off = s.hist + E;
@@ -57,7 +72,54 @@ __device__ inline RouteSmem carve_route_smem(unsigned char* base, int E, int64_t
   const uintptr_t st = reinterpret_cast<uintptr_t>(s.ids + (s.cached ? n : 0));
   s.stage = reinterpret_cast<int32_t*>((st + 15) & ~static_cast<uintptr_t>(15));
   s.stage_cap = route_stage_cap(E, n);
+  s.ca = s.cb = s.cc = s.cd = s.clam = nullptr;
+  s.csk = s.cubm_idx = s.ctiles = s.cubm = nullptr;
+  if (route_cfg_staged(E, n, n_cfg)) {
+    const uintptr_t c0 = (reinterpret_cast<uintptr_t>(s.stage + s.stage_cap) + 15) & ~static_cast<uintptr_t>(15);
+    s.ca = reinterpret_cast<double*>(c0);
+    s.cb = s.ca + n_cfg;
+    s.cc = s.cb + n_cfg;
+    s.cd = s.cc + n_cfg;
+    s.clam = s.cd + n_cfg;
+    s.csk = reinterpret_cast<int32_t*>(s.clam + n_cfg);
+    s.cubm_idx = s.csk + n_cfg;
+    s.ctiles = s.cubm_idx + n_cfg;
+    s.cubm = s.ctiles + n_cfg;
+  }
   return s;
+}
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Kernel entry: thread i copies config i's static fields (and warp u's lane 0
+// the distinct bm value u) into shared memory asynchronously -- no registers
+// stay live, and the global latency overlaps the histogram pass.
+__device__ inline void stage_table(const ramp_table_t& t, RouteSmem& s) {
+  if (!s.ca) return;
+  const int i = threadIdx.x;
+  if (i < t.n_cfg) {
+    cp_async8(s.ca + i, t.a + i);
+    cp_async8(s.cb + i, t.b + i);
+    cp_async8(s.cc + i, t.c + i);
+    cp_async8(s.cd + i, t.d + i);
+    if (t.lam) cp_async8(s.clam + i, t.lam + i);
+    cp_async4(s.csk + i, t.split_k + i);
+    cp_async4(s.cubm_idx + i, t.ubm_index + i);
+    cp_async4(s.ctiles + i, t.ntile ? t.ntile + i : t.ttn + i);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0 && w < t.n_ubm) cp_async4(s.cubm + w, t.ubm + w);
+  asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 // Lanes of the warp holding the same value e (e < 0 marks an empty lane):
@@ -209,35 +271,27 @@ __device__ inline bool argmin_better(const ArgMin& x, const ArgMin& y) {
   return x.i < y.i;
 }
 
-// Static fields of one config, loaded into registers at kernel entry so their
-// global-memory latency overlaps the histogram pass (the table is constant;
-// only g depends on the routing).
+// Static fields of one config (the table is constant; only g depends on the
+// routing): from the shared-memory stage when the kernel staged the table,
+// else straight from global memory.
 struct CfgRegs {
   long long stripes;  // work tiles per M-tile (ntile, or ceil(N/ttn))
   int sk, ubm_idx;
-  int ubm_w;          // distinct bm value number (warp index), for the M-tile counts
   double a, b, c, d, lam;
 };
 
-__device__ __forceinline__ CfgRegs load_cfg(const ramp_table_t& t, int i) {
+__device__ __forceinline__ CfgRegs load_cfg(const ramp_table_t& t, int i, const RouteSmem* s) {
   CfgRegs r;
-  r.sk = __ldg(t.split_k + i);
-  r.ubm_idx = __ldg(t.ubm_index + i);
-  r.stripes = t.ntile ? __ldg(t.ntile + i) : (static_cast<long long>(t.N) + __ldg(t.ttn + i) - 1) / __ldg(t.ttn + i);
-  r.a = __ldg(t.a + i);
-  r.b = __ldg(t.b + i);
-  r.c = __ldg(t.c + i);
-  r.d = __ldg(t.d + i);
-  r.lam = t.lam ? __ldg(t.lam + i) : 0.0;
-  return r;
-}
-
-// Config handled first by this thread (index threadIdx.x), prefetched.
-__device__ __forceinline__ CfgRegs dispatch_prefetch(const ramp_table_t& t) {
-  CfgRegs r{};
-  if (static_cast<int>(threadIdx.x) < t.n_cfg) r = load_cfg(t, threadIdx.x);
-  const int w = threadIdx.x >> 5;
-  r.ubm_w = w < t.n_ubm ? __ldg(t.ubm + w) : 1;
+  const bool st = s && s->ca && i < kCfgStageMax;
+  r.sk = st ? s->csk[i] : __ldg(t.split_k + i);
+  r.ubm_idx = st ? s->cubm_idx[i] : __ldg(t.ubm_index + i);
+  const int tl = st ? s->ctiles[i] : (t.ntile ? __ldg(t.ntile + i) : __ldg(t.ttn + i));
+  r.stripes = t.ntile ? tl : (static_cast<long long>(t.N) + tl - 1) / tl;
+  r.a = st ? s->ca[i] : __ldg(t.a + i);
+  r.b = st ? s->cb[i] : __ldg(t.b + i);
+  r.c = st ? s->cc[i] : __ldg(t.c + i);
+  r.d = st ? s->cd[i] : __ldg(t.d + i);
+  r.lam = t.lam ? (st ? s->clam[i] : __ldg(t.lam + i)) : 0.0;
   return r;
 }
 
@@ -245,8 +299,8 @@ __device__ __forceinline__ CfgRegs dispatch_prefetch(const ramp_table_t& t) {
 // returns (in every thread) the selected id.  fp64 arithmetic follows
 // predict_batch exactly: ((a + b*ceil(g/sm)) + c*g) + d*log(g+1)
 // (ramp/cost_model.py:104-114), gate (g/split_k)/sm < 0.2 (ramp/dispatch.py:107-114),
-// first argmin over +inf-masked predictions (:118-119).  `pre` holds the
-// prefetched fields of config threadIdx.x (dispatch_prefetch).
+// first argmin over +inf-masked predictions (:118-119).  With `rs` the
+// static config fields come from the kernel-entry shared-memory stage.
 //
 // Runs on warps [0, nwarps) of the block; with nwarps < blockDim/32 the group
 // synchronises on named barrier 3 only, so the other warps can walk the
@@ -260,7 +314,7 @@ __device__ __forceinline__ void group_sync(int nwarps) {
   }
 }
 
-__device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_table_t& t, const CfgRegs& pre,
+__device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_table_t& t, const RouteSmem* rs,
                                      int64_t* grid_out, double* pred_out, int* n_eval_out,
                                      int64_t* mt_smem /*[kMaxUbm]*/, ArgMin* red_smem /*[32]*/,
                                      int* cnt_smem /*[32]*/, unsigned long long* stamps = nullptr,
@@ -276,8 +330,10 @@ __device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_tabl
   };
   // M-tiles per distinct bm: sum over active experts of ceil(c_e / bm)
   // (m_tile_counts, ramp/routing.py:197-203).
+  if (rs && rs->ca) cp_async_wait_all();  // this thread's staged fields have landed
+  __syncwarp();
   for (int u = warp; u < t.n_ubm; u += nwarps) {
-    const int bm = u == warp ? pre.ubm_w : t.ubm[u];
+    const int bm = (rs && rs->ca && u == warp) ? rs->cubm[u] : t.ubm[u];
     long long acc = 0;
     for (int e = lane; e < E; e += 32) {
       const int c = hist[e];
@@ -306,7 +362,7 @@ __device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_tabl
   int kept = 0;
   const long long smi = t.sm_count;
   for (int i = threadIdx.x; i < t.n_cfg; i += nwarps * 32) {
-    const CfgRegs r = i == static_cast<int>(threadIdx.x) ? pre : load_cfg(t, i);
+    const CfgRegs r = load_cfg(t, i, rs);
     const int sk = r.sk;
     const long long stripes = r.stripes;
     const long long g = mt_smem[r.ubm_idx] * stripes * sk;

@@ -260,11 +260,42 @@ def test_b4_fit_recovers_planted_model():
     t = 20.0 + 3.0 * np.ceil(g / 148) + 0.05 * gl + 1.5 * np.log(gl + 1.0)
     samples = [ProfilingSample(config_id=0, S=8, beta_target=0.5, seed=i, g=int(g[i]), time_us=float(t[i]))
                for i in range(n)]
-    r = fit_b4(samples, B4Features(g=g, n_act=n_act, m_tiles=mt, jobs_per_mtile=jpm), hw)
-    c = r.coefficients
-    assert c.variant == "B4" and abs(c.lam - lam) < 1e-9
-    assert np.allclose([c.a, c.b, c.c, c.d], [20.0, 3.0, 0.05, 1.5], rtol=1e-6, atol=1e-6)
-    assert r.r_squared > 1 - 1e-9
+    feats = B4Features(g=g, n_act=n_act, m_tiles=mt, jobs_per_mtile=jpm)
+    for relative in (False, True):  # B4 and B4r recover an exact model alike
+        r = fit_b4(samples, feats, hw, relative=relative)
+        c = r.coefficients
+        assert c.variant == "B4" and abs(c.lam - lam) < 1e-9
+        assert np.allclose([c.a, c.b, c.c, c.d], [20.0, 3.0, 0.05, 1.5], rtol=1e-6, atol=1e-6)
+        assert r.r_squared > 1 - 1e-9
+
+
+def test_b4r_weights_relative_residuals():
+    """On data no model fits exactly, B4r trades absolute error on the long
+    points for relative error on the short ones."""
+    from paper_2604_26039_b200.config_space import HardwareModel
+    from paper_2604_26039_b200.cost_model import B4Features, ProfilingSample, fit_b4, traffic_grid
+
+    hw = HardwareModel.b200()
+    rng = np.random.default_rng(3)
+    n = 80
+    n_act = rng.integers(1, 65, n)
+    mt = n_act + rng.integers(0, 400, n)
+    jpm = 24
+    g = mt * jpm
+    t = 20.0 + 3.0 * np.ceil(g / 148) + 0.05 * traffic_grid(jpm, n_act, mt, 0.35) + 0.002 * g ** 1.3
+    samples = [ProfilingSample(config_id=0, S=8, beta_target=0.5, seed=i, g=int(g[i]), time_us=float(t[i]))
+               for i in range(n)]
+    feats = B4Features(g=g, n_act=n_act, m_tiles=mt, jobs_per_mtile=jpm)
+
+    def rel_err(rep):
+        c = rep.coefficients
+        gl = traffic_grid(jpm, n_act, mt, c.lam)
+        pred = c.a + c.b * np.ceil(g / 148) + c.c * gl + c.d * np.log(gl + 1.0)
+        return np.abs(pred / t - 1.0)
+
+    abs_fit, rel_fit = fit_b4(samples, feats, hw), fit_b4(samples, feats, hw, relative=True)
+    short = t < np.median(t)
+    assert np.mean(rel_err(rel_fit)[short] ** 2) <= np.mean(rel_err(abs_fit)[short] ** 2)
 
 
 def test_b4_coeff_store_round_trip_and_validation():
