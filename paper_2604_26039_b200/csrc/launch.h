@@ -41,8 +41,8 @@ struct RouteArgs {
   float* w_out;          // [S, top_k]
 };
 
-int pdl_mode();
-int64_t prefetch_cap();  // RAMP_PREFETCH_MB (default 0 = off; e.g. 64 enables the speculative weight prefetch)  // RAMP_PDL: 0 off, 1 trigger at route entry (default), 2 trigger at route exit
+int pdl_mode();          // RAMP_PDL: 0 off, 1 trigger at route entry (default), 2 trigger at route exit
+int64_t prefetch_cap();  // RAMP_PREFETCH_MB: speculative weight prefetch budget (default 0 = off)
 
 cudaError_t launch_route(const RouteArgs& a, int zero_blocks, cudaStream_t stream);
 cudaError_t launch_align(const int32_t* ids, int64_t n, int E, int bm, int32_t* hist, int32_t* sorted_ids,
