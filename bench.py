@@ -283,6 +283,66 @@ def fp8_leg(dev):
             "coeffs": path.name}
 
 
+# ------------------------------------------------------------------ Mixtral leg
+MIX_MODEL = "Mixtral-8x7B"
+MIX_POINTS = ((64, 1.0), (512, 1.0), (512, 0.5))
+
+
+def mixtral_leg(dev):
+    """BASELINE configs[3]: Mixtral-8x7B MoE layer (E=8, top-2, d=4096,
+    d_ff=14336), BF16, the large-K regime.  No fitted table ships for this
+    geometry (a full profiling sweep of 614 configs at ~0.5 ms per call is a
+    separate offline job), so this leg is a bounded exhaustive search over the
+    large-tile split-mode candidates (bm 16..128, ttn 256/512, split-K 1/4)
+    and reports the best config per point with and without split-K.  Untimed
+    by the step contract; reported as a side object of the line."""
+    import torch
+
+    from paper_2604_26039_b200.catalog import BASELINE_MODELS
+    from paper_2604_26039_b200.config_space import HardwareModel, enumerate_b200_configs
+    from paper_2604_26039_b200.dispatch import EVAL_HIST_DOMAIN, derive_seed
+    from paper_2604_26039_b200.moe import DeviceTable
+    from paper_2604_26039_b200.routing import sample_histogram
+    from paper_2604_26039_b200.sweep import MeasuredTimer, make_inputs
+
+    geom = BASELINE_MODELS[MIX_MODEL]
+    pool = enumerate_b200_configs(geom, HardwareModel.b200())
+    cols = pool.columns()
+    n = len(pool)
+    best_stg: dict = {}
+    for c in pool:
+        if c.mode == 1 and not c.group_m and c.kps == 1 and c.bm >= 16 and c.ttn >= 256:
+            key = (c.bm, c.ttn, c.split_k)
+            if key not in best_stg or c.stg > pool.by_id(best_stg[key]).stg:
+                best_stg[key] = c.id
+    cand = sorted(best_stg.values())
+    flat = DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
+                       group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], kps=cols["kps"], a=np.ones(n),
+                       b=np.zeros(n), c=np.zeros(n), d=np.zeros(n), N=geom.N, kappa_ok=True, sm_count=148,
+                       device=dev)
+    timer = MeasuredTimer(geom, flat, iters=3, device=dev)
+    H, I = geom.K, geom.N // 2
+    rows = []
+    for S, beta in MIX_POINTS:
+        hs = derive_seed(42, EVAL_HIST_DOMAIN, S, round(beta * 1000), 0)
+        hist = sample_histogram(geom.E, S, geom.top_k, beta, hs).histogram
+        x, ids, w = make_inputs(geom, hist, hs, dev)
+        t = timer.time_configs(x, ids, w, cand)
+        i = int(np.argmin(t))
+        c = pool.by_id(cand[i])
+        no_sk = min(tt for tt, cid in zip(t, cand) if pool.by_id(cid).split_k == 1)
+        nbytes = hist.active_experts * 3 * H * I * 2 + S * H * 4
+        rows.append({"S": S, "beta": beta, "active": hist.active_experts, "us": round(float(t[i]), 2),
+                     "tflops": round(6 * S * geom.top_k * H * I / t[i] / 1e6, 2), "gbs": round(nbytes / t[i] / 1e3, 1),
+                     "best_without_split_k_us": round(float(no_sk), 2),
+                     "cfg": {"id": c.id, "bm": c.bm, "ttn": c.ttn, "stg": c.stg, "split_k": c.split_k}})
+    del timer
+    torch.cuda.empty_cache()
+    return {"workload": f"{MIX_MODEL} MoE layer (E=8, top-2, d=4096, d_ff=14336) BF16, large-K regime",
+            "method": f"exhaustive search over {len(cand)} large-tile split-mode candidates per point "
+                      "(L2 flushed before each timed replay)", "points": rows}
+
+
 # ------------------------------------------------------------------ EP leg
 EP_MODEL = "DeepSeek-V3"
 EP_LOCAL = "DeepSeek-V3-EP8"
@@ -618,6 +678,13 @@ def ours(args, geom):
         cpu = {"value": f / t / 1e12, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
                "sample": f"first {n} of {len(pts)} sweep points (fp32 numpy oracle, oracle/moe_ref.py)"}
 
+    mix = None
+    if not args.no_mixtral:
+        try:
+            mix = mixtral_leg(dev)
+        except Exception as exc:  # noqa: BLE001 - reported in the line, never fatal for the main metric
+            mix = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     fp8 = None
     if not args.no_fp8:
         try:
@@ -658,6 +725,7 @@ def ours(args, geom):
         "dispatch": ra,
         "per_point": per_point,
         "fp8": fp8,
+        "mixtral": mix,
         "ep": ep_res,
     }
     print(json.dumps(line), flush=True)
@@ -675,6 +743,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     ap.add_argument("--no-fp8", action="store_true", help="skip the Qwen3 FP8 side measurement")
     ap.add_argument("--no-ep", action="store_true", help="skip the DeepSeek-V3 expert-parallel side measurement")
+    ap.add_argument("--no-mixtral", action="store_true", help="skip the Mixtral large-K side measurement")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

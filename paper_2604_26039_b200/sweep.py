@@ -123,6 +123,17 @@ class MeasuredTimer:
             res[n] = float(ts[trim:len(ts) - trim].mean())
         return res
 
+    def confirm(self, pool: ConfigPool, hist: ExpertHistogram, point_seed: int, config_ids, factor: int = 4):
+        """Re-time a few configs side by side with `factor` x the replays
+        (the regret harness's winner's-curse correction)."""
+        x, ids, w = make_inputs(self.geom, hist, point_seed, self.device)
+        iters = self.iters
+        self.iters = iters * factor
+        try:
+            return self.time_configs(x, ids, w, list(config_ids))
+        finally:
+            self.iters = iters
+
     def pool_times(self, pool: ConfigPool, hist: ExpertHistogram, point_seed: int, shared_noise: bool = False,
                    grids=None) -> np.ndarray:
         key = (hist.counts, point_seed, len(pool), self.iters)
