@@ -26,7 +26,7 @@ int cuda_fail(cudaError_t err, const char* where) {
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct WorkspaceLayout {
-  size_t ctrl, hist, sorted, tiles, done, acc, xs, act, acc_a, split_cnt, xq, xsf, actq, actsf, total;
+  size_t ctrl, hist, sorted, tiles, done, acc, xs, act, acc_a, split_cnt, xq, xsf, actq, actsf, route, total;
   int64_t capacity, rows;
 };
 
@@ -60,6 +60,7 @@ WorkspaceLayout layout_for(int32_t S, int32_t H, int32_t I, int32_t E, int32_t t
   w.xsf = take((size_t)mt_max * (H / 128 + 1) * 512);
   w.actq = take((size_t)w.rows * I);
   w.actsf = take((size_t)mt_max * (I / 128 + 1) * 512);
+  w.route = take(sizeof(int32_t) * 2 * (size_t)E);  // inline route: histogram + placement cursors
   w.total = off;
   return w;
 }
@@ -205,7 +206,11 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   // route kernel, which publishes the histogram early
   // (decode sizes only: at prefill sizes the prefetch competes with the token
   // gather for HBM and costs more than it hides, measured at S*k = 4096)
-  const bool prefetch = !fp8 && (phases & 1) && ramp::prefetch_cap() > 0 && (int64_t)S * top_k <= 256;
+  // The BF16 layer routes inside the megakernel (one launch); the FP8 path,
+  // router fusion and split-phase calls keep the separate route kernel.
+  const bool inline_route = !fp8 && !logits && phases == 3 && ramp::inline_route_enabled();
+  const bool prefetch = !inline_route && !fp8 && (phases & 1) && ramp::prefetch_cap() > 0 &&
+                        (int64_t)S * top_k <= 256;
   ra.publish_hist = prefetch ? 1 : 0;
   ra.logits = logits;
   ra.logits_bf16 = logits_bf16;
@@ -213,7 +218,7 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   ra.w_out = w_out;
   const int zero_blocks = 0;
   cudaError_t err = cudaSuccess;
-  if (phases & 1) {
+  if ((phases & 1) && !inline_route) {
     err = ramp::launch_route(ra, zero_blocks, st);
     if (err != cudaSuccess) return cuda_fail(err, "route kernel");
   }
@@ -252,6 +257,15 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   ml.hist = ra.hist_out;
   ml.pf_flag = ra.ctrl + 11;
   ml.pf_cap = prefetch ? ramp::prefetch_cap() : 0;
+  ml.inline_route = inline_route;
+  ml.forced_cfg = forced_cfg;
+  ml.topk_ids = topk_ids;
+  ml.tot = reinterpret_cast<int32_t*>(ws + L.route);
+  ml.cursor = ml.tot + E;
+  ml.gflag = ra.ctrl + 12;
+  ml.gcnt = ra.ctrl + 13;
+  ml.sel_out = sel_out;
+  ml.hist_out = ra.hist_out;
   const char* why = nullptr;
   err = ramp::launch_fused_moe(ml, st, &why);
   if (err != cudaSuccess) return why ? fail(RAMP_ECUDA, why) : cuda_fail(err, "fused_moe kernel");

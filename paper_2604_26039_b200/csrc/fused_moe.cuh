@@ -35,13 +35,14 @@
 #include <cstdint>
 
 #include "../../include/ramp_b200.h"
+#include "inline_route.cuh"
 #include "launch.h"
 #include "ptx.cuh"
 
 namespace ramp {
 
 constexpr int kMoeThreads = 256;
-constexpr int kCtrlBytes = 4096;                  // barriers + per-job metadata
+constexpr int kCtrlBytes = 6144;                  // barriers + per-job metadata + route offsets
 constexpr int kStageBytesScatter = 16 * 128 * 4;  // 16 tokens x 128 rows fp32 transpose buffer
 constexpr int kSubTileBytes = 128 * 128;          // 128 rows x 64 bf16 (one SW128 box)
 constexpr int kMaxStages = 12;
@@ -126,6 +127,17 @@ struct MoeParams {
   const void* w2_base;
   int32_t* pf_flag;            // raised by the route kernel, cleared at the end of this kernel
   int64_t pf_cap;              // bytes to prefetch at most (0: off)
+  // Inline route (inline_route.cuh): this kernel computes the histogram,
+  // dispatch and placement itself (no route kernel before it).
+  int32_t inline_route;
+  int32_t forced_cfg;
+  const int32_t* topk_ids;     // [n_assign]
+  int32_t* tot;                // [E] global histogram (cleared at the end of the call)
+  int32_t* cursor;             // [E] per-expert placement cursors (cleared at the end)
+  int32_t* gflag;              // generation flag of the grid barriers (monotonic)
+  int32_t* gcnt;               // [3] arrival counters: route A, gather C, end
+  int32_t* sel_out;            // optional [4]
+  int32_t* hist_out;           // optional [E]
 };
 constexpr int64_t kPrefetchCap = 64ll << 20;  // half the 126 MB L2
 // jobs logged per CTA: {job id, claimed, loads issued, epilogue done} (ns);
@@ -168,6 +180,8 @@ struct CtrlSmem {
   int32_t epi_tok[128];
   float epi_w[128];
   int16_t pf_act[512];  // active experts of the speculative prefetch (E <= 512)
+  int32_t r_off[kMaxExperts + 1];  // inline route: bm-padded expert offsets (M-tile -> expert)
+  int32_t r_cfg, r_npp, r_neval;
 };
 static_assert(sizeof(CtrlSmem) <= kCtrlBytes, "control block overflow");
 
@@ -326,12 +340,46 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       }
     }
   }
-  pdl_wait();  // the route kernel's selection, alignment and gathered rows are now visible
+  // Generation of this call's grid barriers (inline route); read before any
+  // CTA can arrive anywhere, so every CTA sees the same value.
+  const int g0 = p.inline_route ? ld_acquire_gpu(p.gflag) : 0;
+  int cfg, n_post_pad;
+  if (!kFp8 && p.inline_route) {
+    const InlineRouteResult rr = inline_route<kMoeThreads>(
+        p.topk_ids, p.n_assign, p.E, p.top_k, p.forced_cfg, p.table, p.x, p.x_sorted, p.H,
+        const_cast<int32_t*>(p.sorted_ids), p.tot, p.cursor, p.gcnt, p.gcnt + 1, p.gflag, g0,
+        const_cast<int32_t*>(p.ctrl) + 4, *reinterpret_cast<InlineRouteScratch*>(base + kCtrlBytes + kStageBytesScatter),
+        cs.r_off);
+    cfg = rr.cfg;
+    n_post_pad = rr.n_post_pad;
+    if (threadIdx.x == 0) {
+      gen_arrive(p.gcnt + 1, p.gflag, g0 + 2);  // rows gathered (the producers wait on it)
+      if (blockIdx.x == 0) {
+        int32_t* ctrl = const_cast<int32_t*>(p.ctrl);
+        ctrl[0] = cfg;
+        ctrl[1] = n_post_pad;
+        ctrl[2] = n_post_pad / p.table.bm[cfg];
+        ctrl[3] = rr.n_eval;
+        if (p.sel_out) {
+          p.sel_out[0] = cfg;
+          p.sel_out[1] = n_post_pad;
+          p.sel_out[2] = n_post_pad / p.table.bm[cfg];
+          p.sel_out[3] = rr.n_eval;
+        }
+      }
+    }
+    if (blockIdx.x == 0 && p.hist_out)
+      for (int e = threadIdx.x; e < p.E; e += blockDim.x)
+        p.hist_out[e] = reinterpret_cast<InlineRouteScratch*>(base + kCtrlBytes + kStageBytesScatter)->tot[e];
+    __syncthreads();  // the scratch (in the ring) is dead from here on
+  } else {
+    pdl_wait();  // the route kernel's selection, alignment and gathered rows are now visible
+    cfg = p.ctrl[0];
+    n_post_pad = p.ctrl[1];
+  }
   if (ts && threadIdx.x == 0) ts[kTsStart] = globaltimer();
 
   // --- runtime tile config chosen by the dispatcher (no host round trip)
-  const int cfg = p.ctrl[0];
-  const int n_post_pad = p.ctrl[1];
   const int stg = p.table.stg[cfg];
   Geometry G;
   G.mode = p.table.mode ? p.table.mode[cfg] : kModeFused;
@@ -373,7 +421,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   // Token blocks of <= 16 rows skip phase 0: their producer gathers the rows
   // straight from x with TMA gather4 (4 rows per instruction), so decode-size
   // calls need no grid barrier before the first MMA.
-  const bool direct_x = !kFp8 && bmN == 16;
+  const bool direct_x = !kFp8 && bmN == 16 && !p.inline_route;
   if (kFp8 && warp >= 2) {
     // FP8: gather + quantise every row to MXFP8 (per-32 power-of-two scales)
     // into x_q and the per-M-tile scale atoms x_sf.
@@ -420,7 +468,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     named_bar_sync(2, 32 * kGatherWarps);
     if (warp == 2 && lane == 0) atomicAdd(p.gbar, 1);
   }
-  if (!kFp8 && warp >= 2 && !direct_x) {
+  if (!kFp8 && warp >= 2 && !direct_x && !p.inline_route) {
     constexpr int kGatherWarps = 6, kUnroll = 8;
     const int row_vec = p.H / 8;  // 16-byte vectors per row
     const int gw = blockIdx.x * kGatherWarps + (warp - 2), nw = gridDim.x * kGatherWarps;
@@ -538,7 +586,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       }
 #endif
       const Job jb = G.job(j);
-      const int e = warp_uniform(p.tile_expert[jb.m]);
+      const int e = warp_uniform(p.inline_route ? tile_expert_of(cs.r_off, p.E, G.bm, jb.m) : p.tile_expert[jb.m]);
       const int row0 = jb.m * G.bm;
       if (jb.kind == 0) {
         const uint32_t tx1 = u_kps * (nA * kSubTileBytes + bmN * 128) + (kFp8 ? (nA + 1) * 512 : 0);
@@ -597,7 +645,11 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             ++npend;
             if (npend == u_stg || kb + u_kps >= kb1) {
               pc.lap();
-              while (ld_acquire_gpu(p.gbar) < (int)gridDim.x) __nanosleep(32);
+              if (p.inline_route) {
+                gen_wait(p.gflag, g0 + 2);
+              } else {
+                while (ld_acquire_gpu(p.gbar) < (int)gridDim.x) __nanosleep(32);
+              }
               fence_proxy_async_global();
               c_dep += pc.lap();
               gathered = true;
@@ -1140,8 +1192,15 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
   if (threadIdx.x == 0) {
     if (ts) ts[kTsEndArrive] = globaltimer();
-    atomicAdd(p.gbar + 1, 1);
-    while (ld_acquire_gpu(p.gbar + 1) < (int)gridDim.x) __nanosleep(64);
+    if (p.inline_route) {
+      gen_arrive(p.gcnt + 2, p.gflag, g0 + 3);
+      gen_wait(p.gflag, g0 + 3);
+      // every CTA is done with this call's jobs: clear the per-call state
+      if (blockIdx.x == 0) atomicExch(p.job_counter, 0);
+    } else {
+      atomicAdd(p.gbar + 1, 1);
+      while (ld_acquire_gpu(p.gbar + 1) < (int)gridDim.x) __nanosleep(64);
+    }
     // every CTA is past its prologue: re-arm the prefetch flag for the next call
     if (blockIdx.x == 0 && p.pf_flag) *p.pf_flag = 0;
     if (ts) ts[kTsEndPass] = globaltimer();
@@ -1162,6 +1221,14 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       o2[i] = pk;
       a4[i] = z;
     }
+  }
+  if (p.inline_route) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < p.E; e += gridDim.x * blockDim.x) {
+      p.tot[e] = 0;
+      p.cursor[e] = 0;
+    }
+    const int n_mt = n_post_pad / G.bm;
+    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < n_mt; m += gridDim.x * blockDim.x) p.done[m] = 0;
   }
   if (ts && threadIdx.x == 0) ts[kTsFinal] = globaltimer();
 }

@@ -80,7 +80,19 @@ struct MoeLaunch {
   const int32_t* hist;  // speculative prefetch: published histogram, flag, byte cap (0 = off)
   int32_t* pf_flag;
   int64_t pf_cap;
+  // inline route (the megakernel routes itself; no route kernel, no PDL)
+  bool inline_route;
+  int32_t forced_cfg;
+  const int32_t* topk_ids;
+  int32_t* tot;
+  int32_t* cursor;
+  int32_t* gflag;
+  int32_t* gcnt;
+  int32_t* sel_out;
+  int32_t* hist_out;
 };
+
+bool inline_route_enabled();  // RAMP_INLINE_ROUTE (default 0: the separate route kernel measured faster)
 
 extern unsigned long long* g_prof_buffer;  // diagnostics, see ramp_set_profile_buffer
 

@@ -21,6 +21,14 @@ int64_t prefetch_cap() {
   return cap;
 }
 
+bool inline_route_enabled() {
+  static bool on = [] {
+    const char* v = getenv("RAMP_INLINE_ROUTE");
+    return v ? atoi(v) != 0 : false;
+  }();
+  return on;
+}
+
 int pdl_mode() {
   static int mode = [] {
     const char* v = getenv("RAMP_PDL");
@@ -224,6 +232,15 @@ cudaError_t launch_fused_moe(const MoeLaunch& l, cudaStream_t stream, const char
   p.w2_base = l.w2;
   p.pf_flag = l.pf_flag;
   p.pf_cap = l.pf_cap;
+  p.inline_route = l.inline_route ? 1 : 0;
+  p.forced_cfg = l.forced_cfg;
+  p.topk_ids = l.topk_ids;
+  p.tot = l.tot;
+  p.cursor = l.cursor;
+  p.gflag = l.gflag;
+  p.gcnt = l.gcnt;
+  p.sel_out = l.sel_out;
+  p.hist_out = l.hist_out;
   // Programmatic dependent launch: the megakernel's prologue (barrier init,
   // TMEM allocation, descriptor prefetch) may overlap the route kernel's tail.
   cudaLaunchAttribute pdl[1];
@@ -235,7 +252,8 @@ cudaError_t launch_fused_moe(const MoeLaunch& l, cudaStream_t stream, const char
   cfg.dynamicSmemBytes = kSmemLimit;
   cfg.stream = stream;
   cfg.attrs = pdl;
-  cfg.numAttrs = pdl_mode() ? 1 : 0;
+  // the inline route has no primary kernel to overlap with
+  cfg.numAttrs = (pdl_mode() && !l.inline_route) ? 1 : 0;
   err = l.fp8 ? cudaLaunchKernelEx(&cfg, fused_moe_kernel<true>, maps, p)
               : cudaLaunchKernelEx(&cfg, fused_moe_kernel<false>, maps, p);
   if (err != cudaSuccess) return err;

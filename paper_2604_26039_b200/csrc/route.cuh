@@ -343,18 +343,20 @@ __device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_tabl
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) mt_smem[u] = acc;
   }
-  // Active experts (only the B4 traffic grid needs them).
-  __shared__ int s_nact;
+  // Active experts (only the B4 traffic grid needs them); parked in
+  // red_smem[31] (no static shared memory: the megakernel embeds this code
+  // and its dynamic allocation is already at the opt-in maximum).
   if (t.lam && warp == nwarps - 1) {
     int na = 0;
     for (int e = lane; e < E; e += 32) na += hist[e] > 0 ? 1 : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) na += __shfl_xor_sync(0xffffffffu, na, o);
-    if (lane == 0) s_nact = na;
+    if (lane == 0) red_smem[31].i = na;
   }
   group_sync(nwarps);
   stamp(12);
-  const double nact = t.lam ? static_cast<double>(s_nact) : 0.0;
+  const double nact = t.lam ? static_cast<double>(red_smem[31].i) : 0.0;
+  group_sync(nwarps);  // everyone has read it before red_smem is reused below
 
   const double sm = static_cast<double>(t.sm_count);
   const double omega_max = t.omega_max > 0.0 ? t.omega_max : 0.2;
