@@ -224,7 +224,7 @@ def fp8_leg(dev):
     from paper_2604_26039_b200 import moe
     from paper_2604_26039_b200.catalog import BASELINE_MODELS
     from paper_2604_26039_b200.config_space import HardwareModel, enumerate_b200_configs
-    from paper_2604_26039_b200.cost_model import parse_coeff_store, read_coeff_store
+    from paper_2604_26039_b200.cost_model import active_ids_of, parse_coeff_store, read_coeff_store
     from paper_2604_26039_b200.dispatch import EVAL_HIST_DOMAIN, DispatchTable, derive_seed
     from paper_2604_26039_b200.routing import BetaUnreachableError, sample_histogram
     from paper_2604_26039_b200.sweep import make_fp8_weights, make_inputs
@@ -234,8 +234,10 @@ def fp8_leg(dev):
     if not path.exists():
         return {"skipped": f"{path.name} missing (scripts/profile_b200.py --model {FP8_MODEL} --dtype fp8)"}
     pool = enumerate_b200_configs(geom, HardwareModel.b200(), dtype="fp8")
-    _, sm, co = parse_coeff_store(read_coeff_store(path))
-    dtab = DispatchTable(model=FP8_MODEL, pool=pool, coefficients=co, sm_count=sm).device_table(device=dev)
+    store = read_coeff_store(path)
+    _, sm, co = parse_coeff_store(store)
+    dtab = DispatchTable(model=FP8_MODEL, pool=pool, coefficients=co, sm_count=sm,
+                         active=active_ids_of(store)).device_table(device=dev)
     copies = [make_fp8_weights(geom, seed=100 + c, device=dev) for c in range(FP8_COPIES)]
     H, I, E, k = geom.K, geom.N // 2, geom.E, geom.top_k
     side = torch.cuda.Stream(device=dev)
@@ -270,7 +272,7 @@ def fp8_leg(dev):
             us = float(np.median(ts[FP8_COPIES:]))
             a = hist.active_experts
             nbytes = a * 3 * H * I * (1 + 1 / 32) + S * H * 4 + 8 * S * k
-            c = pool.by_id(int(ws.sel[0].item()))
+            c = pool.by_id(dtab.pool_id(int(ws.sel[0].item())))
             rows.append({"S": S, "beta": beta, "active": a, "us": round(us, 2),
                          "tflops": round(6 * S * k * H * I / us / 1e6, 2), "gbs": round(nbytes / us / 1e3, 1),
                          "cfg": {"id": c.id, "bm": c.bm, "ttn": c.ttn, "stg": c.stg, "group_m": int(c.group_m)}})
@@ -363,7 +365,7 @@ def ep_leg(dev, world, rank, iters=10, warmup=3):
     from paper_2604_26039_b200 import ep
     from paper_2604_26039_b200.catalog import BASELINE_MODELS, MoeGeometry
     from paper_2604_26039_b200.config_space import HardwareModel, enumerate_b200_configs
-    from paper_2604_26039_b200.cost_model import parse_coeff_store, read_coeff_store
+    from paper_2604_26039_b200.cost_model import active_ids_of, parse_coeff_store, read_coeff_store
     from paper_2604_26039_b200.dispatch import DispatchTable, derive_seed
     from paper_2604_26039_b200.routing import sample_histogram
     from paper_2604_26039_b200.sweep import make_fp8_weights, make_inputs
@@ -379,8 +381,10 @@ def ep_leg(dev, world, rank, iters=10, warmup=3):
     per = geom.E // world
     lgeom = MoeGeometry(name=f"{EP_MODEL}-EP{world}", E=per, N=geom.N, K=geom.K, top_k=geom.top_k)
     pool = enumerate_b200_configs(lgeom, HardwareModel.b200(), dtype="fp8")
-    _, sm, co = parse_coeff_store(read_coeff_store(path))
-    dtab = DispatchTable(model=lgeom.name, pool=pool, coefficients=co, sm_count=sm).device_table(device=dev)
+    store = read_coeff_store(path)
+    _, sm, co = parse_coeff_store(store)
+    dtab = DispatchTable(model=lgeom.name, pool=pool, coefficients=co, sm_count=sm,
+                         active=active_ids_of(store)).device_table(device=dev)
     weights = make_fp8_weights(lgeom, seed=1000 + rank, device=dev)
     hs = derive_seed(42, 9, EP_TOKENS, round(EP_BETA * 1000), rank)
     hist = sample_histogram(geom.E, EP_TOKENS, geom.top_k, EP_BETA, hs).histogram
@@ -430,14 +434,16 @@ def ep_leg(dev, world, rank, iters=10, warmup=3):
 
 # ------------------------------------------------------------------ GPU arm
 def load_table(geom, pool, hw):
-    from paper_2604_26039_b200.cost_model import parse_coeff_store, read_coeff_store
+    from paper_2604_26039_b200.cost_model import active_ids_of, parse_coeff_store, read_coeff_store
     from paper_2604_26039_b200.dispatch import DispatchTable
 
     path = ROOT / "paper_2604_26039_b200" / "data" / f"coeffs_{MODEL}_b200.json"
     if not path.exists():
         raise SystemExit(f"{path} missing: run scripts/profile_b200.py on a B200 first")
-    _, sm, coeffs = parse_coeff_store(read_coeff_store(path))
-    return DispatchTable(model=MODEL, pool=pool, coefficients=coeffs, sm_count=sm), path
+    store = read_coeff_store(path)
+    _, sm, coeffs = parse_coeff_store(store)
+    return DispatchTable(model=MODEL, pool=pool, coefficients=coeffs, sm_count=sm,
+                         active=active_ids_of(store)), path
 
 
 def _ensure_single_pg() -> bool:
@@ -579,7 +585,7 @@ def ours(args, geom):
             torch.cuda.synchronize()
             lat.append(a0.elapsed_time(a1) * 1e3)
             k3.append(b0.elapsed_time(b1) * 1e3)
-        cfg = int(wss[p].sel[0].item())
+        cfg = dtab.pool_id(int(wss[p].sel[0].item()))
         us, k3us = float(np.median(lat)), float(np.median(k3))
         nbytes = layer_bytes(geom, pt["hist"], pt["S"])
         k3_bytes += nbytes

@@ -42,7 +42,7 @@
 namespace ramp {
 
 constexpr int kMoeThreads = 256;
-constexpr int kCtrlBytes = 6144;                  // barriers + per-job metadata + route offsets
+constexpr int kCtrlBytes = 4096;                  // barriers + per-job metadata
 constexpr int kStageBytesScatter = 16 * 128 * 4;  // 16 tokens x 128 rows fp32 transpose buffer
 constexpr int kSubTileBytes = 128 * 128;          // 128 rows x 64 bf16 (one SW128 box)
 constexpr int kMaxStages = 12;
@@ -180,8 +180,6 @@ struct CtrlSmem {
   int32_t epi_tok[128];
   float epi_w[128];
   int16_t pf_act[512];  // active experts of the speculative prefetch (E <= 512)
-  int32_t r_off[kMaxExperts + 1];  // inline route: bm-padded expert offsets (M-tile -> expert)
-  int32_t r_cfg, r_npp, r_neval;
 };
 static_assert(sizeof(CtrlSmem) <= kCtrlBytes, "control block overflow");
 
@@ -348,8 +346,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     const InlineRouteResult rr = inline_route<kMoeThreads>(
         p.topk_ids, p.n_assign, p.E, p.top_k, p.forced_cfg, p.table, p.x, p.x_sorted, p.H,
         const_cast<int32_t*>(p.sorted_ids), p.tot, p.cursor, p.gcnt, p.gcnt + 1, p.gflag, g0,
-        const_cast<int32_t*>(p.ctrl) + 4, *reinterpret_cast<InlineRouteScratch*>(base + kCtrlBytes + kStageBytesScatter),
-        cs.r_off);
+        const_cast<int32_t*>(p.ctrl) + 4, const_cast<int32_t*>(p.tile_expert),
+        *reinterpret_cast<InlineRouteScratch*>(base + kCtrlBytes + kStageBytesScatter));
     cfg = rr.cfg;
     n_post_pad = rr.n_post_pad;
     if (threadIdx.x == 0) {
@@ -586,7 +584,14 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       }
 #endif
       const Job jb = G.job(j);
-      const int e = warp_uniform(p.inline_route ? tile_expert_of(cs.r_off, p.E, G.bm, jb.m) : p.tile_expert[jb.m]);
+      if (p.inline_route && !gathered) {
+        // inline route: the M-tile -> expert map is written by the owner CTAs
+        // before barrier C (weights cannot stream ahead of it in this mode)
+        gen_wait(p.gflag, g0 + 2);
+        fence_proxy_async_global();
+        gathered = true;
+      }
+      const int e = warp_uniform(p.tile_expert[jb.m]);
       const int row0 = jb.m * G.bm;
       if (jb.kind == 0) {
         const uint32_t tx1 = u_kps * (nA * kSubTileBytes + bmN * 128) + (kFp8 ? (nA + 1) * 512 : 0);

@@ -11,9 +11,9 @@
 //   step 3  CTA b reserves a contiguous run inside each expert's segment for
 //           its slice (one global atomicAdd per (CTA, expert) on `cursor`),
 //           writes sorted_ids and copies the token rows into x_sorted; the
-//           owner CTA of expert e (e % grid) writes e's padding -> arrive on
-//           grid barrier C (the producers wait on it before loading tokens;
-//           weights stream right away)
+//           owner CTA of expert e (e % grid) writes e's padding and M-tile
+//           experts -> arrive on grid barrier C (the producers wait on it
+//           before their first job)
 //
 // Within an expert the order of assignments is by CTA arrival, not by flat
 // index: the layer's result does not depend on it (each token is one MMA
@@ -39,6 +39,7 @@ struct InlineRouteScratch {  // lives in the (not yet used) pipeline ring
   ArgMin red[32];
   int32_t cnt[32];
   int32_t warp_tot[32];
+  int32_t off[kMaxExperts + 1];  // bm-padded exclusive offsets
   int32_t bad;
 };
 
@@ -60,16 +61,16 @@ struct InlineRouteResult {
   int cfg, n_post_pad, n_eval;
 };
 
-// All threads of the CTA call it; `off` (E + 1 ints) must outlive the call
-// (the producer maps M-tiles to experts with it).  Returns the same result in
-// every thread of every CTA.
+// All threads of the CTA call it.  Returns the same result in every thread of
+// every CTA; tile_expert[] is written by the owner CTAs (visible after barrier C).
 template <int kThreads>
 __device__ inline InlineRouteResult inline_route(const int32_t* __restrict__ ids, int n, int E, int top_k,
                                                  int forced_cfg, const ramp_table_t& table,
                                                  const __nv_bfloat16* __restrict__ x, __nv_bfloat16* x_sorted, int H,
                                                  int32_t* __restrict__ sorted_ids, int* tot_g, int* cursor_g,
                                                  int* cnt_a, int* cnt_c, int* gflag, int g0, int* bad_flag,
-                                                 InlineRouteScratch& sc, int32_t* off) {
+                                                 int32_t* __restrict__ tile_expert, InlineRouteScratch& sc) {
+  int32_t* off = sc.off;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x, b = blockIdx.x;
   const int lo = static_cast<int>(static_cast<int64_t>(b) * n / G);
@@ -162,8 +163,10 @@ __device__ inline InlineRouteResult inline_route(const int32_t* __restrict__ ids
     int4* dst = dv + static_cast<int64_t>(pos) * row_vec;
     for (int c = lane; c < row_vec; c += 32) dst[c] = __ldg(src + c);
   }
-  // padding of the experts this CTA owns: sentinel ids and zero rows
+  // padding of the experts this CTA owns: sentinel ids and zero rows, and
+  // their M-tiles' expert
   for (int e = b; e < E; e += G) {
+    for (int t = off[e] / bm + tid; t < off[e + 1] / bm; t += kThreads) tile_expert[t] = e;
     const int start = off[e] + sc.tot[e], end = off[e + 1];
     for (int q = start + warp; q < end; q += kThreads / 32) {
       if (lane == 0) sorted_ids[q] = n;
@@ -174,19 +177,6 @@ __device__ inline InlineRouteResult inline_route(const int32_t* __restrict__ ids
   __threadfence();  // rows and ids are published by the caller's barrier-C arrival
   __syncthreads();
   return {sel, n_post_pad, n_eval};
-}
-
-// Expert of M-tile m: the e with off[e] <= m*bm < off[e+1] (binary search in
-// the shared-memory offsets; empty experts have off[e] == off[e+1]).
-__device__ __forceinline__ int tile_expert_of(const int32_t* off, int E, int bm, int m) {
-  const int row = m * bm;
-  int lo = 0, hi = E - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (off[mid] <= row) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
 }
 
 }  // namespace ramp

@@ -51,6 +51,7 @@ class DeviceTable:
     omega_max: float = 0.0            # split-K gate threshold (<= 0: the reference's 0.2)
     lam: np.ndarray | None = None     # B4 L2-reuse factor per config (None: the reference model)
     kps: np.ndarray | None = None     # k-blocks per pipeline stage per config (None: 1)
+    id_map: np.ndarray | None = None  # table index -> pool id (a pruned table); None: identity
     _tensors: dict = field(default_factory=dict, repr=False)
     struct: _lib.RampTable | None = field(default=None, repr=False)
 
@@ -106,6 +107,19 @@ class DeviceTable:
 
     def __len__(self) -> int:
         return len(self.bm)
+
+    def pool_id(self, index: int) -> int:
+        """Pool id of table entry `index` (what the device reports in sel)."""
+        return int(index) if self.id_map is None else int(self.id_map[int(index)])
+
+    def table_index(self, pool_id: int) -> int:
+        """Table entry of a pool id (forced configs); -1 stays -1."""
+        if pool_id < 0 or self.id_map is None:
+            return int(pool_id)
+        hit = np.flatnonzero(np.asarray(self.id_map) == int(pool_id))
+        if len(hit) == 0:
+            raise ValueError(f"config {pool_id} is not a candidate of this (pruned) table")
+        return int(hit[0])
 
     @property
     def ref(self):
@@ -191,7 +205,7 @@ def fused_moe(
     _lib.check(
         lib.ramp_fused_moe_bf16_ex(
             hidden_states.data_ptr(), w1.data_ptr(), w2.data_ptr(), topk_weights.data_ptr(),
-            topk_ids.data_ptr(), S, H, I, E, k, table.ref, int(forced_cfg), out.data_ptr(),
+            topk_ids.data_ptr(), S, H, I, E, k, table.ref, table.table_index(int(forced_cfg)), out.data_ptr(),
             workspace.sel.data_ptr(), workspace.buf.data_ptr(), workspace.buf.numel(), int(phases), _stream(),
         )
     )
@@ -249,7 +263,7 @@ def fused_moe_gating(
         lib.ramp_fused_moe_gating_bf16(
             hidden_states.data_ptr(), w1.data_ptr(), w2.data_ptr(), gating_output.data_ptr(),
             int(gating_output.dtype == torch.bfloat16), int(bool(renormalize)), topk_w.data_ptr(),
-            topk_ids.data_ptr(), S, H, I, E, k, table.ref, int(forced_cfg), out.data_ptr(),
+            topk_ids.data_ptr(), S, H, I, E, k, table.ref, table.table_index(int(forced_cfg)), out.data_ptr(),
             workspace.sel.data_ptr(), workspace.buf.data_ptr(), workspace.buf.numel(), _stream(),
         )
     )
@@ -308,7 +322,7 @@ def fused_moe_fp8(
         lib.ramp_fused_moe_fp8(
             hidden_states.data_ptr(), weights.w1_q.data_ptr(), weights.w1_sf.data_ptr(), weights.w2_q.data_ptr(),
             weights.w2_sf.data_ptr(), topk_weights.data_ptr(), topk_ids.data_ptr(), S, H, I, E, k, table.ref,
-            int(forced_cfg), out.data_ptr(), workspace.sel.data_ptr(), workspace.buf.data_ptr(),
+            table.table_index(int(forced_cfg)), out.data_ptr(), workspace.sel.data_ptr(), workspace.buf.data_ptr(),
             workspace.buf.numel(), int(phases), _stream(),
         )
     )

@@ -36,7 +36,7 @@ sys.path.insert(0, str(ROOT))
 from paper_2604_26039_b200.catalog import BASELINE_MODELS  # noqa: E402
 from paper_2604_26039_b200.config_space import HardwareModel, enumerate_b200_configs  # noqa: E402
 from paper_2604_26039_b200.cost_model import (B200_BATCH_SIZES, b4_features, coeff_store_dict, fit, fit_b4, profiling_plan,  # noqa: E402
-                                              write_coeff_store)
+                                              useful_configs, write_coeff_store)
 from paper_2604_26039_b200.routing import sample_histogram  # noqa: E402
 from paper_2604_26039_b200.dispatch import DispatchTable, evaluate_regret, speedup_ra_vs_static  # noqa: E402
 from paper_2604_26039_b200.moe import DeviceTable  # noqa: E402
@@ -104,6 +104,9 @@ def main() -> None:
     ap.add_argument("--eval-iters", type=int, default=7)
     ap.add_argument("--dtype", default="bf16", choices=("bf16", "fp8"))
     ap.add_argument("--refit", action="store_true", help="reuse the existing trace (no profiling sweep)")
+    ap.add_argument("--prune-tol", type=float, default=0.05,
+                    help="keep as dispatch candidates only configs within this fraction of the best at some "
+                         "profiled point (0: keep all)")
     a = ap.parse_args()
     out = Path(a.out)
     out.mkdir(parents=True, exist_ok=True)
@@ -139,16 +142,21 @@ def main() -> None:
         by_cfg.setdefault(s.config_id, []).append(s)
     variant, validation = choose_variant(pool, trace, hw, geom)
     reports = _fit_all(pool, by_cfg, hw, variant, geom)
-    write_coeff_store(out / f"coeffs_{tag}.json", coeff_store_dict(a.model, hw.sm_count, reports))
+    store = coeff_store_dict(a.model, hw.sm_count, reports)
+    active = useful_configs(trace.samples, a.prune_tol) if a.prune_tol > 0 else None
+    if active is not None:
+        store["active_ids"] = list(active)
+    write_coeff_store(out / f"coeffs_{tag}.json", store)
     r2 = np.array([r.r_squared for r in reports.values()])
     summary = {"model": a.model, "pool": n, "plan_points": len(plan), "samples": len(trace.samples),
                "profile_s": round(t_prof, 1), "r2_median": float(np.median(r2)), "r2_min": float(r2.min()),
-               "variant": variant, "heldout_regret_by_variant": validation}
+               "variant": variant, "heldout_regret_by_variant": validation,
+               "active_configs": None if active is None else len(active), "prune_tol": a.prune_tol}
     print(json.dumps(summary), flush=True)
     if not a.skip_eval:
         table = DispatchTable(model=a.model, pool=pool,
                               coefficients={c: r.coefficients for c, r in reports.items()},
-                              sm_count=hw.sm_count)
+                              sm_count=hw.sm_count, active=active)
         t0 = time.time()
         timer = timer or make_timer()
         timer.iters = a.eval_iters

@@ -323,3 +323,44 @@ def test_shipped_olmoe_coeffs_load_into_the_table():
     path = Path(__file__).resolve().parents[1] / "paper_2604_26039_b200" / "data" / "coeffs_OLMoE-1B-7B_b200.json"
     _, sm, co = parse_coeff_store(read_coeff_store(path))
     DispatchTable(model=g.name, pool=pool, coefficients=co, sm_count=sm)
+
+
+def test_pruned_table_masks_and_maps_ids():
+    """DispatchTable(active=...): inactive configs are never selected on the
+    host, and the compacted device table maps its indices back to pool ids."""
+    from paper_2604_26039_b200.catalog import BASELINE_MODELS
+    from paper_2604_26039_b200.config_space import HardwareModel, enumerate_b200_configs
+    from paper_2604_26039_b200.cost_model import CostCoefficients, useful_configs
+    from paper_2604_26039_b200.dispatch import DispatchTable
+    from paper_2604_26039_b200.routing import sample_histogram
+
+    geom = BASELINE_MODELS["OLMoE-1B-7B"]
+    pool = enumerate_b200_configs(geom, HardwareModel.b200())
+    rng = np.random.default_rng(0)
+    co = {c.id: CostCoefficients(a=float(rng.uniform(10, 50)), b=float(rng.uniform(0, 5)), c=0.01, d=0.5,
+                                 uses_log=True, variant="P4") for c in pool}
+    full = DispatchTable(model="m", pool=pool, coefficients=co, sm_count=148)
+    hist = sample_histogram(geom.E, 64, geom.top_k, 0.5, 7).histogram
+    best = full.host_select(hist)
+    active = tuple(i for i in range(0, len(pool), 3) if i != best)
+    pruned = DispatchTable(model="m", pool=pool, coefficients=co, sm_count=148, active=active)
+    sel = pruned.host_select(hist)
+    assert sel in active and sel != best
+    p_full, p_pruned = full.host_predict(hist), pruned.host_predict(hist)
+    assert np.isinf(p_pruned[best]) and p_pruned[sel] == p_full[sel]
+    dt = pruned.device_table(device="cpu")
+    assert len(dt) == len(active)
+    assert [dt.pool_id(i) for i in range(len(dt))] == sorted(active)
+    assert dt.table_index(active[5]) == 5 and dt.table_index(-1) == -1
+    with pytest.raises(ValueError):
+        dt.table_index(best)
+    with pytest.raises(ValueError):
+        DispatchTable(model="m", pool=pool, coefficients=co, sm_count=148, active=(len(pool),))
+
+    class S:
+        def __init__(self, cid, t, seed):
+            self.config_id, self.time_us, self.S, self.beta_target, self.seed = cid, t, 8, 0.5, seed
+
+    samples = [S(0, 10.0, 1), S(1, 10.4, 1), S(2, 12.0, 1), S(0, 20.0, 2), S(2, 19.0, 2)]
+    assert useful_configs(samples, 0.05) == (0, 1, 2)
+    assert useful_configs(samples, 0.01) == (0, 2)
