@@ -471,7 +471,7 @@ def ours(args, geom):
 
     from paper_2604_26039_b200 import _lib, moe
     from paper_2604_26039_b200.config_space import HardwareModel, enumerate_b200_configs
-    from paper_2604_26039_b200.dispatch import evaluate_regret, speedup_ra_vs_static
+    from paper_2604_26039_b200.dispatch import DispatchTable, evaluate_regret, speedup_ra_vs_static
     from paper_2604_26039_b200.sweep import MeasuredTimer, make_inputs, make_weights
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -601,7 +601,10 @@ def ours(args, geom):
     # ---------------- routing-aware vs static and regret against an exhaustive on-GPU sweep
     ra = None
     if not args.no_sweep:
-        timer = MeasuredTimer(geom, dtab, w1=copies[0][0], w2=copies[0][1], iters=5, device=dev)
+        # the exhaustive sweep times every pool config, pruned or not
+        full_tab = DispatchTable(model=MODEL, pool=pool, coefficients=table.coefficients,
+                                 sm_count=table.sm_count).device_table(device=dev)
+        timer = MeasuredTimer(geom, full_tab, w1=copies[0][0], w2=copies[0][1], iters=5, device=dev)
         points = [(pt["S"], pt["beta"]) for pt in pts]
         spd = speedup_ra_vs_static(table, pool, geom, timer, points=points, seeds_per_point=1)
         reg = evaluate_regret(table, pool, geom, timer, test_points=points, seeds_per_point=1)

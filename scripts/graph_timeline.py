@@ -84,7 +84,7 @@ for spec, forced in [(p, int(f)) for p in a.points.split(",") for f in a.cfg.spl
 
     full, route, mega = graph(run), graph(lambda: run(1)), graph(lambda: run(2))
     t_full, t_route, t_mega = timeit(full), timeit(route), timeit(mega)
-    cfg = int(ws.sel[0].item())
+    cfg = dtab.pool_id(int(ws.sel[0].item()))
     c = pool.by_id(cfg)
     buf = torch.zeros(149 * 32 + 148 * 16 * 4, dtype=torch.int64, device=dev)
     lib.ramp_set_profile_buffer(buf.data_ptr())
