@@ -212,6 +212,8 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   const bool prefetch = !inline_route && !fp8 && (phases & 1) && ramp::prefetch_cap() > 0 &&
                         (int64_t)S * top_k <= 256;
   ra.publish_hist = prefetch ? 1 : 0;
+  // early hand-off route -> megakernel (both launched by this call)
+  ra.early_flag = (phases == 3 && !inline_route && ramp::early_handoff_enabled()) ? ra.ctrl + 10 : nullptr;
   ra.logits = logits;
   ra.logits_bf16 = logits_bf16;
   ra.renorm = renorm;
@@ -257,6 +259,7 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   ml.hist = ra.hist_out;
   ml.pf_flag = ra.ctrl + 11;
   ml.pf_cap = prefetch ? ramp::prefetch_cap() : 0;
+  ml.early_flag = ra.early_flag;
   ml.inline_route = inline_route;
   ml.forced_cfg = forced_cfg;
   ml.topk_ids = topk_ids;

@@ -126,6 +126,10 @@ struct MoeParams {
   const void* w1_base;         // raw expert weights (the TMA maps hold the same pointers)
   const void* w2_base;
   int32_t* pf_flag;            // raised by the route kernel, cleared at the end of this kernel
+  // Early hand-off from the route kernel (null: wait for its completion):
+  // raised once the config, tile_expert[] and the counters are final; the
+  // token-side consumers still wait for the route kernel's completion.
+  int32_t* early_flag;
   int64_t pf_cap;              // bytes to prefetch at most (0: off)
   // Inline route (inline_route.cuh): this kernel computes the histogram,
   // dispatch and placement itself (no route kernel before it).
@@ -370,6 +374,14 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       for (int e = threadIdx.x; e < p.E; e += blockDim.x)
         p.hist_out[e] = reinterpret_cast<InlineRouteScratch*>(base + kCtrlBytes + kStageBytesScatter)->tot[e];
     __syncthreads();  // the scratch (in the ring) is dead from here on
+  } else if (p.early_flag) {
+    // the config and M-tile map are published before the route kernel
+    // finishes placing the assignments: weights can start streaming now
+    if (threadIdx.x == 0)
+      while (ld_acquire_gpu(p.early_flag) == 0) __nanosleep(32);
+    __syncthreads();
+    cfg = __ldcg(p.ctrl);
+    n_post_pad = __ldcg(p.ctrl + 1);
   } else {
     pdl_wait();  // the route kernel's selection, alignment and gathered rows are now visible
     cfg = p.ctrl[0];
@@ -420,6 +432,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   // straight from x with TMA gather4 (4 rows per instruction), so decode-size
   // calls need no grid barrier before the first MMA.
   const bool direct_x = !kFp8 && bmN == 16 && !p.inline_route;
+  if (p.early_flag && warp >= 2 && (kFp8 || !direct_x)) pdl_wait();  // sorted_ids are final
   if (kFp8 && warp >= 2) {
     // FP8: gather + quantise every row to MXFP8 (per-32 power-of-two scales)
     // into x_q and the per-M-tile scale atoms x_sf.
@@ -559,7 +572,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
 #ifdef RAMP_JOBLOG
     int n_claimed = 0;
 #endif
-    bool gathered = direct_x;
+    // direct_x reads sorted_ids itself: under the early hand-off it defers its
+    // token loads until the route kernel has completed
+    bool gathered = direct_x && !p.early_flag;
     while (true) {
       // claim the next job (dynamic, in global order) and publish it to the ring
       int j = 0;
@@ -591,7 +606,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         fence_proxy_async_global();
         gathered = true;
       }
-      const int e = warp_uniform(p.tile_expert[jb.m]);
+      const int e = warp_uniform(__ldcg(p.tile_expert + jb.m));
       const int row0 = jb.m * G.bm;
       if (jb.kind == 0) {
         const uint32_t tx1 = u_kps * (nA * kSubTileBytes + bmN * 128) + (kFp8 ? (nA + 1) * 512 : 0);
@@ -599,15 +614,27 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         const int kb0 = G.kb_lo(jb), kb1 = G.kb_hi(jb);
         int first_pending = 0, npend = 0;
         int trow[16];  // direct_x: token row of each of the 16 MMA columns
-        if (direct_x) {
+        bool have_trow = false;
+        auto ensure_trow = [&]() {  // whole warp; only once sorted_ids are final
+          if (!direct_x || have_trow) return;
           int mine = 0;
           if (lane < G.bm) {
-            const int a = p.sorted_ids[row0 + lane];
+            const int a = __ldcg(p.sorted_ids + row0 + lane);
             mine = a < p.n_assign ? a / p.top_k : 0;
           }
 #pragma unroll
           for (int q = 0; q < 16; ++q) trow[q] = __shfl_sync(0xffffffffu, mine, q);
-        }
+          have_trow = true;
+        };
+        auto gather_tokens = [&](uint32_t sb, uint32_t full, int kb) {  // direct_x token loads of one stage
+          for (int u = 0; u < u_kps; ++u) {
+#pragma unroll
+            for (int q = 0; q < 16; q += 4)
+              tma_gather4(sb + u_tok + u * 16 * 128 + q * 128, &maps.x, full, (kb + u) * 64, trow[q], trow[q + 1],
+                          trow[q + 2], trow[q + 3], pol_x);
+          }
+        };
+        if (gathered) ensure_trow();
         // token-side loads of one stage (tiles + FP8 scale atom), deferrable
         auto load_tokens = [&](uint32_t sb, uint32_t full, int kb) {
           for (int q = 0; q < u_kps; ++q)
@@ -631,15 +658,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
                 bulk_g2s(sb + sf_off + t * 512, p.w1_sf + (rb * G.kbH + kb) * 512, 512, full);
               }
             }
-            if (direct_x) {
-              for (int u = 0; u < u_kps; ++u) {
-#pragma unroll
-                for (int q = 0; q < 16; q += 4)
-                  tma_gather4(sb + u_tok + u * 16 * 128 + q * 128, &maps.x, full, (kb + u) * 64, trow[q], trow[q + 1],
-                              trow[q + 2], trow[q + 3], pol_x);
-              }
-            } else if (gathered) {
-              load_tokens(sb, full, kb);
+            if (gathered) {
+              if (direct_x) gather_tokens(sb, full, kb);
+              else load_tokens(sb, full, kb);
             }
           }
           __syncwarp();
@@ -652,17 +673,21 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
               pc.lap();
               if (p.inline_route) {
                 gen_wait(p.gflag, g0 + 2);
+              } else if (direct_x) {
+                pdl_wait();  // early hand-off: the route kernel has completed, sorted_ids are final
               } else {
                 while (ld_acquire_gpu(p.gbar) < (int)gridDim.x) __nanosleep(32);
               }
               fence_proxy_async_global();
               c_dep += pc.lap();
               gathered = true;
+              ensure_trow();
               if (ts && lane == 0) ts[kTsGathered] = globaltimer();
               if (elect_one()) {
                 for (int q = 0; q < npend; ++q) {
                   const uint32_t st = (stage + u_stg - (npend - 1) + q) % u_stg;
-                  load_tokens(ring_addr + st * u_sbytes, smem_u32(&cs.full[st]), first_pending + q * u_kps);
+                  if (direct_x) gather_tokens(ring_addr + st * u_sbytes, smem_u32(&cs.full[st]), first_pending + q * u_kps);
+                  else load_tokens(ring_addr + st * u_sbytes, smem_u32(&cs.full[st]), first_pending + q * u_kps);
                 }
               }
               __syncwarp();
@@ -941,6 +966,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     }
   } else if (warp >= 4) {
     // ============================ epilogue ===============================
+    if (p.early_flag) pdl_wait();  // the epilogue reads sorted_ids: wait for the route kernel
     const int et = threadIdx.x - 128;  // TMEM lane == weight row of the 128-row MMA tile
     const uint32_t lane_off = static_cast<uint32_t>(et & ~31) << 16;
     uint32_t jl = 0, acc_cnt[2] = {0, 0}, chunk_cnt[2] = {0, 0};
@@ -1206,8 +1232,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       atomicAdd(p.gbar + 1, 1);
       while (ld_acquire_gpu(p.gbar + 1) < (int)gridDim.x) __nanosleep(64);
     }
-    // every CTA is past its prologue: re-arm the prefetch flag for the next call
+    // every CTA is past its prologue: re-arm the prefetch / hand-off flags for the next call
     if (blockIdx.x == 0 && p.pf_flag) *p.pf_flag = 0;
+    if (blockIdx.x == 0 && p.early_flag) *p.early_flag = 0;
     if (ts) ts[kTsEndPass] = globaltimer();
   }
   __syncthreads();

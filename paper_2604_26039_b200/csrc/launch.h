@@ -33,6 +33,7 @@ struct RouteArgs {
   void* x_sorted;        // [rows, H] bf16, gathered by the helper blocks (null: skip)
   int32_t S, H, top_k;
   int32_t publish_hist;  // write hist_out and raise ctrl[11] right after the histogram pass
+  int32_t* early_flag;   // raised (1) once config, tile_expert and counters are final (null: off)
   int32_t pdl_early;     // trigger the dependent launch at entry (1) or after the alignment (0)
   // router fusion: when logits != null the route kernel first computes the
   // softmax top-k into topk_ids (== ids_out) and w_out
@@ -80,6 +81,7 @@ struct MoeLaunch {
   const int32_t* hist;  // speculative prefetch: published histogram, flag, byte cap (0 = off)
   int32_t* pf_flag;
   int64_t pf_cap;
+  int32_t* early_flag;  // the route kernel's early hand-off flag (null: wait for its completion)
   // inline route (the megakernel routes itself; no route kernel, no PDL)
   bool inline_route;
   int32_t forced_cfg;
@@ -92,6 +94,7 @@ struct MoeLaunch {
   int32_t* hist_out;
 };
 
+bool early_handoff_enabled();  // RAMP_EARLY (default 0: measured neutral)
 bool inline_route_enabled();  // RAMP_INLINE_ROUTE (default 0: the separate route kernel measured faster)
 
 extern unsigned long long* g_prof_buffer;  // diagnostics, see ramp_set_profile_buffer

@@ -21,6 +21,14 @@ int64_t prefetch_cap() {
   return cap;
 }
 
+bool early_handoff_enabled() {
+  static bool on = [] {
+    const char* v = getenv("RAMP_EARLY");
+    return v ? atoi(v) != 0 : false;
+  }();
+  return on;
+}
+
 bool inline_route_enabled() {
   static bool on = [] {
     const char* v = getenv("RAMP_INLINE_ROUTE");
@@ -232,6 +240,7 @@ cudaError_t launch_fused_moe(const MoeLaunch& l, cudaStream_t stream, const char
   p.w2_base = l.w2;
   p.pf_flag = l.pf_flag;
   p.pf_cap = l.pf_cap;
+  p.early_flag = l.early_flag;
   p.inline_route = l.inline_route ? 1 : 0;
   p.forced_cfg = l.forced_cfg;
   p.topk_ids = l.topk_ids;

@@ -80,26 +80,39 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   if (a.prof && threadIdx.x == 0) a.prof[7] = clock64();
   const int bm = a.table.bm[sel];
   int32_t* n_post_pad = a.ctrl + 1;
+  // Early hand-off: once the padded offsets and tile_expert[] are final, the
+  // megakernel only needs the config, the M-tile map and its counters to
+  // start streaming weights; the placement of the assignments (and the token
+  // gather behind it) follows.
+  auto publish = [&](int npp) {
+    if (a.done)
+      for (int m = threadIdx.x; m < npp / bm; m += blockDim.x) a.done[m] = 0;
+    if (threadIdx.x == 0) {
+      a.ctrl[0] = sel;
+      a.ctrl[2] = npp / bm;
+      a.ctrl[3] = n_eval;
+      a.ctrl[7] = 0;  // megakernel job counter
+      a.ctrl[8] = 0;  // megakernel grid barrier 0 (rows gathered)
+      a.ctrl[9] = 0;  // megakernel grid barrier 1 (all jobs reduced)
+    }
+    if (a.early_flag) {
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) st_release_gpu(a.early_flag, 1);
+    }
+  };
   if (kDispatch && overlap) {
-    block_place(a.n_assign, a.E, bm, s, st.warp_tot, a.sorted_ids, a.tile_expert, n_post_pad, a.prof);
+    block_place(a.n_assign, a.E, bm, s, st.warp_tot, a.sorted_ids, a.tile_expert, n_post_pad, a.prof, publish);
   } else {
     block_align(a.topk_ids, a.n_assign, a.E, bm, s, st.warp_tot, a.sorted_ids, a.tile_expert, n_post_pad,
-                a.prof);
+                a.prof, publish);
   }
   stamp(3);
   const int npp = s.off[a.E];
   for (int e = threadIdx.x; e < a.E; e += blockDim.x)
     if (a.hist_out) a.hist_out[e] = s.hist[e];
-  if (a.done)
-    for (int m = threadIdx.x; m < npp / bm; m += blockDim.x) a.done[m] = 0;
   if (threadIdx.x == 0) {
-    a.ctrl[0] = sel;
-    a.ctrl[2] = npp / bm;
-    a.ctrl[3] = n_eval;
     a.ctrl[4] = st.bad;
-    a.ctrl[7] = 0;  // megakernel job counter
-    a.ctrl[8] = 0;  // megakernel grid barrier 0 (rows gathered)
-    a.ctrl[9] = 0;  // megakernel grid barrier 1 (all jobs reduced)
     if (a.sel_out) {
       a.sel_out[0] = sel;
       a.sel_out[1] = npp;

@@ -512,9 +512,19 @@ __device__ inline void block_walk_ranks(int64_t n, int E, RouteSmem& s, int firs
   }
 }
 
+struct NoPublish {
+  __device__ void operator()(int) const {}
+};
+
+// `on_offsets(n_post_pad)` runs (in every thread, after a block barrier) as
+// soon as the padded offsets and tile_expert[] are final -- before the
+// bm-dependent placement of the assignments -- so the route kernel can hand
+// the selected config and the M-tile map to the megakernel early.
+template <class Publish = NoPublish>
 __device__ inline void block_place(int64_t n, int E, int bm, RouteSmem& s, int* warp_tot,
                                    int32_t* __restrict__ sorted_ids, int32_t* __restrict__ tile_expert,
-                                   int32_t* n_post_pad_out, unsigned long long* stamps = nullptr) {
+                                   int32_t* n_post_pad_out, unsigned long long* stamps = nullptr,
+                                   Publish on_offsets = Publish{}) {
   auto stamp = [&](int slot) {
     if (stamps && threadIdx.x == 0) {
       unsigned long long t;
@@ -545,6 +555,7 @@ __device__ inline void block_place(int64_t n, int E, int bm, RouteSmem& s, int* 
   }
   __syncthreads();
   stamp(5);
+  on_offsets(total);
   for (int64_t i = tid; i < n; i += blockDim.x) {
     const int v = s.ids[i];
     if (v >= 0) dst[s.off[v & ((1 << kRankShift) - 1)] + (v >> kRankShift)] = static_cast<int32_t>(i);
@@ -565,10 +576,11 @@ __device__ inline void block_place(int64_t n, int E, int bm, RouteSmem& s, int* 
 // Single pass (no dispatch to overlap with): padded scan first, then one walk
 // that writes every position straight to global memory.  Ids come from the
 // shared-memory cache when n <= kIdCache, else from global memory.
+template <class Publish = NoPublish>
 __device__ inline void block_align(const int32_t* __restrict__ ids, int64_t n, int E, int bm,
                                    RouteSmem& s, int* warp_tot, int32_t* __restrict__ sorted_ids,
                                    int32_t* __restrict__ tile_expert, int32_t* n_post_pad_out,
-                                   unsigned long long* stamps = nullptr) {
+                                   unsigned long long* stamps = nullptr, Publish on_offsets = Publish{}) {
   auto stamp = [&](int slot) {
     if (stamps && threadIdx.x == 0) {
       unsigned long long t;
@@ -595,6 +607,7 @@ __device__ inline void block_align(const int32_t* __restrict__ ids, int64_t n, i
   }
   __syncthreads();
   stamp(5);
+  on_offsets(total);
   const int nbits = bits_for(E);
   const int64_t seg = (n + kRouteWarps - 1) / kRouteWarps;
   const int64_t lo = warp * seg, hi = lo + seg < n ? lo + seg : n;
