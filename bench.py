@@ -567,26 +567,34 @@ def ours(args, geom):
         torch.cuda.synchronize()
         return g
 
+    # per-point layer time: a graph of 8 back-to-back calls (rotating weight
+    # copies), so graph-launch latency is amortised as in the step graph;
+    # megakernel time: first CTA past the route hand-off -> last CTA exit, from the kernel's own
+    # globaltimer stamps (the kernel duration, as ncu counts it)
+    prof_buf = torch.zeros(149 * 32 + 148 * 16 * 4, dtype=torch.int64, device=dev)
+    lib = _lib.load()
     for p, pt in enumerate(pts):
-        full = [graph_of(lambda c=c: layer(p, c)) for c in range(2)]
-        route = graph_of(lambda: layer(p, 2, phases=1))
-        mega = [graph_of(lambda c=c: layer(p, c, phases=2)) for c in range(3, 5)]
-        lat, k3 = [], []
-        for r in range(6):
+        g8 = graph_of(lambda: [layer(p, c) for c in range(N_COPIES)])
+        lat = []
+        for r in range(5):
             a0, a1 = ev(), ev()
             a0.record()
-            full[r % 2].replay()
+            g8.replay()
             a1.record()
-            route.replay()
-            b0, b1 = ev(), ev()
-            b0.record()
-            mega[r % 2].replay()
-            b1.record()
             torch.cuda.synchronize()
-            lat.append(a0.elapsed_time(a1) * 1e3)
-            k3.append(b0.elapsed_time(b1) * 1e3)
+            lat.append(a0.elapsed_time(a1) * 1e3 / N_COPIES)
+        lib.ramp_set_profile_buffer(prof_buf.data_ptr())
+        gp = graph_of(lambda: layer(p, 1))
+        lib.ramp_set_profile_buffer(None)
+        k3 = []
+        for r in range(4):
+            prof_buf.zero_()
+            gp.replay()
+            torch.cuda.synchronize()
+            st = prof_buf[:148 * 32].view(148, 32).cpu().numpy()
+            k3.append((st[:, 23].max() - st[:, 17].min()) / 1e3)  # kTsFinal - kTsStart (after the route), ns -> us
         cfg = dtab.pool_id(int(wss[p].sel[0].item()))
-        us, k3us = float(np.median(lat)), float(np.median(k3))
+        us, k3us = float(np.median(lat)), float(np.median(k3[1:]))
         nbytes = layer_bytes(geom, pt["hist"], pt["S"])
         k3_bytes += nbytes
         k3_time += k3us

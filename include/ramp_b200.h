@@ -76,6 +76,14 @@ typedef struct ramp_table {
    *            1, 2 or 4 (BF16 megakernel; null = 1).  Larger stages raise the
    *            per-CTA weight-streaming rate of the decode configs. */
   const int32_t* kps;
+  /* step_cache  optional device-resident StepCache (ramp/dispatch.py:40-54):
+   *             int32 [3 + 2*cap] = {current step, cached step, n, (M, cfg) x cap}.
+   *             The caller advances the step by writing [0] (graph-capturable);
+   *             the dispatcher resets the entries when [1] != [0], reuses the
+   *             selection cached for this step's M = hist total, and appends on
+   *             a miss.  null = no cache. */
+  int32_t* step_cache;
+  int32_t step_cache_cap;
 } ramp_table_t;
 
 /* Library version (major*10000 + minor*100 + patch) and sm_100a build flag. */

@@ -83,6 +83,8 @@ class RampTable(ctypes.Structure):
         ("omega_max", ctypes.c_double),
         ("lam", ctypes.c_void_p),
         ("kps", ctypes.c_void_p),
+        ("step_cache", ctypes.c_void_p),
+        ("step_cache_cap", ctypes.c_int32),
     ]
 
 

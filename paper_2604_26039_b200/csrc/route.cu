@@ -59,7 +59,40 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   // remaining warps walk the (bm-independent) alignment ranks meanwhile.
   const int cfg_warps = (a.table.n_cfg + 31) >> 5;
   const bool overlap = kDispatch && s.cached && cfg_warps <= kRouteWarps - 8;
-  if constexpr (kDispatch) {
+  // Device StepCache (ramp/dispatch.py:40-54): a selection cached for this
+  // step's M skips the dispatcher; a new step clears the entries.
+  int cached = -1;
+  int32_t* const scache = a.table.step_cache;
+  if (kDispatch && scache) {
+    if (threadIdx.x < 32) {
+      int m = 0;
+      for (int e = threadIdx.x; e < a.E; e += 32) m += s.hist[e];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+      if (threadIdx.x == 0) {
+        if (scache[1] != scache[0]) {
+          scache[1] = scache[0];
+          scache[2] = 0;
+        }
+        const int nc = scache[2];
+        int hit = -1;
+        for (int q = 0; q < nc; ++q)
+          if (scache[3 + 2 * q] == m) hit = scache[4 + 2 * q];
+        st.cnt[31] = hit;
+        st.warp_tot[31] = m;
+      }
+    }
+    __syncthreads();
+    cached = st.cnt[31];
+  }
+  if (kDispatch && cached >= 0) {
+    sel = cached;  // hit: no evaluations (DispatchTable.evaluations unchanged)
+    if (overlap) {
+      // the walkers still need their ranks; every warp walks
+      block_walk_ranks(a.n_assign, a.E, s, 0, kRouteWarps);
+      __syncthreads();
+    }
+  } else if constexpr (kDispatch) {
     if (!overlap) {
       sel = block_dispatch(s.hist, a.E, a.table, &s, a.grid_out, a.pred_out, a.n_eval_out, st.mt, st.red,
                            st.cnt, a.prof);
@@ -74,6 +107,14 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
       __syncthreads();
       sel = st.red[0].i;
       n_eval = st.cnt[0];
+    }
+    if (scache && threadIdx.x == 0) {
+      const int nc = scache[2];
+      if (nc < a.table.step_cache_cap) {
+        scache[3 + 2 * nc] = st.warp_tot[31];
+        scache[4 + 2 * nc] = sel;
+        scache[2] = nc + 1;
+      }
     }
   }
   stamp(2);

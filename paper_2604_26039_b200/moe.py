@@ -52,6 +52,7 @@ class DeviceTable:
     lam: np.ndarray | None = None     # B4 L2-reuse factor per config (None: the reference model)
     kps: np.ndarray | None = None     # k-blocks per pipeline stage per config (None: 1)
     id_map: np.ndarray | None = None  # table index -> pool id (a pruned table); None: identity
+    step_cache: "DeviceStepCache | None" = None  # device StepCache (None: every call dispatches)
     _tensors: dict = field(default_factory=dict, repr=False)
     struct: _lib.RampTable | None = field(default=None, repr=False)
 
@@ -103,6 +104,8 @@ class DeviceTable:
                 raise ValueError("kps values must be 1, 2 or 4")
             t["kps"] = torch.as_tensor(kps.astype(np.int32), **i32)
         s.kps = t["kps"].data_ptr() if "kps" in t else None
+        s.step_cache = self.step_cache.buf.data_ptr() if self.step_cache is not None else None
+        s.step_cache_cap = self.step_cache.capacity if self.step_cache is not None else 0
         self.struct = s
 
     def __len__(self) -> int:
@@ -135,6 +138,32 @@ class DeviceTable:
         self._fp8_ok = all(int(m) == 1 and int(sk) == 1 and lib.ramp_config_smem_bytes_fp8(int(bm), int(t), int(st)) > 0
                            for bm, t, st, sk, m in zip(self.bm, self.ttn, self.stg, self.split_k, self.mode))
         return self._fp8_ok
+
+
+class DeviceStepCache:
+    """Device-resident StepCache (ramp/dispatch.py:40-54): per step, M = the
+    histogram total -> selected config.  The route kernel consults it before
+    dispatching and clears it when the step changes; `advance()` starts a new
+    step with a device-side increment, so it can live inside a captured CUDA
+    graph (one advance per replayed step)."""
+
+    def __init__(self, capacity: int = 64, device="cuda"):
+        if capacity < 1:
+            raise ValueError("capacity must be >= 1")
+        self.capacity = int(capacity)
+        # {current step, cached step, n, (M, cfg) x capacity}; cached step -1: empty
+        self.buf = torch.zeros(3 + 2 * self.capacity, dtype=torch.int32, device=device)
+        self.buf[1] = -1
+
+    def advance(self) -> None:
+        self.buf[0:1].add_(1)
+
+    def entries(self) -> dict[int, int]:
+        """Host copy {M: cfg} of the current step's entries (diagnostics)."""
+        h = self.buf.cpu().tolist()
+        if h[1] != h[0]:
+            return {}
+        return {h[3 + 2 * q]: h[4 + 2 * q] for q in range(h[2])}
 
 
 def workspace_bytes(S: int, H: int, I: int, E: int, top_k: int) -> int:

@@ -432,3 +432,46 @@ def test_b4_device_dispatch_matches_oracle():
         want = R.select(cfgs, coeffs, counts.tolist(), g.N, 148, True, ntile=cols["ntile"].tolist(),
                         omega_max=float("inf"), lam=lam)
         assert (int(cfg.item()), int(n_eval.item())) == want
+
+
+def test_device_step_cache():
+    """Device StepCache (ramp/dispatch.py:40-54): within a step the selection
+    cached for M is reused (no evaluations), a new step dispatches again."""
+    M = _M()
+    from paper_2604_26039_b200.catalog import MoeGeometry
+    from paper_2604_26039_b200.config_space import enumerate_b200_configs
+
+    E, H, I, k, S = 16, 256, 256, 4, 24
+    pool = enumerate_b200_configs(MoeGeometry(name="t", E=E, N=2 * I, K=H, top_k=k))
+    cols = pool.columns()
+    n = len(pool)
+    x, w1, w2, w, ids_a = random_moe(S, H, I, E, k, seed=4)
+    ids_b = np.zeros_like(ids_a)  # same M, all assignments on experts 0..k-1 (skewed)
+    ids_b[:] = np.arange(k, dtype=np.int32)[None, :]
+    rng = np.random.default_rng(0)
+    for _ in range(20):  # coefficients under which the two routings select differently
+        a, c = rng.uniform(1, 2, n), rng.uniform(0.0, 0.2, n)
+
+        def table(cache=None):
+            return M.DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
+                                 group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], kps=cols["kps"],
+                                 a=a, b=np.zeros(n), c=c, d=np.zeros(n), N=2 * I, kappa_ok=True, sm_count=148,
+                                 step_cache=cache)
+
+        plain = table()
+        sel_a = _run_fused(x, w1, w2, w, ids_a, plain, -1)[1]
+        sel_b = _run_fused(x, w1, w2, w, ids_b, plain, -1)[1]
+        if sel_a[0] != sel_b[0]:
+            break
+    assert sel_a[0] != sel_b[0]
+    cache = M.DeviceStepCache(8)
+    cached = table(cache)
+    out, s1 = _run_fused(x, w1, w2, w, ids_a, cached, -1)
+    assert s1[0] == sel_a[0] and s1[3] > 0
+    out_b, s2 = _run_fused(x, w1, w2, w, ids_b, cached, -1)
+    assert s2[0] == sel_a[0] and s2[3] == 0, "same step, same M: the cached selection, no evaluations"
+    assert _rel(out_b, fused_moe_ref(x, w1, w2, w, ids_b)) < RTOL_BF16
+    assert cache.entries() == {S * k: int(sel_a[0])}
+    cache.advance()
+    _, s3 = _run_fused(x, w1, w2, w, ids_b, cached, -1)
+    assert s3[0] == sel_b[0] and s3[3] > 0, "a new step dispatches again"
