@@ -393,7 +393,7 @@ def ep_leg(dev, world, rank, iters=10, warmup=3):
     group = None
 
     def layer():
-        return ep.ep_moe_layer(x, ids, w, geom.E, local_fn, group=group)
+        return ep.ep_moe_layer(x, ids, w, geom.E, local_fn, group=group, wire="fp8")
 
     for _ in range(warmup):
         layer()
@@ -408,7 +408,7 @@ def ep_leg(dev, world, rank, iters=10, warmup=3):
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3)
     # the local megakernel alone on this rank's received rows
-    plan, rx, rids, rw = ep.dispatch(x, ids, w, geom.E, group)
+    plan, rx, rids, rw = ep.dispatch(x, ids, w, geom.E, group, wire="fp8")
     for _ in range(iters):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -424,8 +424,10 @@ def ep_leg(dev, world, rank, iters=10, warmup=3):
     torch.cuda.empty_cache()
     return {"workload": f"{EP_MODEL} MoE layer (E=256, top-8, d=7168, d_ff=2048) MXFP8, expert-parallel over "
                         f"{world} GPU(s): {per} experts/rank, {EP_TOKENS} tokens/rank, beta={EP_BETA}",
-            "exchange": "NCCL all_to_all_single (token rows bf16 + local ids/weights; combine of per-(token,rank) "
-                        "partial sums)",
+            "exchange": "NCCL all_to_all_single: token rows as MXFP8 (E4M3 + UE8M0 per 32) + local ids/weights; "
+                        "combine of per-(token,rank) partial sums in bf16",
+            "dispatch_wire_bytes_rank0": plan.wire_bytes,
+            "dispatch_wire_bytes_if_bf16": int(len(plan.pair_token) * geom.K * 2),
             "world": world, "us_per_layer": us, "local_megakernel_us": local_us, "max_rows_per_rank": int(rows),
             "tflops": flops / us / 1e6, "timing": "CUDA events per layer call (includes the split-size host read), "
                                                  "median of iters, max over ranks",

@@ -37,6 +37,7 @@ class EPPlan:
     recv_counts: list[int]
     order: torch.Tensor        # unique (token, rank) pairs sorted by destination rank
     pair_token: torch.Tensor   # origin token of every sent row (sorted order)
+    wire_bytes: int = 0        # token-row payload this rank sent (dispatch direction)
 
 
 def expert_owner(ids: torch.Tensor, E: int, world: int) -> torch.Tensor:
@@ -44,9 +45,18 @@ def expert_owner(ids: torch.Tensor, E: int, world: int) -> torch.Tensor:
     return torch.div(ids, per, rounding_mode="floor")
 
 
-def dispatch(x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor, E: int, group=None):
+def dispatch(x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor, E: int, group=None,
+             wire: str = "bf16"):
     """Route token rows to expert owners.  Returns (plan, recv_x [R, H],
-    recv_ids [R, k] local expert ids, recv_w [R, k])."""
+    recv_ids [R, k] local expert ids, recv_w [R, k]).
+
+    wire = "fp8" sends the token rows as MXFP8 -- E4M3 plus
+    one UE8M0 scale per 32 features, the operand format of the FP8 megakernel,
+    H + H/32 bytes per row instead of 2H -- and the receiver expands them back
+    exactly (E4M3 x 2^k is representable in bf16); the FP8 megakernel then
+    re-derives the same per-32 scales in its gather.  The combine stays bf16."""
+    if wire not in ("bf16", "fp8"):
+        raise ValueError(f"wire must be bf16 or fp8, got {wire!r}")
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     per = E // world
@@ -70,13 +80,26 @@ def dispatch(x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor, E: i
     row_w = torch.where(hit, topk_w[pair_token], torch.zeros((), dtype=topk_w.dtype, device=dev))
     send_x = x[pair_token].contiguous()
     R = sum(rc)
-    recv_x = torch.empty(R, x.shape[1], dtype=x.dtype, device=dev)
+    H = x.shape[1]
     recv_ids = torch.empty(R, k, dtype=torch.int64, device=dev)
     recv_w = torch.empty(R, k, dtype=topk_w.dtype, device=dev)
-    dist.all_to_all_single(recv_x, send_x, rc, sc, group=group)
+    if wire == "fp8":
+        from .quant import GROUP, mx_dequantize, mx_quantize
+
+        q, sf = mx_quantize(send_x)
+        recv_q = torch.empty(R, H, dtype=torch.uint8, device=dev)
+        recv_sf = torch.empty(R, H // GROUP, dtype=torch.uint8, device=dev)
+        dist.all_to_all_single(recv_q, q.view(torch.uint8).contiguous(), rc, sc, group=group)
+        dist.all_to_all_single(recv_sf, sf.contiguous(), rc, sc, group=group)
+        recv_x = mx_dequantize(recv_q.view(torch.float8_e4m3fn), recv_sf).to(x.dtype)
+        wire_bytes = int(send_x.shape[0]) * (H + H // GROUP)
+    else:
+        recv_x = torch.empty(R, H, dtype=x.dtype, device=dev)
+        dist.all_to_all_single(recv_x, send_x, rc, sc, group=group)
+        wire_bytes = int(send_x.numel() * send_x.element_size())
     dist.all_to_all_single(recv_ids, row_ids.contiguous(), rc, sc, group=group)
     dist.all_to_all_single(recv_w, row_w.contiguous(), rc, sc, group=group)
-    plan = EPPlan(send_counts=sc, recv_counts=rc, order=pairs, pair_token=pair_token)
+    plan = EPPlan(send_counts=sc, recv_counts=rc, order=pairs, pair_token=pair_token, wire_bytes=wire_bytes)
     return plan, recv_x, recv_ids.to(torch.int32), recv_w
 
 
@@ -89,9 +112,9 @@ def combine(plan: EPPlan, partial: torch.Tensor, S: int, group=None) -> torch.Te
     return out.to(partial.dtype)
 
 
-def ep_moe_layer(x, topk_ids, topk_w, E: int, local_fn, group=None):
+def ep_moe_layer(x, topk_ids, topk_w, E: int, local_fn, group=None, wire: str = "bf16"):
     """dispatch -> local_fn(recv_x, recv_ids, recv_w) -> combine."""
-    plan, rx, rids, rw = dispatch(x, topk_ids, topk_w, E, group)
+    plan, rx, rids, rw = dispatch(x, topk_ids, topk_w, E, group, wire=wire)
     partial = local_fn(rx, rids, rw)
     return combine(plan, partial, x.shape[0], group)
 

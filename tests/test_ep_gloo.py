@@ -19,7 +19,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, E, S, k, H, I, q):
+def _worker(rank, world, port, E, S, k, H, I, q, wire="bf16"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -41,19 +41,23 @@ def _worker(rank, world, port, E, S, k, H, I, q):
             return torch.from_numpy(fused_moe_ref(rx.numpy(), w1[lo:lo + per], w2[lo:lo + per], rw.numpy(),
                                                   rids.numpy()))
 
-        out = ep_moe_layer(torch.from_numpy(x), torch.from_numpy(ids), torch.from_numpy(w), E, local_fn)
+        out = ep_moe_layer(torch.from_numpy(x), torch.from_numpy(ids), torch.from_numpy(w), E, local_fn, wire=wire)
+        if wire == "fp8":  # the wire carries MXFP8 token rows: the reference sees the same rounding
+            from paper_2604_26039_b200.quant import mx_dequantize, mx_quantize
+
+            x = mx_dequantize(*mx_quantize(torch.from_numpy(x))).numpy()
         ref = fused_moe_ref(x, w1, w2, w, ids)
         q.put((rank, float(np.abs(out.numpy() - ref).max()), float(np.abs(ref).max())))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("E,S,k", [(8, 13, 2), (16, 5, 4)])
-def test_ep_world2_matches_dense(E, S, k):
+@pytest.mark.parametrize("E,S,k,wire", [(8, 13, 2, "bf16"), (16, 5, 4, "bf16"), (16, 9, 4, "fp8")])
+def test_ep_world2_matches_dense(E, S, k, wire):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, E, S, k, 32, 16, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, E, S, k, 32, 16, q, wire)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in procs]
