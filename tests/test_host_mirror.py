@@ -364,3 +364,24 @@ def test_pruned_table_masks_and_maps_ids():
     samples = [S(0, 10.0, 1), S(1, 10.4, 1), S(2, 12.0, 1), S(0, 20.0, 2), S(2, 19.0, 2)]
     assert useful_configs(samples, 0.05) == (0, 1, 2)
     assert useful_configs(samples, 0.01) == (0, 2)
+
+
+def test_triton_pool_and_config_dict():
+    """The third-party (vLLM Triton fused_moe) pool: grid semantics of the
+    reference (g = sum ceil(c_e/BM) * ceil(N/BN)) and the override dicts."""
+    from paper_2604_26039_b200.catalog import BASELINE_MODELS
+    from paper_2604_26039_b200.config_space import enumerate_triton_configs, triton_config_dict
+    from paper_2604_26039_b200.routing import pool_grids, sample_histogram
+
+    geom = BASELINE_MODELS["OLMoE-1B-7B"]
+    pool = enumerate_triton_configs(geom)
+    assert len(pool) == 40 and all(c.family == "triton" for c in pool)
+    hist = sample_histogram(geom.E, 32, geom.top_k, 0.5, 3).histogram
+    counts = np.asarray(hist.counts)
+    g = pool_grids(pool, hist)
+    for c in pool:
+        want = int(sum(-(-n // c.bm) for n in counts if n > 0)) * (-(-geom.N // c.ttn))
+        assert g[c.id] == want
+        d = triton_config_dict(c)
+        assert (d["BLOCK_SIZE_M"], d["BLOCK_SIZE_N"], d["BLOCK_SIZE_K"]) == (c.bm, c.ttn, 64 * c.kps)
+        assert d["num_stages"] * (c.bm + c.ttn) * d["BLOCK_SIZE_K"] * 2 <= 200 * 1024
