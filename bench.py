@@ -392,8 +392,12 @@ def ep_leg(dev, world, rank, iters=10, warmup=3):
     local_fn = ep.make_local_megakernel(weights, dtab)
     group = None
 
+    # MXFP8 token rows on the wire when there is a wire (N > 1); at N = 1 the
+    # exchange is a local copy and the quantise/expand kernels would only add time
+    wire = "fp8" if world > 1 else "bf16"
+
     def layer():
-        return ep.ep_moe_layer(x, ids, w, geom.E, local_fn, group=group, wire="fp8")
+        return ep.ep_moe_layer(x, ids, w, geom.E, local_fn, group=group, wire=wire)
 
     for _ in range(warmup):
         layer()
@@ -408,7 +412,7 @@ def ep_leg(dev, world, rank, iters=10, warmup=3):
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3)
     # the local megakernel alone on this rank's received rows
-    plan, rx, rids, rw = ep.dispatch(x, ids, w, geom.E, group, wire="fp8")
+    plan, rx, rids, rw = ep.dispatch(x, ids, w, geom.E, group, wire=wire)
     for _ in range(iters):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -424,8 +428,8 @@ def ep_leg(dev, world, rank, iters=10, warmup=3):
     torch.cuda.empty_cache()
     return {"workload": f"{EP_MODEL} MoE layer (E=256, top-8, d=7168, d_ff=2048) MXFP8, expert-parallel over "
                         f"{world} GPU(s): {per} experts/rank, {EP_TOKENS} tokens/rank, beta={EP_BETA}",
-            "exchange": "NCCL all_to_all_single: token rows as MXFP8 (E4M3 + UE8M0 per 32) + local ids/weights; "
-                        "combine of per-(token,rank) partial sums in bf16",
+            "exchange": f"NCCL all_to_all_single: token rows as {'MXFP8 (E4M3 + UE8M0 per 32)' if wire == 'fp8' else 'bf16'}"
+                        " + local ids/weights; combine of per-(token,rank) partial sums in bf16",
             "dispatch_wire_bytes_rank0": plan.wire_bytes,
             "dispatch_wire_bytes_if_bf16": int(len(plan.pair_token) * geom.K * 2),
             "world": world, "us_per_layer": us, "local_megakernel_us": local_us, "max_rows_per_rank": int(rows),
@@ -614,7 +618,7 @@ def ours(args, geom):
         # the exhaustive sweep times every pool config, pruned or not
         full_tab = DispatchTable(model=MODEL, pool=pool, coefficients=table.coefficients,
                                  sm_count=table.sm_count).device_table(device=dev)
-        timer = MeasuredTimer(geom, full_tab, w1=copies[0][0], w2=copies[0][1], iters=5, device=dev)
+        timer = MeasuredTimer(geom, full_tab, w1=copies[0][0], w2=copies[0][1], iters=9, device=dev)
         points = [(pt["S"], pt["beta"]) for pt in pts]
         spd = speedup_ra_vs_static(table, pool, geom, timer, points=points, seeds_per_point=1)
         reg = evaluate_regret(table, pool, geom, timer, test_points=points, seeds_per_point=1)
