@@ -226,7 +226,9 @@ struct Geometry {
   __device__ __forceinline__ int kb_hi(const Job& jb) const { return (jb.kq + 1) * (jb.kind ? kbI : kbH) / sk; }
 };
 
-__device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + __expf(-g)) * u; }
+// silu(g) * u; the fast division returns 0 for a huge denominator (g -> -inf),
+// which is silu's limit, and its ~2 ulp error is far below the bf16 rounding.
+__device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.0f + __expf(-g)) * u; }
 
 // Scatter-reduce 16 token columns of a [128 x bm] TMEM accumulator block into
 // out (fp32): scale by the top-k weight, transpose through shared memory so
@@ -1074,12 +1076,19 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             // Thread et owns features f = th*128 + et of the stripe.
             for (int th = 0; th < nA / 2; ++th) {
               const int f = th * 128 + et;
-              for (int j0 = 0; j0 < bmN; j0 += 16) {
-                float g[16], u[16];
+              // two 16-column chunks per TMEM round trip
+              for (int j0 = 0; j0 < bmN; j0 += 32) {
+                float g[16], u[16], g1[16], u1[16];
+                const bool two = j0 + 16 < bmN;
                 tmem_ld16(acc + th * bmN + j0, g);
                 tmem_ld16(acc + (nA / 2 + th) * bmN + j0, u);
+                if (two) {
+                  tmem_ld16(acc + th * bmN + j0 + 16, g1);
+                  tmem_ld16(acc + (nA / 2 + th) * bmN + j0 + 16, u1);
+                }
                 tmem_ld_wait();
                 store_act(f, j0, g, u);
+                if (two) store_act(f, j0 + 16, g1, u1);
               }
             }
           }
@@ -1124,15 +1133,18 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             mbar_wait(smem_u32(&cs.chunk_full[b]), chunk_cnt[b] & 1);
             c_wchunk += pc.lap();
             tc_fence_after();
-            for (int j0 = 0; j0 < G.bm; j0 += 16) {
-              float v[16];
+            for (int j0 = 0; j0 < G.bm; j0 += 32) {  // two 16-column chunks per TMEM round trip
+              float v[16], v1[16];
+              const bool two = j0 + 16 < G.bm;
               tmem_ld16(tmem + lane_off + b * bmN + j0, v);
+              if (two) tmem_ld16(tmem + lane_off + b * bmN + j0 + 16, v1);
               tmem_ld_wait();
-              if (j0 + 16 >= G.bm) {
+              if (j0 + 32 >= G.bm) {
                 tc_fence_before();
                 mbar_arrive(smem_u32(&cs.chunk_empty[b]));
               }
               scatter16(v, j0, G.bm, et, tbuf, cs, p.out_acc, p.H, hc * 128);
+              if (two) scatter16(v1, j0 + 16, G.bm, et, tbuf, cs, p.out_acc, p.H, hc * 128);
             }
             ++chunk_cnt[b];
             c_scatter += pc.lap();
@@ -1186,15 +1198,19 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         }
       } else {
         // ---- split phase 3 epilogue: one 128-row chunk, full I reduced in TMEM
-        for (int j0 = 0; j0 < G.bm; j0 += 16) {
-          float v[16];
+        // (two 16-column chunks per TMEM round trip)
+        for (int j0 = 0; j0 < G.bm; j0 += 32) {
+          float v[16], v1[16];
+          const bool two = j0 + 16 < G.bm;
           tmem_ld16(acc + j0, v);
+          if (two) tmem_ld16(acc + j0 + 16, v1);
           tmem_ld_wait();
-          if (j0 + 16 >= G.bm) {
+          if (j0 + 32 >= G.bm) {
             tc_fence_before();
             mbar_arrive(smem_u32(&cs.acc_empty[r]));
           }
           scatter16(v, j0, G.bm, et, tbuf, cs, p.out_acc, p.H, jb.hc * 128);
+          if (two) scatter16(v1, j0 + 16, G.bm, et, tbuf, cs, p.out_acc, p.H, jb.hc * 128);
         }
         c_scatter += pc.lap();
       }
