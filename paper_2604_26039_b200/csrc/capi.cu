@@ -202,6 +202,7 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   ra.H = H;
   ra.top_k = top_k;
   ra.pdl_early = ramp::pdl_mode() == 1;
+  ra.pdl_prev = ramp::pdl_prev_enabled() ? 1 : 0;
   // speculative weight prefetch (BF16): only when this call also runs the
   // route kernel, which publishes the histogram early
   // (decode sizes only: at prefill sizes the prefetch competes with the token

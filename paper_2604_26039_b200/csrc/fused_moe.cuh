@@ -1232,6 +1232,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
 
   // ---- grid barrier 1: every job's reductions have landed; then convert
   // the fp32 accumulator to bf16 and clear it for the next call.
+  // The next route kernel (a PDL secondary) may be scheduled from here on; it
+  // waits for this grid's completion before it reads or writes anything.
+  pdl_launch_dependents();
   __threadfence();
   tc_fence_before();
   __syncthreads();

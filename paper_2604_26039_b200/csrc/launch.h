@@ -34,6 +34,7 @@ struct RouteArgs {
   int32_t S, H, top_k;
   int32_t publish_hist;  // write hist_out and raise ctrl[11] right after the histogram pass
   int32_t* early_flag;   // raised (1) once config, tile_expert and counters are final (null: off)
+  int32_t pdl_prev;      // launched as a PDL secondary of the previous kernel (waits before reading)
   int32_t pdl_early;     // trigger the dependent launch at entry (1) or after the alignment (0)
   // router fusion: when logits != null the route kernel first computes the
   // softmax top-k into topk_ids (== ids_out) and w_out
@@ -94,6 +95,7 @@ struct MoeLaunch {
   int32_t* hist_out;
 };
 
+bool pdl_prev_enabled();       // RAMP_PDL_PREV (default 1): route kernel as PDL secondary of the previous kernel
 bool early_handoff_enabled();  // RAMP_EARLY (default 0: measured neutral)
 bool inline_route_enabled();  // RAMP_INLINE_ROUTE (default 0: the separate route kernel measured faster)
 

@@ -21,6 +21,14 @@ int64_t prefetch_cap() {
   return cap;
 }
 
+bool pdl_prev_enabled() {
+  static bool on = [] {
+    const char* v = getenv("RAMP_PDL_PREV");
+    return v ? atoi(v) != 0 : true;
+  }();
+  return on;
+}
+
 bool early_handoff_enabled() {
   static bool on = [] {
     const char* v = getenv("RAMP_EARLY");

@@ -34,6 +34,10 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   if (a.prof && threadIdx.x == 0) a.prof[6] = clock64();
   // the dispatch table is constant: start copying it to shared memory now
   if constexpr (kDispatch) stage_table(a.table, s);
+  // Launched as a programmatic dependent of the previous kernel in the stream
+  // (typically the previous layer's megakernel): everything above overlaps its
+  // tail; nothing above touches the inputs or the workspace.
+  if (a.pdl_prev) pdl_wait();
   if (threadIdx.x == 0) st.bad = 0;
   if constexpr (kGating) {
     // router fusion: the top-k is computed here (host checked n <= kIdCache)
@@ -211,7 +215,20 @@ static cudaError_t launch_route_t(const RouteArgs& a, cudaStream_t stream) {
     if (err != cudaSuccess) return err;
     attr_set = true;
   }
-  route_kernel<kGating, kDispatch><<<1, kRouteThreads, smem, stream>>>(a);
+  // PDL on the route launch too: it may start (and stage its table) while the
+  // previous kernel drains; it waits for it before reading anything it wrote
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(kRouteThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = pdl;
+  cfg.numAttrs = a.pdl_prev ? 1 : 0;
+  cudaError_t err = cudaLaunchKernelEx(&cfg, route_kernel<kGating, kDispatch>, a);
+  if (err != cudaSuccess) return err;
   return cudaGetLastError();
 }
 
