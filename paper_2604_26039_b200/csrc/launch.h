@@ -95,7 +95,7 @@ struct MoeLaunch {
   int32_t* hist_out;
 };
 
-bool pdl_prev_enabled();       // RAMP_PDL_PREV (default 1): route kernel as PDL secondary of the previous kernel
+bool pdl_prev_enabled();       // RAMP_PDL_PREV (default 0, measured neutral): route as PDL secondary of the previous kernel
 bool early_handoff_enabled();  // RAMP_EARLY (default 0: measured neutral)
 bool inline_route_enabled();  // RAMP_INLINE_ROUTE (default 0: the separate route kernel measured faster)
 

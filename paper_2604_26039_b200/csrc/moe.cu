@@ -24,7 +24,7 @@ int64_t prefetch_cap() {
 bool pdl_prev_enabled() {
   static bool on = [] {
     const char* v = getenv("RAMP_PDL_PREV");
-    return v ? atoi(v) != 0 : true;
+    return v ? atoi(v) != 0 : false;
   }();
   return on;
 }
