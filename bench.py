@@ -319,7 +319,7 @@ def mixtral_leg(dev):
                 best_stg[key] = c.id
     cand = sorted(best_stg.values())
     flat = DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
-                       group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], kps=cols["kps"], a=np.ones(n),
+                       group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], kps=cols["kps"], h3=cols["h3"], a=np.ones(n),
                        b=np.zeros(n), c=np.zeros(n), d=np.zeros(n), N=geom.N, kappa_ok=True, sm_count=148,
                        device=dev)
     timer = MeasuredTimer(geom, flat, iters=3, device=dev)

@@ -84,6 +84,11 @@ typedef struct ramp_table {
    *             a miss.  null = no cache. */
   int32_t* step_cache;
   int32_t step_cache_cap;
+  /* h3[i]      split-mode phase-3 jobs of config i cover h3 128-row chunks of
+   *            d_model sharing one act tile: 1, 2 or 4, at most ttn/128 (BF16
+   *            megakernel; null = 1).  Halves/quarters the act re-reads and the
+   *            phase-3 job count of the prefill configs. */
+  const int32_t* h3;
 } ramp_table_t;
 
 /* Library version (major*10000 + minor*100 + patch) and sm_100a build flag. */

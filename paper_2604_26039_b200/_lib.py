@@ -85,6 +85,7 @@ class RampTable(ctypes.Structure):
         ("kps", ctypes.c_void_p),
         ("step_cache", ctypes.c_void_p),
         ("step_cache_cap", ctypes.c_int32),
+        ("h3", ctypes.c_void_p),
     ]
 
 

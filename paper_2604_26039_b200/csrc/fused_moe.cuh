@@ -201,6 +201,7 @@ struct Job {
 
 struct Geometry {
   int mode, bm, bmN, nA, n_i, stripes, n_mtiles, n_hc, kbH, kbI, nJobA, total, group_m, sk, kps;
+  int n3, n_hj;  // split phase 3: 128-row H chunks per job (shared act tile), jobs per M-tile
   bool dbl;  // TMEM double buffering across jobs (split mode, fits in 256 columns)
   __device__ __forceinline__ Job job(int j) const {
     Job r;
@@ -215,8 +216,8 @@ struct Geometry {
       const int jj = j - nJobA, u = jj / sk;
       r.kind = 1;
       r.kq = jj % sk;
-      r.m = group_m ? (u % n_mtiles) : (u / n_hc);
-      r.hc = group_m ? (u / n_mtiles) : (u % n_hc);
+      r.m = group_m ? (u % n_mtiles) : (u / n_hj);
+      r.hc = group_m ? (u / n_mtiles) : (u % n_hj);  // job index: chunks [hc * n3, hc * n3 + n3)
       r.s = 0;
     }
     return r;
@@ -408,7 +409,13 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   G.group_m = p.table.group_m[cfg];
   G.sk = (G.mode == kModeSplit && p.table.split_k[cfg] > 1) ? p.table.split_k[cfg] : 1;
   G.nJobA = G.n_mtiles * G.stripes * G.sk;
-  G.total = G.nJobA + (G.mode == kModeSplit ? G.n_mtiles * G.n_hc * G.sk : 0);
+  G.n3 = 1;
+  if (!kFp8 && G.mode == kModeSplit && p.table.h3) {
+    const int h3 = p.table.h3[cfg];
+    if ((h3 == 2 || h3 == 4) && h3 <= G.nA && G.n_hc % h3 == 0) G.n3 = h3;
+  }
+  G.n_hj = G.n_hc / G.n3;
+  G.total = G.nJobA + (G.mode == kModeSplit ? G.n_mtiles * G.n_hj * G.sk : 0);
   G.dbl = !kFp8 && G.mode == kModeSplit && G.nA * G.bmN <= 256;
   // k-blocks per stage (BF16 only); every job's k-range must split into whole stages
   G.kps = (!kFp8 && p.table.kps) ? p.table.kps[cfg] : 1;
@@ -715,8 +722,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       } else {
         // Split phase 3: weights stream immediately; the act rows wait for
         // every phase-1 job of this M-tile (release/acquire on done[m]).
-        const uint32_t tx = u_kps * (kSubTileBytes + bmN * 128) + (kFp8 ? 2 * 512 : 0);
-        const int wrow = e * p.H + jb.hc * 128;
+        const int n3 = warp_uniform(G.n3);
+        const uint32_t tx = u_kps * (n3 * kSubTileBytes + bmN * 128) + (kFp8 ? 2 * 512 : 0);
+        const int wrow = e * p.H + jb.hc * n3 * 128;
         const int kb0 = G.kb_lo(jb), kb1 = G.kb_hi(jb);
         // act tiles sit after the stage's weight area (FP8: right after the one W2 box)
         const int a_off = kFp8 ? kSubTileBytes : u_tok;
@@ -726,7 +734,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         // still being produced by the phase-1 jobs, HBM keeps streaming weights,
         // and once the dependency resolves the slice arrives from L2.
         if (ld_acquire_gpu(p.done + jb.m) < G.stripes) {
-          for (int kb = kb0 + u_stg * u_kps + lane; kb < kb1; kb += 32) tma_prefetch_2d(tm_w2, kb * kKb, wrow);
+          for (int t = 0; t < n3; ++t)
+            for (int kb = kb0 + u_stg * u_kps + lane; kb < kb1; kb += 32) tma_prefetch_2d(tm_w2, kb * kKb, wrow + t * 128);
         }
         __syncwarp();
         auto load_act = [&](uint32_t sb, uint32_t full, int kb) {
@@ -742,7 +751,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             const uint32_t full = smem_u32(&cs.full[stage]);
             const uint32_t sb = ring_addr + stage * u_sbytes;
             mbar_arrive_expect_tx(full, tx);
-            for (int q = 0; q < u_kps; ++q) tma_load_2d(sb + q * kSubTileBytes, tm_w2, full, (kb + q) * kKb, wrow, pol_w);
+            for (int q = 0; q < u_kps; ++q)
+              for (int t = 0; t < n3; ++t)
+                tma_load_2d(sb + (q * n3 + t) * kSubTileBytes, tm_w2, full, (kb + q) * kKb, wrow + t * 128, pol_w);
             if constexpr (kFp8)
               bulk_g2s(sb + kSubTileBytes + bmN * 128, p.w2_sf + (static_cast<int64_t>(wrow / 128) * G.kbI + kb) * 512,
                        512, full);
@@ -913,6 +924,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           }
         }
       } else {
+        const int n3 = warp_uniform(G.n3);
         for (int kb = kb0; kb < kb1; kb += u_kps) {
           const uint32_t sb = wait_full();
           const uint64_t da = sw128_kmajor_desc(sb);
@@ -927,12 +939,13 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
                 mma_mxf8(acc, da + ((k * 32) >> 4), db + ((k * 32) >> 4), idesc_mxf8(128, bmN, k), ((kb - kb0) | k) != 0,
                          (uint32_t(k) << 30) | (u_tmem + kSfCol), (uint32_t(k) << 30) | (u_tmem + kSfCol + 4));
             } else {
-              for (int q = 0; q < u_kps; ++q) {
+              for (int q = 0; q < u_kps; ++q)
+                for (int t = 0; t < n3; ++t) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                  mma_bf16(acc, da + ((q * kSubTileBytes + k * 32) >> 4), db + ((q * bmN * 128 + k * 32) >> 4), idesc,
-                           ((kb - kb0) | q | k) != 0);
-              }
+                  for (int k = 0; k < 4; ++k)
+                    mma_bf16(acc + t * bmN, da + ((((q * n3 + t) * kSubTileBytes) + k * 32) >> 4),
+                             db + ((q * bmN * 128 + k * 32) >> 4), idesc, ((kb - kb0) | q | k) != 0);
+                }
             }
           }
           __syncwarp();
@@ -1197,20 +1210,23 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           c_swiglu += pc.lap();
         }
       } else {
-        // ---- split phase 3 epilogue: one 128-row chunk, full I reduced in TMEM
+        // ---- split phase 3 epilogue: n3 128-row chunks, full I reduced in TMEM
         // (two 16-column chunks per TMEM round trip)
-        for (int j0 = 0; j0 < G.bm; j0 += 32) {
-          float v[16], v1[16];
-          const bool two = j0 + 16 < G.bm;
-          tmem_ld16(acc + j0, v);
-          if (two) tmem_ld16(acc + j0 + 16, v1);
-          tmem_ld_wait();
-          if (j0 + 32 >= G.bm) {
-            tc_fence_before();
-            mbar_arrive(smem_u32(&cs.acc_empty[r]));
+        for (int t = 0; t < G.n3; ++t) {
+          const int col0 = (jb.hc * G.n3 + t) * 128;
+          for (int j0 = 0; j0 < G.bm; j0 += 32) {
+            float v[16], v1[16];
+            const bool two = j0 + 16 < G.bm;
+            tmem_ld16(acc + t * G.bmN + j0, v);
+            if (two) tmem_ld16(acc + t * G.bmN + j0 + 16, v1);
+            tmem_ld_wait();
+            if (t == G.n3 - 1 && j0 + 32 >= G.bm) {
+              tc_fence_before();
+              mbar_arrive(smem_u32(&cs.acc_empty[r]));
+            }
+            scatter16(v, j0, G.bm, et, tbuf, cs, p.out_acc, p.H, col0);
+            if (two) scatter16(v1, j0 + 16, G.bm, et, tbuf, cs, p.out_acc, p.H, col0);
           }
-          scatter16(v, j0, G.bm, et, tbuf, cs, p.out_acc, p.H, jb.hc * 128);
-          if (two) scatter16(v1, j0 + 16, G.bm, et, tbuf, cs, p.out_acc, p.H, jb.hc * 128);
         }
         c_scatter += pc.lap();
       }

@@ -51,6 +51,7 @@ class DeviceTable:
     omega_max: float = 0.0            # split-K gate threshold (<= 0: the reference's 0.2)
     lam: np.ndarray | None = None     # B4 L2-reuse factor per config (None: the reference model)
     kps: np.ndarray | None = None     # k-blocks per pipeline stage per config (None: 1)
+    h3: np.ndarray | None = None      # split phase-3 H chunks per job per config (None: 1)
     id_map: np.ndarray | None = None  # table index -> pool id (a pruned table); None: identity
     step_cache: "DeviceStepCache | None" = None  # device StepCache (None: every call dispatches)
     _tensors: dict = field(default_factory=dict, repr=False)
@@ -104,6 +105,14 @@ class DeviceTable:
                 raise ValueError("kps values must be 1, 2 or 4")
             t["kps"] = torch.as_tensor(kps.astype(np.int32), **i32)
         s.kps = t["kps"].data_ptr() if "kps" in t else None
+        if self.h3 is not None:
+            h3 = np.asarray(self.h3, dtype=np.int64)
+            if len(h3) != n:
+                raise ValueError("h3 must have one entry per config")
+            if not np.isin(h3, (1, 2, 4)).all():
+                raise ValueError("h3 values must be 1, 2 or 4")
+            t["h3"] = torch.as_tensor(h3.astype(np.int32), **i32)
+        s.h3 = t["h3"].data_ptr() if "h3" in t else None
         s.step_cache = self.step_cache.buf.data_ptr() if self.step_cache is not None else None
         s.step_cache_cap = self.step_cache.capacity if self.step_cache is not None else 0
         self.struct = s

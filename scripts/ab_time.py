@@ -2,7 +2,7 @@
 
     RAMP_B200_LIB=<lib.so> python scripts/ab_time.py --points 16:0.5,1024:0.2 --cfgs "8,128,8,0,1,1,1;128,256,4,0,1,1,1"
 
-Config spec: bm,ttn,stg,group_m,mode,split_k,kps.  Prints one line per
+Config spec: bm,ttn,stg,group_m,mode,split_k,kps[,h3].  Prints one line per
 (point, config): median us over the timer's L2-flushed graph replays.
 """
 import argparse
@@ -26,20 +26,21 @@ ap.add_argument("--cfgs", default="8,128,8,0,1,1,1;16,256,6,0,1,1,1;64,256,4,0,1
 ap.add_argument("--iters", type=int, default=9)
 a = ap.parse_args()
 geom = BASELINE_MODELS["OLMoE-1B-7B"]
-pool = enumerate_b200_configs(geom, HardwareModel.b200())
+pool = enumerate_b200_configs(geom, HardwareModel.b200(), phase3_chunks=True)
 cols = pool.columns()
 n = len(pool)
 flat = DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
-                   group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], kps=cols["kps"], a=np.ones(n),
-                   b=np.zeros(n), c=np.zeros(n), d=np.zeros(n), N=geom.N, kappa_ok=True, sm_count=148)
-timer = MeasuredTimer(geom, flat, iters=a.iters)
+                   group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], kps=cols["kps"], h3=cols["h3"],
+                   a=np.ones(n), b=np.zeros(n), c=np.zeros(n), d=np.zeros(n), N=geom.N, kappa_ok=True, sm_count=148)
 want = [tuple(int(v) for v in c.split(",")) for c in a.cfgs.split(";")]
+want = [w if len(w) == 8 else w + (1,) for w in want]  # h3 defaults to 1
 ids = []
 for w in want:
-    m = [c.id for c in pool if (c.bm, c.ttn, c.stg, int(c.group_m), c.mode, c.split_k, c.kps) == w]
+    m = [c.id for c in pool if (c.bm, c.ttn, c.stg, int(c.group_m), c.mode, c.split_k, c.kps, c.h3) == w]
     if not m:
         raise SystemExit(f"config {w} not in the pool")
     ids.append(m[0])
+timer = MeasuredTimer(geom, flat, iters=a.iters)
 for spec in a.points.split(","):
     S, beta = int(spec.split(":")[0]), float(spec.split(":")[1])
     hs = derive_seed(42, EVAL_HIST_DOMAIN, S, round(beta * 1000), 0)

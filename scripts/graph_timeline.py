@@ -35,7 +35,7 @@ if a.flat:
     cols = pool.columns()
     n = len(pool)
     dtab = moe.DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
-                           group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], kps=cols.get("kps"), a=np.ones(n), b=np.zeros(n),
+                           group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], kps=cols.get("kps"), h3=cols.get("h3"), a=np.ones(n), b=np.zeros(n),
                            c=np.zeros(n), d=np.zeros(n), N=geom.N, kappa_ok=True, sm_count=148, device=dev)
 else:
     table, _ = load_table(geom, pool, HardwareModel.b200())

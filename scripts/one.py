@@ -36,7 +36,7 @@ pool = enumerate_b200_configs(MoeGeometry(name="p", E=E, N=2 * I, K=H, top_k=k))
 cols = pool.columns()
 n = len(pool)
 table = M.DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
-                      group_m=cols["group_m"].astype(np.int64), mode=cols.get("mode"), kps=cols.get("kps"), a=np.ones(n), b=np.zeros(n), c=np.zeros(n),
+                      group_m=cols["group_m"].astype(np.int64), mode=cols.get("mode"), kps=cols.get("kps"), h3=cols.get("h3"), a=np.ones(n), b=np.zeros(n), c=np.zeros(n),
                       d=np.zeros(n), N=2 * I, kappa_ok=False, sm_count=148)
 cfg = [c.id for c in pool if (c.bm, c.ttn, c.stg, int(c.group_m), c.mode, c.split_k) == (a.bm, a.ttn, a.stg, a.gm, a.mode, a.sk)][0]
 x = torch.randn(S, H, device="cuda", generator=gen).to(torch.bfloat16)

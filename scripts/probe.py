@@ -50,7 +50,7 @@ def main():
     cols = pool.columns()
     n = len(pool)
     table = M.DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
-                          group_m=cols["group_m"].astype(np.int64), mode=cols.get("mode"), kps=cols.get("kps"), a=np.ones(n), b=np.zeros(n),
+                          group_m=cols["group_m"].astype(np.int64), mode=cols.get("mode"), kps=cols.get("kps"), h3=cols.get("h3"), a=np.ones(n), b=np.zeros(n),
                           c=np.zeros(n), d=np.zeros(n), N=2 * I, kappa_ok=False, sm_count=148)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     print(f"pool {n} configs", flush=True)

@@ -25,7 +25,7 @@ pool = enumerate_b200_configs(geom, hw)
 cols = pool.columns()
 n = len(pool)
 flat = DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
-                   group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], kps=cols.get("kps"), a=np.ones(n), b=np.zeros(n),
+                   group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], kps=cols.get("kps"), h3=cols.get("h3"), a=np.ones(n), b=np.zeros(n),
                    c=np.zeros(n), d=np.zeros(n), N=geom.N, kappa_ok=True, sm_count=148, ntile=cols["ntile"],
                    omega_max=float("inf"))
 timer = MeasuredTimer(geom, flat, iters=a.iters)

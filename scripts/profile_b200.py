@@ -121,7 +121,7 @@ def main() -> None:
     t0 = time.time()
     def make_timer():
         flat = DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
-                           group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], kps=cols.get("kps"), a=np.ones(n),
+                           group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], kps=cols.get("kps"), h3=cols.get("h3"), a=np.ones(n),
                            b=np.zeros(n), c=np.zeros(n), d=np.zeros(n), N=geom.N, kappa_ok=False,
                            sm_count=hw.sm_count)
         if a.dtype == "fp8":

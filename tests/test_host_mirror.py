@@ -208,6 +208,28 @@ def test_b200_pool_is_kernel_admissible():
         assert [c.id for c in pool] == list(range(len(pool)))
 
 
+def test_phase3_chunk_variants():
+    """h3 > 1 (opt-in): split-mode BF16 only, h3 <= ttn/128, d_model chunks
+    divisible by h3; the job grid counts H/(128*h3) phase-3 jobs per M-tile."""
+    g = C.BASELINE_MODELS["OLMoE-1B-7B"]
+    base = CS.enumerate_b200_configs(g)
+    ext = CS.enumerate_b200_configs(g, phase3_chunks=True)
+    assert all(c.h3 == 1 for c in base)
+    extra = [c for c in ext if c.h3 > 1]
+    assert len(ext) == len(base) + len(extra) and extra
+    cols = ext.columns()
+    for c in extra:
+        assert c.mode == 1 and c.dtype == "bf16" and c.h3 <= c.ttn // 128 and c.bm >= CS.B200_H3_MIN_BM
+        assert cols["ntile"][c.id] == g.N // c.ttn + g.K // 128 // c.h3
+        assert c.to_dict()["h3"] == c.h3
+    with pytest.raises(ValueError):
+        CS.TileConfig(id=0, bm=64, bn=128, wn=1, stg=3, ttn=128, family="b200", mode=1, h3=2)  # h3 > ttn/128
+    with pytest.raises(ValueError):
+        CS.TileConfig(id=0, bm=64, bn=128, wn=2, stg=3, ttn=256, family="b200", mode=0, h3=2)  # fused mode
+    with pytest.raises(ValueError):
+        CS.TileConfig(id=0, bm=64, bn=128, wn=2, stg=3, ttn=256, family="b200", mode=1, h3=3)
+
+
 # ------------------------------------------------------------- B4 variant
 def _b4_table(seed=0):
     from paper_2604_26039_b200.catalog import BASELINE_MODELS

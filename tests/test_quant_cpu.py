@@ -92,7 +92,7 @@ def test_fp8_pool_and_table_gate():
         cols = pool.columns()
         n = len(pool)
         t = DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
-                        group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], kps=cols.get("kps"), a=np.ones(n), b=np.zeros(n),
+                        group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], kps=cols.get("kps"), h3=cols.get("h3"), a=np.ones(n), b=np.zeros(n),
                         c=np.zeros(n), d=np.zeros(n), N=g.N, kappa_ok=False, sm_count=148, device="cpu")
         assert t.fp8_compatible() is want
         if dtype == "fp8":
