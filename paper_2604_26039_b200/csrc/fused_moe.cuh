@@ -152,6 +152,7 @@ constexpr int kJobLog = 16;
 enum ProfSlot {
   kPrWaitEmpty = 0, kPrIssue, kMmaWaitFull, kMmaWaitAcc, kMmaWaitAct, kEpiWaitAcc, kEpiSwiglu,
   kEpiWaitChunk, kEpiScatter, kTotal, kItems, kEpiMeta, kPrWaitDep,
+  kLatTma, kLatRelease, kNumStages,  // RAMP_PROF_LAT builds: stage issue->landed, commit->slot free
   // globaltimer stamps (ns)
   kTsEntry = 16, kTsStart, kTsGathered, kTsProducerDone, kTsEpilogueDone, kTsEndArrive, kTsEndPass, kTsFinal,
   kNumProf = 32
@@ -184,8 +185,43 @@ struct CtrlSmem {
   int32_t epi_tok[128];
   float epi_w[128];
   int16_t pf_act[512];  // active experts of the speculative prefetch (E <= 512)
+#ifdef RAMP_PROF_LAT
+  unsigned long long t_issue[kMaxStages], t_commit[kMaxStages];
+#endif
 };
 static_assert(sizeof(CtrlSmem) <= kCtrlBytes, "control block overflow");
+
+// Kernel-shape fields of one config, packed in a word (staged in smem at entry).
+constexpr int kMaxStagedCfgs = 4096;  // 16 KB of the ring
+struct CfgFields {
+  int bm, ttn, stg, split_k, group_m, mode, kps, h3;
+};
+__device__ __forceinline__ uint32_t pack_cfg(const ramp_table_t& t, int i) {
+  const uint32_t bm = static_cast<uint32_t>(t.bm[i]);            // <= 256: 9 bits
+  const uint32_t ttn = static_cast<uint32_t>(t.ttn[i]) >> 7;     // 1, 2, 4
+  const uint32_t stg = static_cast<uint32_t>(t.stg[i]);          // <= 15
+  const uint32_t sk = static_cast<uint32_t>(t.split_k[i]);       // 1, 2, 4
+  const uint32_t gm = t.group_m[i] ? 1u : 0u;
+  const uint32_t mode = t.mode ? static_cast<uint32_t>(t.mode[i]) & 1u : static_cast<uint32_t>(kModeFused);
+  const int kv = t.kps ? t.kps[i] : 1;
+  const uint32_t kps = (kv == 2 || kv == 4) ? static_cast<uint32_t>(kv) : 1u;
+  const int hv = t.h3 ? t.h3[i] : 1;
+  const uint32_t h3 = (hv == 2 || hv == 4) ? static_cast<uint32_t>(hv) : 1u;
+  return (bm & 511u) | (ttn & 7u) << 9 | (stg & 15u) << 12 | (sk & 7u) << 16 | gm << 19 | mode << 20 |
+         kps << 21 | h3 << 24;
+}
+__device__ __forceinline__ CfgFields unpack_cfg(uint32_t w) {
+  CfgFields f;
+  f.bm = static_cast<int>(w & 511u);
+  f.ttn = static_cast<int>((w >> 9) & 7u) << 7;
+  f.stg = static_cast<int>((w >> 12) & 15u);
+  f.split_k = static_cast<int>((w >> 16) & 7u);
+  f.group_m = static_cast<int>((w >> 19) & 1u);
+  f.mode = static_cast<int>((w >> 20) & 1u);
+  f.kps = static_cast<int>((w >> 21) & 7u);
+  f.h3 = static_cast<int>((w >> 24) & 7u);
+  return f;
+}
 
 // Job decoding, identical in every role.
 template <int N>
@@ -298,6 +334,13 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(smem_u32(&cs.tmem_base));
+  // The dispatch table's kernel-shape fields, packed one word per config,
+  // staged in the (still unused) ring while the route kernel runs: once the
+  // selection is visible the geometry needs no second global round trip.
+  uint32_t* const cfg_words = reinterpret_cast<uint32_t*>(base + kCtrlBytes + kStageBytesScatter);
+  const bool staged_cfg = !p.inline_route && p.table.n_cfg <= kMaxStagedCfgs;
+  if (staged_cfg)
+    for (int i = threadIdx.x; i < p.table.n_cfg; i += blockDim.x) cfg_words[i] = pack_cfg(p.table, i);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -393,12 +436,14 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   if (ts && threadIdx.x == 0) ts[kTsStart] = globaltimer();
 
   // --- runtime tile config chosen by the dispatcher (no host round trip)
-  const int stg = p.table.stg[cfg];
+  const CfgFields cf = staged_cfg ? unpack_cfg(cfg_words[cfg]) : unpack_cfg(pack_cfg(p.table, cfg));
+  __syncthreads();  // the staged words are dead from here on (the ring is about to be filled)
+  const int stg = cf.stg;
   Geometry G;
-  G.mode = p.table.mode ? p.table.mode[cfg] : kModeFused;
-  G.bm = p.table.bm[cfg];
+  G.mode = cf.mode;
+  G.bm = cf.bm;
   G.bmN = bm_mma(G.bm);
-  const int ttn = p.table.ttn[cfg];
+  const int ttn = cf.ttn;
   G.nA = ttn >= 256 ? ttn / 128 : 1;  // ttn = 128: one tile = 64 gate rows + 64 up rows
   G.n_i = ttn / 2;
   G.stripes = p.I / G.n_i;
@@ -406,19 +451,19 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   G.n_hc = p.H / 128;
   G.kbH = p.H / kKb;
   G.kbI = p.I / kKb;
-  G.group_m = p.table.group_m[cfg];
-  G.sk = (G.mode == kModeSplit && p.table.split_k[cfg] > 1) ? p.table.split_k[cfg] : 1;
+  G.group_m = cf.group_m;
+  G.sk = (G.mode == kModeSplit && cf.split_k > 1) ? cf.split_k : 1;
   G.nJobA = G.n_mtiles * G.stripes * G.sk;
   G.n3 = 1;
-  if (!kFp8 && G.mode == kModeSplit && p.table.h3) {
-    const int h3 = p.table.h3[cfg];
+  if (!kFp8 && G.mode == kModeSplit) {
+    const int h3 = cf.h3;
     if ((h3 == 2 || h3 == 4) && h3 <= G.nA && G.n_hc % h3 == 0) G.n3 = h3;
   }
   G.n_hj = G.n_hc / G.n3;
   G.total = G.nJobA + (G.mode == kModeSplit ? G.n_mtiles * G.n_hj * G.sk : 0);
   G.dbl = !kFp8 && G.mode == kModeSplit && G.nA * G.bmN <= 256;
   // k-blocks per stage (BF16 only); every job's k-range must split into whole stages
-  G.kps = (!kFp8 && p.table.kps) ? p.table.kps[cfg] : 1;
+  G.kps = kFp8 ? 1 : cf.kps;
   if (G.kps != 2 && G.kps != 4) G.kps = 1;
   if ((G.kbH / G.sk) % G.kps != 0 || (G.mode == kModeSplit && (G.kbI / G.sk) % G.kps != 0)) G.kps = 1;
   const int bmN = G.bmN, nA = G.nA, kps = G.kps;
@@ -567,17 +612,27 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     ProfClock pc;
     pc.start();
     auto next = [&]() {
+#ifdef RAMP_PROF_LAT
+      if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(&cs.t_issue[stage]) = clock64();
+#endif
       if (++stage == (uint32_t)u_stg) {
         stage = 0;
         phase ^= 1;
       }
     };
+#ifdef RAMP_PROF_LAT
+    unsigned long long c_rel = 0;
+#endif
     auto acquire = [&]() {
       c_issue += pc.lap();
       mbar_wait(smem_u32(&cs.empty[stage]), phase ^ 1);
       c_wait += pc.lap();
+#ifdef RAMP_PROF_LAT
+      if (phase) c_rel += clock64() - *reinterpret_cast<volatile unsigned long long*>(&cs.t_commit[stage]);
+#endif
     };
     uint32_t js = 0, jph = 0;
+    bool first_job = true;
 #ifdef RAMP_JOBLOG
     int n_claimed = 0;
 #endif
@@ -586,8 +641,11 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     bool gathered = direct_x && !p.early_flag;
     while (true) {
       // claim the next job (dynamic, in global order) and publish it to the ring
-      int j = 0;
-      if (lane == 0) j = atomicAdd(p.job_counter, 1);
+      // the first job is static (job = CTA index: no claim round trip before
+      // the first loads); later ones are claimed past the static wave
+      int j = static_cast<int>(blockIdx.x);
+      if (!first_job && lane == 0) j = static_cast<int>(gridDim.x) + atomicAdd(p.job_counter, 1);
+      first_job = false;
       j = warp_uniform(j);
       if (j >= G.total) j = -1;
       mbar_wait(smem_u32(&cs.job_empty[js]), jph ^ 1);
@@ -751,9 +809,14 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             const uint32_t full = smem_u32(&cs.full[stage]);
             const uint32_t sb = ring_addr + stage * u_sbytes;
             mbar_arrive_expect_tx(full, tx);
-            for (int q = 0; q < u_kps; ++q)
-              for (int t = 0; t < n3; ++t)
-                tma_load_2d(sb + (q * n3 + t) * kSubTileBytes, tm_w2, full, (kb + q) * kKb, wrow + t * 128, pol_w);
+            if (n3 == 1) {  // the common case keeps its compile-time trip count
+              for (int q = 0; q < u_kps; ++q)
+                tma_load_2d(sb + q * kSubTileBytes, tm_w2, full, (kb + q) * kKb, wrow, pol_w);
+            } else {
+              for (int q = 0; q < u_kps; ++q)
+                for (int t = 0; t < n3; ++t)
+                  tma_load_2d(sb + (q * n3 + t) * kSubTileBytes, tm_w2, full, (kb + q) * kKb, wrow + t * 128, pol_w);
+            }
             if constexpr (kFp8)
               bulk_g2s(sb + kSubTileBytes + bmN * 128, p.w2_sf + (static_cast<int64_t>(wrow / 128) * G.kbI + kb) * 512,
                        512, full);
@@ -793,6 +856,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       pr[kPrIssue] = c_issue + pc.lap();
       pr[kPrWaitDep] = c_dep;
       pr[kTotal] = clock64() - t_begin;
+#ifdef RAMP_PROF_LAT
+      pr[kLatRelease] = c_rel;
+#endif
     }
     };
     // kps is chosen on the device per call: one compiled copy of the role per
@@ -826,15 +892,25 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     unsigned long long c_full = 0, c_acc = 0, c_act = 0, items = 0;
     ProfClock pc;
     pc.start();
+#ifdef RAMP_PROF_LAT
+    unsigned long long c_lat = 0, n_st = 0;
+#endif
     auto wait_full = [&]() -> uint32_t {
       pc.lap();
       mbar_wait(smem_u32(&cs.full[stage]), phase);
       c_full += pc.lap();
+#ifdef RAMP_PROF_LAT
+      c_lat += clock64() - *reinterpret_cast<volatile unsigned long long*>(&cs.t_issue[stage]);
+      ++n_st;
+#endif
       tc_fence_after();
       return ring_addr + stage * u_sbytes;
     };
     auto release = [&]() {
       if (elect_one()) mma_commit(smem_u32(&cs.empty[stage]));
+#ifdef RAMP_PROF_LAT
+      if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(&cs.t_commit[stage]) = clock64();
+#endif
       __syncwarp();
       if (++stage == (uint32_t)u_stg) {
         stage = 0;
@@ -938,6 +1014,13 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
               for (int k = 0; k < 4; ++k)
                 mma_mxf8(acc, da + ((k * 32) >> 4), db + ((k * 32) >> 4), idesc_mxf8(128, bmN, k), ((kb - kb0) | k) != 0,
                          (uint32_t(k) << 30) | (u_tmem + kSfCol), (uint32_t(k) << 30) | (u_tmem + kSfCol + 4));
+            } else if (n3 == 1) {  // the common case keeps its compile-time trip count
+              for (int q = 0; q < u_kps; ++q) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  mma_bf16(acc, da + ((q * kSubTileBytes + k * 32) >> 4), db + ((q * bmN * 128 + k * 32) >> 4), idesc,
+                           ((kb - kb0) | q | k) != 0);
+              }
             } else {
               for (int q = 0; q < u_kps; ++q)
                 for (int t = 0; t < n3; ++t) {
@@ -962,6 +1045,10 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       pr[kMmaWaitAcc] = c_acc;
       pr[kMmaWaitAct] = c_act;
       pr[kItems] = items;
+#ifdef RAMP_PROF_LAT
+      pr[kLatTma] = c_lat;
+      pr[kNumStages] = n_st;
+#endif
     }
     };
     // kps is chosen on the device per call: one compiled copy of the role per

@@ -65,7 +65,8 @@ if a.prof:
         for i, n in enumerate(tl) if np.all(pr[:, 16 + i] > 0)))
     print('route stamps (ns from start): hist %.0f dispatch %.0f scan+pad %.0f align %.0f done %.0f' % tuple(rt[i] - rt[0] for i in (1, 2, 5, 3, 4)))
     names = ["pr_wait_empty", "pr_issue", "mma_wait_full", "mma_wait_acc", "mma_wait_act", "epi_wait_acc",
-             "epi_swiglu", "epi_wait_chunk", "epi_scatter", "total", "items", "epi_meta", "pr_wait_dep"]
+             "epi_swiglu", "epi_wait_chunk", "epi_scatter", "total", "items", "epi_meta", "pr_wait_dep",
+             "lat_tma", "lat_release", "n_stages"]
     act = pr[:, 10] > 0
     print(f"S={S} cfg bm={a.bm} ttn={a.ttn} stg={a.stg}: {e0.elapsed_time(e1)*1000:.1f} us (with profiling)")
     for i, nme in enumerate(names):
