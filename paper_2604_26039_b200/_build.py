@@ -44,13 +44,15 @@ def _stale(target: Path, deps: list[Path]) -> bool:
 
 def build(verbose: bool = False, force: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
+    # development builds (timeline probes): RAMP_EXTRA_NVCC="-DRAMP_JOBLOG" etc.
+    extra = os.environ.get("RAMP_EXTRA_NVCC", "").split()
     headers = sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [PKG.parent / "include" / "ramp_b200.h"]
     objs = []
     for src in SOURCES:
         obj = BUILD / (Path(src).stem + ".o")
         objs.append(obj)
         if force or _stale(obj, [CSRC / src, *headers]):
-            cmd = [nvcc(), *ARCH, *COMMON, *PER_FILE.get(src, []), "-c", str(CSRC / src), "-o", str(obj)]
+            cmd = [nvcc(), *ARCH, *COMMON, *extra, *PER_FILE.get(src, []), "-c", str(CSRC / src), "-o", str(obj)]
             res = subprocess.run(cmd, capture_output=True, text=True)
             log = BUILD / (Path(src).stem + ".ptxas.log")
             log.write_text(res.stdout + res.stderr)

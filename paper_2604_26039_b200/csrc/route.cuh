@@ -12,6 +12,20 @@
 
 namespace ramp {
 
+// Development probe (-DRAMP_ROUTE_CLOCKS): thread 0 records clock64() at the
+// numbered points of the route block into prof[16 + k].
+#ifdef RAMP_ROUTE_CLOCKS
+__shared__ unsigned long long* g_rclk;  // shared: a global pointer load would stall each probe
+#define RCLK(k)                                                          \
+  do {                                                                   \
+    if (threadIdx.x == 0 && g_rclk) g_rclk[k] = clock64();               \
+  } while (0)
+#else
+#define RCLK(k) \
+  do {          \
+  } while (0)
+#endif
+
 constexpr int kRouteThreads = 1024;
 constexpr int kRouteWarps = kRouteThreads / 32;
 constexpr int kMaxExperts = 512;
@@ -40,6 +54,7 @@ struct RouteSmem {
   // dispatch table staged by cp.async at kernel entry (null: read from global)
   double *ca, *cb, *cc, *cd, *clam;
   int32_t *csk, *cubm_idx, *ctiles, *cubm;
+  int ubm_stride;  // cubm[u] was staged by lane 0 of warp u % ubm_stride (0: not staged)
 };
 
 __host__ __device__ inline int route_stage_cap(int E, int64_t n) {
@@ -74,6 +89,7 @@ __device__ inline RouteSmem carve_route_smem(unsigned char* base, int E, int64_t
   s.stage_cap = route_stage_cap(E, n);
   s.ca = s.cb = s.cc = s.cd = s.clam = nullptr;
   s.csk = s.cubm_idx = s.ctiles = s.cubm = nullptr;
+  s.ubm_stride = 0;
   if (route_cfg_staged(E, n, n_cfg)) {
     const uintptr_t c0 = (reinterpret_cast<uintptr_t>(s.stage + s.stage_cap) + 15) & ~static_cast<uintptr_t>(15);
     s.ca = reinterpret_cast<double*>(c0);
@@ -99,26 +115,56 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
                "l"(src)
                : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// x / d for x >= 0, d > 0: a shift when d is a power of two (every bm of the
+// B200 pools), else the integer division (the reference pools' even bm).
+// The route block runs one cold pass: a 30-instruction division chain per
+// expert and bm is latency on the critical path.
+__device__ __forceinline__ int div_pos(int x, int d) {
+  return (d & (d - 1)) == 0 ? (x >> (__ffs(d) - 1)) : x / d;
+}
 
-// Kernel entry: thread i copies config i's static fields (and warp u's lane 0
-// the distinct bm value u) into shared memory asynchronously -- no registers
-// stay live, and the global latency overlaps the histogram pass.
-__device__ inline void stage_table(const ramp_table_t& t, RouteSmem& s) {
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// with an L2 eviction-priority hint (the dispatch table is re-read every
+// layer call while the megakernel streams gigabytes of evict-first weights)
+__device__ __forceinline__ void cp_async4_hint(void* dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8_hint(void* dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src), "l"(pol)
+               : "memory");
+}
+
+// Kernel entry: thread i copies config i's static fields (and lane 0 of warp
+// u % ubm_stride the distinct bm value u -- the warp that reads it in
+// block_dispatch's M-tile loop, so no block barrier is needed before that
+// read) into shared memory asynchronously -- no registers stay live, and the
+// global latency overlaps the histogram pass.  The lines are marked
+// evict-last in L2 so the next layer call finds them there.
+__device__ inline void stage_table(const ramp_table_t& t, RouteSmem& s, int ubm_stride) {
   if (!s.ca) return;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   const int i = threadIdx.x;
   if (i < t.n_cfg) {
-    cp_async8(s.ca + i, t.a + i);
-    cp_async8(s.cb + i, t.b + i);
-    cp_async8(s.cc + i, t.c + i);
-    cp_async8(s.cd + i, t.d + i);
-    if (t.lam) cp_async8(s.clam + i, t.lam + i);
-    cp_async4(s.csk + i, t.split_k + i);
-    cp_async4(s.cubm_idx + i, t.ubm_index + i);
-    cp_async4(s.ctiles + i, t.ntile ? t.ntile + i : t.ttn + i);
+    cp_async8_hint(s.ca + i, t.a + i, pol);
+    cp_async8_hint(s.cb + i, t.b + i, pol);
+    cp_async8_hint(s.cc + i, t.c + i, pol);
+    cp_async8_hint(s.cd + i, t.d + i, pol);
+    if (t.lam) cp_async8_hint(s.clam + i, t.lam + i, pol);
+    cp_async4_hint(s.csk + i, t.split_k + i, pol);
+    cp_async4_hint(s.cubm_idx + i, t.ubm_index + i, pol);
+    cp_async4_hint(s.ctiles + i, t.ntile ? t.ntile + i : t.ttn + i, pol);
   }
   const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0 && w < t.n_ubm) cp_async4(s.cubm + w, t.ubm + w);
+  if ((threadIdx.x & 31) == 0)
+    #pragma unroll 1
+    for (int u = w; w < ubm_stride && u < t.n_ubm; u += ubm_stride) cp_async4_hint(s.cubm + u, t.ubm + u, pol);
+  s.ubm_stride = ubm_stride;
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
@@ -225,9 +271,11 @@ __device__ inline void block_count(const int32_t* __restrict__ ids, int64_t n, i
                                    int* bad, bool ids_in_smem = false) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (s.cached && !ids_in_smem)
-    for (int64_t i = tid; i < n; i += blockDim.x) s.ids[i] = __ldg(ids + i);
+        for (int64_t i = tid; i < n; i += blockDim.x) s.ids[i] = __ldg(ids + i);
   for (int x = tid; x < 32 * E; x += blockDim.x) s.cnt[x] = 0;
+  RCLK(1);
   __syncthreads();
+  RCLK(2);
   const int64_t seg = (n + kRouteWarps - 1) / kRouteWarps;
   const int64_t lo = warp * seg, hi = lo + seg < n ? lo + seg : n;
   for (int64_t c0 = lo; c0 < hi; c0 += 32) {
@@ -242,7 +290,9 @@ __device__ inline void block_count(const int32_t* __restrict__ ids, int64_t n, i
     }
     if (e >= 0) atomicAdd(s.cnt + e * 32 + warp, 1);  // counts commute: no ordering needed here
   }
+  RCLK(3);
   __syncthreads();
+  RCLK(4);
   for (int x = warp; x < E; x += kRouteWarps) {
     const int v = s.cnt[x * 32 + lane];
     int incl = v;
@@ -254,7 +304,9 @@ __device__ inline void block_count(const int32_t* __restrict__ ids, int64_t n, i
     s.cnt[x * 32 + lane] = incl - v;
     if (lane == 31) s.hist[x] = incl;
   }
+  RCLK(5);
   __syncthreads();
+  RCLK(6);
 }
 
 // --------------------------------------------------------------- dispatcher
@@ -269,6 +321,28 @@ __device__ inline bool argmin_better(const ArgMin& x, const ArgMin& y) {
   if (xn != yn) return xn;
   if (!xn && x.v != y.v) return x.v < y.v;
   return x.i < y.i;
+}
+
+// Warp-wide argmin_better over (v, i) with three redux.sync.min on 32-bit
+// words instead of five shuffle rounds: v maps to an order-preserving u64 key
+// (NaN -> 0, the minimum, as in np.argmin; -0.0 == +0.0 as in the compare
+// above), then the lowest index among the lanes holding the minimum key wins.
+__device__ __forceinline__ unsigned long long argmin_key(double v) {
+  if (isnan(v)) return 0ull;
+  if (v == 0.0) v = 0.0;
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ ArgMin warp_argmin(const ArgMin& x) {
+  const unsigned long long k = argmin_key(x.v);
+  const unsigned hi = static_cast<unsigned>(k >> 32), lo = static_cast<unsigned>(k);
+  const unsigned mhi = __reduce_min_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_min_sync(0xffffffffu, hi == mhi ? lo : 0xffffffffu);
+  const bool at_min = hi == mhi && lo == mlo;
+  const unsigned mi = __reduce_min_sync(0xffffffffu, at_min ? static_cast<unsigned>(x.i) : 0xffffffffu);
+  // the value is the one held by the winning lane (bit-identical to its v)
+  const int src = __ffs(__ballot_sync(0xffffffffu, at_min && static_cast<unsigned>(x.i) == mi)) - 1;
+  return ArgMin{__shfl_sync(0xffffffffu, x.v, src), static_cast<int>(mi)};
 }
 
 // Static fields of one config (the table is constant; only g depends on the
@@ -332,37 +406,41 @@ __device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_tabl
   // (m_tile_counts, ramp/routing.py:197-203).
   if (rs && rs->ca) cp_async_wait_all();  // this thread's staged fields have landed
   __syncwarp();
+  RCLK(7);
+  #pragma unroll 1
   for (int u = warp; u < t.n_ubm; u += nwarps) {
-    const int bm = (rs && rs->ca && u == warp) ? rs->cubm[u] : t.ubm[u];
-    long long acc = 0;
+    const int bm = (rs && rs->ca && rs->ubm_stride == nwarps) ? rs->cubm[u] : t.ubm[u];
+    unsigned acc = 0;  // <= n + E M-tiles
+#pragma unroll 4
     for (int e = lane; e < E; e += 32) {
       const int c = hist[e];
-      if (c > 0) acc += (c + bm - 1) / bm;
+      if (c > 0) acc += div_pos(c + bm - 1, bm);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    acc = __reduce_add_sync(0xffffffffu, acc);  // one redux instead of five shuffle rounds
     if (lane == 0) mt_smem[u] = acc;
+    if (u == warp) RCLK(24);
   }
-  // Active experts (only the B4 traffic grid needs them); parked in
-  // red_smem[31] (no static shared memory: the megakernel embeds this code
-  // and its dynamic allocation is already at the opt-in maximum).
-  if (t.lam && warp == nwarps - 1) {
-    int na = 0;
-    for (int e = lane; e < E; e += 32) na += hist[e] > 0 ? 1 : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) na += __shfl_xor_sync(0xffffffffu, na, o);
-    if (lane == 0) red_smem[31].i = na;
+  RCLK(23);
+  // Active experts (only the B4 traffic grid needs them): every warp of the
+  // group counts them itself (one redux), so no second barrier is needed.
+  unsigned na = 0;
+  if (t.lam) {
+#pragma unroll 4
+    for (int e = lane; e < E; e += 32) na += hist[e] > 0 ? 1u : 0u;
+    na = __reduce_add_sync(0xffffffffu, na);
   }
+  const double nact = static_cast<double>(na);
+  RCLK(8);
   group_sync(nwarps);
+  RCLK(9);
   stamp(12);
-  const double nact = t.lam ? static_cast<double>(red_smem[31].i) : 0.0;
-  group_sync(nwarps);  // everyone has read it before red_smem is reused below
 
   const double sm = static_cast<double>(t.sm_count);
   const double omega_max = t.omega_max > 0.0 ? t.omega_max : 0.2;
   ArgMin best{CUDART_INF, 0x7fffffff};
   int kept = 0;
   const long long smi = t.sm_count;
+  #pragma unroll 1
   for (int i = threadIdx.x; i < t.n_cfg; i += nwarps * 32) {
     const CfgRegs r = load_cfg(t, i, rs);
     const int sk = r.sk;
@@ -371,8 +449,19 @@ __device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_tabl
     const double gd = static_cast<double>(g);
     bool keep = true;
     // (an infinite threshold keeps every finite ratio: skip the divisions)
-    if (sk > 1)
-      keep = t.kappa_ok && (isinf(omega_max) || __ddiv_rn(__ddiv_rn(gd, static_cast<double>(sk)), sm) < omega_max);
+    if (sk > 1) {
+      if (omega_max == 0.2 && (sk & (sk - 1)) == 0 && g < (1ll << 40) && smi < (1ll << 20)) {
+        // Exact integer form of the fp64 gate: for a power-of-two split g/sk
+        // is exact, so the test is RN(q) < RN(0.2) with q = g/(sk*sm); a
+        // rational with a denominator < 2^30 is either exactly 1/5 or at
+        // least 1/(5*sk*sm) away from it, far beyond half an ulp, so this
+        // equals q < 1/5, i.e. 5g < sk*sm.
+        keep = t.kappa_ok && 5 * g < static_cast<long long>(sk) * smi;
+      } else {
+        keep = t.kappa_ok &&
+               (isinf(omega_max) || __ddiv_rn(__ddiv_rn(gd, static_cast<double>(sk)), sm) < omega_max);
+      }
+    }
     // B4: HBM-equivalent traffic grid (first M-tile of an expert streams its
     // weights from HBM, later ones re-read them at lam x the cost from L2)
     double gl = gd;
@@ -398,31 +487,26 @@ __device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_tabl
     const ArgMin cand{p, i};
     if (argmin_better(cand, best)) best = cand;
   }
+  RCLK(10);
   stamp(13);
   // only warps that evaluated a config take part in the reduction
   const int cfg_warps = min(nwarps, (t.n_cfg + 31) >> 5);
   if (warp < cfg_warps) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      ArgMin other{__shfl_xor_sync(0xffffffffu, best.v, o), __shfl_xor_sync(0xffffffffu, best.i, o)};
-      if (argmin_better(other, best)) best = other;
-      kept += __shfl_xor_sync(0xffffffffu, kept, o);
-    }
+    best = warp_argmin(best);
+    kept = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(kept));
     if (lane == 0) {
       red_smem[warp] = best;
       cnt_smem[warp] = kept;
     }
   }
+  RCLK(11);
   group_sync(nwarps);
+  RCLK(12);
   if (warp == 0) {
     ArgMin b = lane < cfg_warps ? red_smem[lane] : ArgMin{CUDART_INF, 0x7fffffff};
     int k = lane < cfg_warps ? cnt_smem[lane] : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      ArgMin other{__shfl_xor_sync(0xffffffffu, b.v, o), __shfl_xor_sync(0xffffffffu, b.i, o)};
-      if (argmin_better(other, b)) b = other;
-      k += __shfl_xor_sync(0xffffffffu, k, o);
-    }
+    b = warp_argmin(b);
+    k = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(k)));
     if (lane == 0) {
       red_smem[0] = b;
       cnt_smem[0] = k;
@@ -430,6 +514,7 @@ __device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_tabl
     }
   }
   group_sync(nwarps);
+  RCLK(13);
   stamp(14);
   const int sel = red_smem[0].i;
   group_sync(nwarps);
@@ -512,6 +597,22 @@ __device__ inline void block_walk_ranks(int64_t n, int E, RouteSmem& s, int firs
   }
 }
 
+// After the padded scan (s.off final, block barrier passed): the padding
+// slots of every expert's run get the sentinel n and every M-tile its expert,
+// written by the lanes of one warp per expert (an expert's padding is up to
+// bm - 1 slots: one thread per expert would serialise them).
+__device__ __forceinline__ void pad_and_tiles(int64_t n, int E, int bm, const RouteSmem& s, int32_t* dst,
+                                              int32_t* __restrict__ tile_expert) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int e = warp; e < E; e += kRouteWarps) {
+    const int o = s.off[e], end = s.off[e + 1];
+    if (o == end) continue;
+    for (int q = o + s.hist[e] + lane; q < end; q += 32) dst[q] = static_cast<int32_t>(n);
+    for (int tt = div_pos(o, bm) + lane; tt < div_pos(end, bm); tt += 32) tile_expert[tt] = e;
+  }
+}
+
 struct NoPublish {
   __device__ void operator()(int) const {}
 };
@@ -536,39 +637,43 @@ __device__ inline void block_place(int64_t n, int E, int bm, RouteSmem& s, int* 
   int padded = 0, c = 0;
   if (tid < E) {
     c = s.hist[tid];
-    padded = (c + bm - 1) / bm * bm;
+    padded = div_pos(c + bm - 1, bm) * bm;
   }
   int total = 0;
+  RCLK(14);
   const int off = block_exclusive_scan(padded, warp_tot, &total);
+  RCLK(15);
   // stage in shared memory when the list is long enough for scattered global
   // stores to cost more than the copy-out, and fits (total is block-uniform)
   const bool staged = n >= 2048 && total <= s.stage_cap;
   int32_t* const dst = staged ? s.stage : sorted_ids;
-  if (tid < E) {
-    s.off[tid] = off;
-    for (int q = off + c; q < off + padded; ++q) dst[q] = static_cast<int32_t>(n);
-    for (int tt = off / bm; tt < (off + padded) / bm; ++tt) tile_expert[tt] = tid;
-  }
+  if (tid < E) s.off[tid] = off;
   if (tid == 0) {
     s.off[E] = total;
     if (n_post_pad_out) *n_post_pad_out = total;
   }
+  RCLK(16);
   __syncthreads();
+  RCLK(17);
+  pad_and_tiles(n, E, bm, s, dst, tile_expert);
   stamp(5);
   on_offsets(total);
-  for (int64_t i = tid; i < n; i += blockDim.x) {
+  RCLK(18);
+    for (int64_t i = tid; i < n; i += blockDim.x) {
     const int v = s.ids[i];
     if (v >= 0) dst[s.off[v & ((1 << kRankShift) - 1)] + (v >> kRankShift)] = static_cast<int32_t>(i);
   }
+  RCLK(19);
   __syncthreads();
+  RCLK(20);
   if (staged) {
     // coalesced copy-out (sorted_ids is 16-byte aligned in the workspace)
     const bool vec = (reinterpret_cast<uintptr_t>(sorted_ids) & 15) == 0;
     const int n4 = vec ? total / 4 : 0;
     const int4* src4 = reinterpret_cast<const int4*>(s.stage);
     int4* dst4 = reinterpret_cast<int4*>(sorted_ids);
-    for (int q = tid; q < n4; q += blockDim.x) dst4[q] = src4[q];
-    for (int q = n4 * 4 + tid; q < total; q += blockDim.x) sorted_ids[q] = s.stage[q];
+        for (int q = tid; q < n4; q += blockDim.x) dst4[q] = src4[q];
+        for (int q = n4 * 4 + tid; q < total; q += blockDim.x) sorted_ids[q] = s.stage[q];
     __syncthreads();
   }
 }
@@ -592,20 +697,17 @@ __device__ inline void block_align(const int32_t* __restrict__ ids, int64_t n, i
   int padded = 0, c = 0;
   if (tid < E) {
     c = s.hist[tid];
-    padded = (c + bm - 1) / bm * bm;
+    padded = div_pos(c + bm - 1, bm) * bm;
   }
   int total = 0;
   const int off = block_exclusive_scan(padded, warp_tot, &total);
-  if (tid < E) {
-    s.off[tid] = off;
-    for (int q = off + c; q < off + padded; ++q) sorted_ids[q] = static_cast<int32_t>(n);
-    for (int tt = off / bm; tt < (off + padded) / bm; ++tt) tile_expert[tt] = tid;
-  }
+  if (tid < E) s.off[tid] = off;
   if (tid == 0) {
     s.off[E] = total;
     if (n_post_pad_out) *n_post_pad_out = total;
   }
   __syncthreads();
+  pad_and_tiles(n, E, bm, s, sorted_ids, tile_expert);
   stamp(5);
   on_offsets(total);
   const int nbits = bits_for(E);

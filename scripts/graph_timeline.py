@@ -27,20 +27,32 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--points", default="1:0.2,16:1.0,512:0.2")
 ap.add_argument("--cfg", default="-1", help="comma list of forced config ids (-1: dispatcher)")
 ap.add_argument("--flat", action="store_true", help="flat cost table over the current pool (forced configs only)")
+ap.add_argument("--fp8", action="store_true", help="Qwen3-30B-A3B MXFP8 path with its fitted table")
 a = ap.parse_args()
-geom = BASELINE_MODELS[MODEL]
+geom = BASELINE_MODELS["Qwen3-30B-A3B" if a.fp8 else MODEL]
 dev = torch.device("cuda")
-pool = enumerate_b200_configs(geom, HardwareModel.b200())
+pool = enumerate_b200_configs(geom, HardwareModel.b200(), dtype="fp8" if a.fp8 else "bf16")
 if a.flat:
     cols = pool.columns()
     n = len(pool)
     dtab = moe.DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
                            group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], kps=cols.get("kps"), h3=cols.get("h3"), a=np.ones(n), b=np.zeros(n),
                            c=np.zeros(n), d=np.zeros(n), N=geom.N, kappa_ok=True, sm_count=148, device=dev)
+elif a.fp8:
+    from paper_2604_26039_b200.cost_model import active_ids_of, parse_coeff_store, read_coeff_store
+    from paper_2604_26039_b200.dispatch import DispatchTable
+    from paper_2604_26039_b200.sweep import make_fp8_weights
+    store = read_coeff_store(ROOT / "paper_2604_26039_b200" / "data" / "coeffs_Qwen3-30B-A3B_b200_fp8.json")
+    _, sm, co = parse_coeff_store(store)
+    dtab = DispatchTable(model=geom.name, pool=pool, coefficients=co, sm_count=sm,
+                         active=active_ids_of(store)).device_table(device=dev)
 else:
     table, _ = load_table(geom, pool, HardwareModel.b200())
     dtab = table.device_table(device=dev)
-w1, w2 = make_weights(geom, seed=1, device=dev)
+if a.fp8:
+    wq = make_fp8_weights(geom, seed=1, device=dev)
+else:
+    w1, w2 = make_weights(geom, seed=1, device=dev)
 H, I = geom.K, geom.N // 2
 lib = _lib.load()
 side = torch.cuda.Stream()
@@ -80,7 +92,10 @@ for spec, forced in [(p, int(f)) for p in a.points.split(",") for f in a.cfg.spl
     out = torch.empty(S, H, dtype=torch.bfloat16, device=dev)
 
     def run(phases=3):
-        moe.fused_moe(x, w1, w2, w, ids, dtab, forced, out=out, workspace=ws, phases=phases)
+        if a.fp8:
+            moe.fused_moe_fp8(x, wq, w, ids, dtab, forced, out=out, workspace=ws, phases=phases)
+        else:
+            moe.fused_moe(x, w1, w2, w, ids, dtab, forced, out=out, workspace=ws, phases=phases)
 
     full, route, mega = graph(run), graph(lambda: run(1)), graph(lambda: run(2))
     t_full, t_route, t_mega = timeit(full), timeit(route), timeit(mega)
@@ -90,8 +105,11 @@ for spec, forced in [(p, int(f)) for p in a.points.split(",") for f in a.cfg.spl
     lib.ramp_set_profile_buffer(buf.data_ptr())
     gp = graph(run)
     lib.ramp_set_profile_buffer(None)
-    for _ in range(3):
+    for _ in range(2):
         gp.replay()
+    torch.cuda.synchronize()
+    buf.zero_()  # job-log rows of earlier replays would otherwise linger
+    gp.replay()
     torch.cuda.synchronize()
     hb = buf.cpu().numpy().astype(np.float64)
     allb = hb[:149 * 32].reshape(149, 32)
@@ -106,7 +124,11 @@ for spec, forced in [(p, int(f)) for p in a.points.split(",") for f in a.cfg.spl
           f"mega {t_mega:.2f}")
     print(f"   route stamps (us): hist {(rt[1]-t0)/1e3:.2f} dispatch {(rt[2]-t0)/1e3:.2f} "
           f"align {(rt[3]-t0)/1e3:.2f} done {(rt[4]-t0)/1e3:.2f}  [dispatch: mt {(rt[12]-t0)/1e3:.2f} "
-          f"eval {(rt[13]-t0)/1e3:.2f} reduced {(rt[14]-t0)/1e3:.2f}; align scan+pad {(rt[5]-t0)/1e3:.2f}]  cycles entry->dispatched {rt[7]-rt[6]:.0f}")
+          f"eval {(rt[13]-t0)/1e3:.2f} reduced {(rt[14]-t0)/1e3:.2f}; align scan+pad {(rt[5]-t0)/1e3:.2f}]  cycles entry->dispatched {rt[7]-rt[6]:.0f}"
+          + (f"  [first pass started {(rt[15]-t0)/1e3:.2f}]" if rt[15] > 0 else ""))
+    rc = hb[148 * 32 + 16:148 * 32 + 16 + 25]  # -DRAMP_ROUTE_CLOCKS build (spills into the job-log area)
+    if rc[0] > 0:  # clock64 points of the route block, cycles from entry
+        print("   route clocks: " + " ".join(f"{k}:{int(rc[k] - rc[0])}" for k in range(25) if rc[k] > 0))
     print(f"   timeline (us from route start, min/median/max over CTAs): {line}")
     # per-job log: phase-1 (kind 0) jobs are ids < nJobA
     npp = int(ws.sel[1].item())
