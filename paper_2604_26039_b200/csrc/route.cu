@@ -37,7 +37,9 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
 #endif
   // Warp specialisation (below): the dispatcher needs one thread per config;
   // the remaining warps walk the (bm-independent) alignment ranks meanwhile.
-  const int cfg_warps = (a.table.n_cfg + 31) >> 5;
+  // (at least one warp per distinct bm, up to 8: the M-tile counts per bm are
+  // then one parallel step instead of a serial loop on one warp)
+  const int cfg_warps = max((a.table.n_cfg + 31) >> 5, min(a.table.n_ubm, 8));
   const bool overlap = kDispatch && s.cached && cfg_warps <= kRouteWarps - 8;
   // the dispatch table is constant: start copying it to shared memory now
   if constexpr (kDispatch) stage_table(a.table, s, overlap ? cfg_warps : kRouteWarps);
@@ -125,7 +127,11 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
   RCLK(22);
   stamp(2);
   if (a.prof && threadIdx.x == 0) a.prof[7] = clock64();
-  const int bm = a.table.bm[sel];
+  // bm of the selection from the staged table (landed and visible: every
+  // staging thread waited in block_dispatch, and a block barrier followed);
+  // a step-cache hit skipped the dispatcher and reads it from global memory
+  const bool table_landed = kDispatch && s.ca && cached < 0;
+  const int bm = table_landed ? s.cubm[s.cubm_idx[sel]] : a.table.bm[sel];
   int32_t* n_post_pad = a.ctrl + 1;
   // Early hand-off: once the padded offsets and tile_expert[] are final, the
   // megakernel only needs the config, the M-tile map and its counters to
