@@ -36,6 +36,21 @@
 
 #include "../../include/ramp_b200.h"
 #include "inline_route.cuh"
+
+// Opt-in experimental paths, compiled only into development builds
+// (RAMP_EXTRA_NVCC="-DRAMP_WITH_INLINE_ROUTE -DRAMP_WITH_PREFETCH"): the
+// default kernel leaves their code out, since every unexecuted block between
+// the hot ones costs instruction fetches on each CTA's cold start.
+#ifdef RAMP_WITH_INLINE_ROUTE
+constexpr bool kInlineRoute = true;
+#else
+constexpr bool kInlineRoute = false;
+#endif
+#ifdef RAMP_WITH_PREFETCH
+constexpr bool kSpecPrefetch = true;
+#else
+constexpr bool kSpecPrefetch = false;
+#endif
 #include "launch.h"
 #include "ptx.cuh"
 
@@ -148,6 +163,20 @@ constexpr int64_t kPrefetchCap = 64ll << 20;  // half the 126 MB L2
 // compiled in only with -DRAMP_JOBLOG (diagnostic build)
 constexpr int kJobLog = 16;
 
+// Start-path stamps (kTsCfg..kTsClaimed) only in -DRAMP_START_STAMPS builds:
+// even predicated-off checks in the per-job paths shift the FP8 epilogue's
+// register allocation (measured +0.6-0.9 us per layer).
+#ifdef RAMP_START_STAMPS
+#define START_STAMP(cond, slot)                          \
+  do {                                                   \
+    if (ts && (cond)) ts[slot] = globaltimer();          \
+  } while (0)
+#else
+#define START_STAMP(cond, slot) \
+  do {                          \
+  } while (0)
+#endif
+
 // Diagnostic counters (cycles, per CTA) written when MoeParams::prof != null.
 enum ProfSlot {
   kPrWaitEmpty = 0, kPrIssue, kMmaWaitFull, kMmaWaitAcc, kMmaWaitAct, kEpiWaitAcc, kEpiSwiglu,
@@ -155,6 +184,9 @@ enum ProfSlot {
   kLatTma, kLatRelease, kNumStages,  // RAMP_PROF_LAT builds: stage issue->landed, commit->slot free
   // globaltimer stamps (ns)
   kTsEntry = 16, kTsStart, kTsGathered, kTsProducerDone, kTsEpilogueDone, kTsEndArrive, kTsEndPass, kTsFinal,
+  // start path: config known, first job's expert known, first TMA issued, (unused), first acc ready,
+  // producer role entered, first job claimed
+  kTsCfg, kTsFirstExpert, kTsFirstIssue, kTsUnused27, kTsFirstAcc, kTsRole, kTsClaimed,
   kNumProf = 32
 };
 
@@ -228,6 +260,16 @@ template <int N>
 struct KpsC {
   static constexpr int value = N;
 };
+
+// x / d for x >= 0, d > 0 (once per launch): a shift for powers of two (the
+// usual bm, stripe and split factors) instead of a ~25-instruction division.
+// (BF16 kernel only: in the FP8 kernel the changed register allocation costs
+// more in the epilogue than the divisions, measured +0.6-0.9 us per layer)
+template <bool kFp8>
+__device__ __forceinline__ int pdiv(int x, int d) {
+  if constexpr (kFp8) return x / d;
+  return (d & (d - 1)) == 0 ? (x >> (__ffs(d) - 1)) : x / d;
+}
 
 struct Job {
   int kind;  // 0 = phase 1(+2) of (m, s) [fused: +phase 3], 1 = split phase 3 of (m, hc)
@@ -338,14 +380,14 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   // staged in the (still unused) ring while the route kernel runs: once the
   // selection is visible the geometry needs no second global round trip.
   uint32_t* const cfg_words = reinterpret_cast<uint32_t*>(base + kCtrlBytes + kStageBytesScatter);
-  const bool staged_cfg = !p.inline_route && p.table.n_cfg <= kMaxStagedCfgs;
+  const bool staged_cfg = !(kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route)) && p.table.n_cfg <= kMaxStagedCfgs;
   if (staged_cfg)
     for (int i = threadIdx.x; i < p.table.n_cfg; i += blockDim.x) cfg_words[i] = pack_cfg(p.table, i);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = cs.tmem_base;
-  if (!kFp8 && p.pf_cap > 0 && warp == 3) {
+  if (!kFp8 && (kSpecPrefetch && p.pf_cap > 0) && warp == 3) {
     // Speculative L2 prefetch of the active experts' weights (W1 of every
     // active expert in id order -- the order the first wave of phase-1 jobs
     // reads them -- then W2), capped at pf_cap bytes and split evenly over
@@ -390,9 +432,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   }
   // Generation of this call's grid barriers (inline route); read before any
   // CTA can arrive anywhere, so every CTA sees the same value.
-  const int g0 = p.inline_route ? ld_acquire_gpu(p.gflag) : 0;
+  const int g0 = (kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route)) ? ld_acquire_gpu(p.gflag) : 0;
   int cfg, n_post_pad;
-  if (!kFp8 && p.inline_route) {
+  if (!kFp8 && (kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route))) {
     const InlineRouteResult rr = inline_route<kMoeThreads>(
         p.topk_ids, p.n_assign, p.E, p.top_k, p.forced_cfg, p.table, p.x, p.x_sorted, p.H,
         const_cast<int32_t*>(p.sorted_ids), p.tot, p.cursor, p.gcnt, p.gcnt + 1, p.gflag, g0,
@@ -438,6 +480,12 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   // --- runtime tile config chosen by the dispatcher (no host round trip)
   const CfgFields cf = staged_cfg ? unpack_cfg(cfg_words[cfg]) : unpack_cfg(pack_cfg(p.table, cfg));
   __syncthreads();  // the staged words are dead from here on (the ring is about to be filled)
+#ifdef RAMP_START_STAMPS
+  if (ts && threadIdx.x == 0) {
+    asm volatile("" ::"r"(cf.stg), "r"(n_post_pad));  // stamp after the loads resolved
+    ts[kTsCfg] = globaltimer();
+  }
+#endif
   const int stg = cf.stg;
   Geometry G;
   G.mode = cf.mode;
@@ -446,8 +494,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   const int ttn = cf.ttn;
   G.nA = ttn >= 256 ? ttn / 128 : 1;  // ttn = 128: one tile = 64 gate rows + 64 up rows
   G.n_i = ttn / 2;
-  G.stripes = p.I / G.n_i;
-  G.n_mtiles = n_post_pad / G.bm;
+  G.stripes = pdiv<kFp8>(p.I, G.n_i);
+  G.n_mtiles = pdiv<kFp8>(n_post_pad, G.bm);
   G.n_hc = p.H / 128;
   G.kbH = p.H / kKb;
   G.kbI = p.I / kKb;
@@ -459,13 +507,13 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     const int h3 = cf.h3;
     if ((h3 == 2 || h3 == 4) && h3 <= G.nA && G.n_hc % h3 == 0) G.n3 = h3;
   }
-  G.n_hj = G.n_hc / G.n3;
+  G.n_hj = pdiv<kFp8>(G.n_hc, G.n3);
   G.total = G.nJobA + (G.mode == kModeSplit ? G.n_mtiles * G.n_hj * G.sk : 0);
   G.dbl = !kFp8 && G.mode == kModeSplit && G.nA * G.bmN <= 256;
   // k-blocks per stage (BF16 only); every job's k-range must split into whole stages
   G.kps = kFp8 ? 1 : cf.kps;
   if (G.kps != 2 && G.kps != 4) G.kps = 1;
-  if ((G.kbH / G.sk) % G.kps != 0 || (G.mode == kModeSplit && (G.kbI / G.sk) % G.kps != 0)) G.kps = 1;
+  if (pdiv<kFp8>(G.kbH, G.sk) % G.kps != 0 || (G.mode == kModeSplit && pdiv<kFp8>(G.kbI, G.sk) % G.kps != 0)) G.kps = 1;
   const int bmN = G.bmN, nA = G.nA, kps = G.kps;
   const int sbytes = kFp8 ? stage_bytes_fp8(G.bm, ttn) : stage_bytes(G.bm, ttn, kps);
   const int tok_off = kps * nA * kSubTileBytes;  // token tiles follow the stage's weight boxes
@@ -485,7 +533,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   // Token blocks of <= 16 rows skip phase 0: their producer gathers the rows
   // straight from x with TMA gather4 (4 rows per instruction), so decode-size
   // calls need no grid barrier before the first MMA.
-  const bool direct_x = !kFp8 && bmN == 16 && !p.inline_route;
+  const bool direct_x = !kFp8 && bmN == 16 && !(kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route));
   if (p.early_flag && warp >= 2 && (kFp8 || !direct_x)) pdl_wait();  // sorted_ids are final
   if (kFp8 && warp >= 2) {
     // FP8: gather + quantise every row to MXFP8 (per-32 power-of-two scales)
@@ -533,7 +581,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     named_bar_sync(2, 32 * kGatherWarps);
     if (warp == 2 && lane == 0) atomicAdd(p.gbar, 1);
   }
-  if (!kFp8 && warp >= 2 && !direct_x && !p.inline_route) {
+  if (!kFp8 && warp >= 2 && !direct_x && !(kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route))) {
     constexpr int kGatherWarps = 6, kUnroll = 8;
     const int row_vec = p.H / 8;  // 16-byte vectors per row
     const int gw = blockIdx.x * kGatherWarps + (warp - 2), nw = gridDim.x * kGatherWarps;
@@ -632,7 +680,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
 #endif
     };
     uint32_t js = 0, jph = 0;
-    bool first_job = true;
+    bool first_job = true, first_stamp = true;
+    START_STAMP(lane == 0, kTsRole);
 #ifdef RAMP_JOBLOG
     int n_claimed = 0;
 #endif
@@ -665,8 +714,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         jl_row[1] = globaltimer();
       }
 #endif
+      START_STAMP(lane == 0 && first_stamp, kTsClaimed);
       const Job jb = G.job(j);
-      if (p.inline_route && !gathered) {
+      if ((kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route)) && !gathered) {
         // inline route: the M-tile -> expert map is written by the owner CTAs
         // before barrier C (weights cannot stream ahead of it in this mode)
         gen_wait(p.gflag, g0 + 2);
@@ -674,6 +724,12 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         gathered = true;
       }
       const int e = warp_uniform(__ldcg(p.tile_expert + jb.m));
+#ifdef RAMP_START_STAMPS
+      if (ts && lane == 0 && first_stamp) {
+        asm volatile("" ::"r"(e));
+        ts[kTsFirstExpert] = globaltimer();
+      }
+#endif
       const int row0 = jb.m * G.bm;
       if (jb.kind == 0) {
         const uint32_t tx1 = u_kps * (nA * kSubTileBytes + bmN * 128) + (kFp8 ? (nA + 1) * 512 : 0);
@@ -709,6 +765,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           if constexpr (kFp8)
             bulk_g2s(sb + sf_off + nA * 512, p.x_sf + (static_cast<int64_t>(jb.m) * G.kbH + kb) * 512, 512, full);
         };
+        START_STAMP(lane == 0 && first_stamp, kTsFirstIssue);  // first stage slot is free
+        first_stamp = false;
         for (int kb = kb0; kb < kb1; kb += u_kps) {
           acquire();
           if (elect_one()) {
@@ -738,7 +796,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             ++npend;
             if (npend == u_stg || kb + u_kps >= kb1) {
               pc.lap();
-              if (p.inline_route) {
+              if ((kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route))) {
                 gen_wait(p.gflag, g0 + 2);
               } else if (direct_x) {
                 pdl_wait();  // early hand-off: the route kernel has completed, sorted_ids are final
@@ -1097,6 +1155,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       named_bar_sync(1, 128);
       c_meta += pc.lap();
       mbar_wait(smem_u32(&cs.acc_full[r]), acc_cnt[r] & 1);
+      START_STAMP(jl == 0 && et == 0, kTsFirstAcc);
       ++acc_cnt[r];
       c_wacc += pc.lap();
       tc_fence_after();
@@ -1345,7 +1404,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
   if (threadIdx.x == 0) {
     if (ts) ts[kTsEndArrive] = globaltimer();
-    if (p.inline_route) {
+    if ((kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route))) {
       gen_arrive(p.gcnt + 2, p.gflag, g0 + 3);
       gen_wait(p.gflag, g0 + 3);
       // every CTA is done with this call's jobs: clear the per-call state
@@ -1376,7 +1435,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       a4[i] = z;
     }
   }
-  if (p.inline_route) {
+  if ((kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route))) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < p.E; e += gridDim.x * blockDim.x) {
       p.tot[e] = 0;
       p.cursor[e] = 0;

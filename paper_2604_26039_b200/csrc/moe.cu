@@ -14,6 +14,9 @@ namespace ramp {
 unsigned long long* g_prof_buffer = nullptr;
 
 int64_t prefetch_cap() {
+#ifndef RAMP_WITH_PREFETCH
+  return 0;  // not compiled into this build
+#endif
   static int64_t cap = [] {
     const char* v = getenv("RAMP_PREFETCH_MB");
     return (v ? atoll(v) : 0ll) << 20;
@@ -38,6 +41,9 @@ bool early_handoff_enabled() {
 }
 
 bool inline_route_enabled() {
+#ifndef RAMP_WITH_INLINE_ROUTE
+  return false;  // not compiled into this build
+#endif
   static bool on = [] {
     const char* v = getenv("RAMP_INLINE_ROUTE");
     return v ? atoi(v) != 0 : false;

@@ -116,9 +116,12 @@ for spec, forced in [(p, int(f)) for p in a.points.split(",") for f in a.cfg.spl
     jl = hb[149 * 32:].reshape(148, 16, 4)
     pr, rt = allb[:148], allb[148]
     t0 = rt[0]
-    tl = ["entry", "start", "gathered", "producer_done", "epilogue_done", "end_arrive", "end_pass", "final"]
-    line = "  ".join(f"{n} {np.min(pr[:, 16 + i] - t0) / 1e3:.1f}/{np.median(pr[:, 16 + i] - t0) / 1e3:.1f}/"
-                     f"{np.max(pr[:, 16 + i] - t0) / 1e3:.1f}" for i, n in enumerate(tl) if np.all(pr[:, 16 + i] > 0))
+    tl = ["entry", "start", "gathered", "producer_done", "epilogue_done", "end_arrive", "end_pass", "final",
+          "cfg", "first_expert", "first_issue", "unused", "first_acc", "role", "claimed"]
+    def q3(v):
+        v = (v[v > 0] - t0) / 1e3
+        return f"{np.min(v):.1f}/{np.median(v):.1f}/{np.max(v):.1f}" + ("" if len(v) == len(pr) else f"({len(v)})")
+    line = "  ".join(f"{n} {q3(pr[:, 16 + i])}" for i, n in enumerate(tl) if np.any(pr[:, 16 + i] > 0))
     print(f"S={S} beta={beta} active={hist.active_experts} cfg {cfg} (bm {c.bm} ttn {c.ttn} stg {c.stg} gm "
           f"{int(c.group_m)} mode {c.mode} sk {c.split_k}): full {t_full:.2f} us  route {t_route:.2f}  "
           f"mega {t_mega:.2f}")
