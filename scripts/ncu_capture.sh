@@ -22,4 +22,7 @@ done
 $NCU --set full --import-source on -k regex:route_kernel -s 2 -c 1 -o "$out/${tag}_route_s512_b0.5" -f \
   python scripts/ncu_point.py --S 512 --beta 0.5 --reps 3 > "$out/${tag}_route.log" 2>&1
 ncu -i "$out/${tag}_route_s512_b0.5.ncu-rep" --page details --csv > "$out/${tag}_route_s512_b0.5_details.csv" 2>/dev/null
+$NCU --set full --import-source on -k regex:route_kernel -s 2 -c 1 -o "$out/${tag}_route_s1_b0.2" -f \
+  python scripts/ncu_point.py --S 1 --beta 0.2 --reps 3 > "$out/${tag}_route1.log" 2>&1
+ncu -i "$out/${tag}_route_s1_b0.2.ncu-rep" --page details --csv > "$out/${tag}_route_s1_b0.2_details.csv" 2>/dev/null
 ls -la "$out" | grep "$tag"
