@@ -16,7 +16,9 @@ Rank r of a P-rank group owns experts [r*E/P, (r+1)*E/P).  One MoE layer:
 
 The exchanges are NCCL all-to-alls (torch.distributed.all_to_all_single over
 NVLink 5 / NVSwitch); the split sizes need one small host read of the
-per-destination counts (exchanged with an all-to-all of int64 counts first).
+per-destination counts (exchanged with an all-to-all of int64 counts first;
+the (token, rank) pairs come from a [world, S] mask whose nonzeros are read
+with the already-known size, so that read is the only device sync).
 The local computation is pluggable (`local_fn`), which lets the gloo CPU tests
 check the routing, packing and combine arithmetic against a dense oracle.
 """
@@ -63,15 +65,18 @@ def dispatch(x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor, E: i
     S, k = topk_ids.shape
     dev = x.device
     owner = expert_owner(topk_ids.long(), E, world)                     # [S, k]
-    # unique (token, rank) pairs, ordered by destination rank then token
-    key = owner * S + torch.arange(S, device=dev)[:, None]               # [S, k]
-    pairs = torch.unique(key.reshape(-1))                                # sorted => grouped by rank
-    pair_rank = torch.div(pairs, S, rounding_mode="floor")
-    pair_token = pairs % S
-    send_counts = torch.bincount(pair_rank, minlength=world)
+    # unique (token, rank) pairs as a [world, S] mask: its row-major nonzeros
+    # are ordered by destination rank then token (no sort, no device sync)
+    mask = torch.zeros(world, S, dtype=torch.bool, device=dev)
+    mask[owner, torch.arange(S, device=dev)[:, None].expand(S, k)] = True
+    send_counts = mask.sum(1)
     recv_counts = torch.empty_like(send_counts)
     dist.all_to_all_single(recv_counts, send_counts, group=group)
-    sc, rc = send_counts.tolist(), recv_counts.tolist()                  # the one host read
+    counts = torch.cat([send_counts, recv_counts]).tolist()              # the one host read
+    sc, rc = counts[:world], counts[world:]
+    pairs = torch.nonzero_static(mask.reshape(-1), size=sum(sc)).squeeze(1)
+    pair_rank = torch.div(pairs, S, rounding_mode="floor")
+    pair_token = pairs % S
     # per sent row: the token's assignments that live on that rank (others -> weight 0)
     row_owner = owner[pair_token]                                        # [P, k]
     hit = row_owner == pair_rank[:, None]
@@ -81,8 +86,6 @@ def dispatch(x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor, E: i
     send_x = x[pair_token].contiguous()
     R = sum(rc)
     H = x.shape[1]
-    recv_ids = torch.empty(R, k, dtype=torch.int64, device=dev)
-    recv_w = torch.empty(R, k, dtype=topk_w.dtype, device=dev)
     if wire == "fp8":
         from .quant import GROUP, mx_dequantize, mx_quantize
 
@@ -97,10 +100,20 @@ def dispatch(x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor, E: i
         recv_x = torch.empty(R, H, dtype=x.dtype, device=dev)
         dist.all_to_all_single(recv_x, send_x, rc, sc, group=group)
         wire_bytes = int(send_x.numel() * send_x.element_size())
-    dist.all_to_all_single(recv_ids, row_ids.contiguous(), rc, sc, group=group)
-    dist.all_to_all_single(recv_w, row_w.contiguous(), rc, sc, group=group)
+    if topk_w.dtype == torch.float32:
+        # local ids (int32) and weights (fp32 bits) travel as one [P, k, 2] int32 exchange
+        meta = torch.stack([row_ids.to(torch.int32), row_w.contiguous().view(torch.int32)], dim=-1).contiguous()
+        recv_meta = torch.empty(R, k, 2, dtype=torch.int32, device=dev)
+        dist.all_to_all_single(recv_meta, meta, rc, sc, group=group)
+        recv_ids = recv_meta[..., 0].contiguous()
+        recv_w = recv_meta[..., 1].contiguous().view(torch.float32)
+    else:
+        recv_ids = torch.empty(R, k, dtype=torch.int32, device=dev)
+        recv_w = torch.empty(R, k, dtype=topk_w.dtype, device=dev)
+        dist.all_to_all_single(recv_ids, row_ids.to(torch.int32).contiguous(), rc, sc, group=group)
+        dist.all_to_all_single(recv_w, row_w.contiguous(), rc, sc, group=group)
     plan = EPPlan(send_counts=sc, recv_counts=rc, order=pairs, pair_token=pair_token, wire_bytes=wire_bytes)
-    return plan, recv_x, recv_ids.to(torch.int32), recv_w
+    return plan, recv_x, recv_ids, recv_w
 
 
 def combine(plan: EPPlan, partial: torch.Tensor, S: int, group=None) -> torch.Tensor:
