@@ -59,7 +59,7 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
   if (a.publish_hist && a.hist_out && (threadIdx.x >> 5) == kRouteWarps - 1) {
     // publish the histogram now: the megakernel CTAs (already resident under
     // PDL) start prefetching the active experts' weights while we dispatch
-    #pragma unroll 1
+#pragma unroll 1
     for (int e = threadIdx.x & 31; e < a.E; e += 32) a.hist_out[e] = s.hist[e];
     __syncwarp();
     if ((threadIdx.x & 31) == 0) {
@@ -76,7 +76,7 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
   if (kDispatch && scache) {
     if (threadIdx.x < 32) {
       int m = 0;
-      #pragma unroll 1
+#pragma unroll 1
       for (int e = threadIdx.x; e < a.E; e += 32) m += s.hist[e];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
@@ -87,7 +87,7 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
         }
         const int nc = scache[2];
         int hit = -1;
-        #pragma unroll 1
+#pragma unroll 1
         for (int q = 0; q < nc; ++q)
           if (scache[3 + 2 * q] == m) hit = scache[4 + 2 * q];
         st.cnt[31] = hit;
@@ -164,7 +164,7 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
   }
   stamp(3);
   const int npp = s.off[a.E];
-  #pragma unroll 1
+#pragma unroll 1
   for (int e = threadIdx.x; e < a.E; e += blockDim.x)
     if (a.hist_out) a.hist_out[e] = s.hist[e];
   if (threadIdx.x == 0) {

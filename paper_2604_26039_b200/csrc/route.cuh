@@ -162,7 +162,7 @@ __device__ inline void stage_table(const ramp_table_t& t, RouteSmem& s, int ubm_
   }
   const int w = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0)
-    #pragma unroll 1
+#pragma unroll 1
     for (int u = w; w < ubm_stride && u < t.n_ubm; u += ubm_stride) cp_async4_hint(s.cubm + u, t.ubm + u, pol);
   s.ubm_stride = ubm_stride;
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -407,7 +407,7 @@ __device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_tabl
   if (rs && rs->ca) cp_async_wait_all();  // this thread's staged fields have landed
   __syncwarp();
   RCLK(7);
-  #pragma unroll 1
+#pragma unroll 1
   for (int u = warp; u < t.n_ubm; u += nwarps) {
     const int bm = (rs && rs->ca && rs->ubm_stride == nwarps) ? rs->cubm[u] : t.ubm[u];
     unsigned acc = 0;  // <= n + E M-tiles
@@ -440,7 +440,7 @@ __device__ inline int block_dispatch(const int32_t* hist, int E, const ramp_tabl
   ArgMin best{CUDART_INF, 0x7fffffff};
   int kept = 0;
   const long long smi = t.sm_count;
-  #pragma unroll 1
+#pragma unroll 1
   for (int i = threadIdx.x; i < t.n_cfg; i += nwarps * 32) {
     const CfgRegs r = load_cfg(t, i, rs);
     const int sk = r.sk;
