@@ -590,3 +590,51 @@ def test_device_step_cache():
     cache.advance()
     _, s3 = _run_fused(x, w1, w2, w, ids_b, cached, -1)
     assert s3[0] == sel_b[0] and s3[3] > 0, "a new step dispatches again"
+
+
+@pytest.mark.parametrize("reps", [1, 2])  # 2: a table past the overlap / shared-memory staging limits
+@pytest.mark.parametrize("case", ["all_equal", "nan", "tie", "signed_zero", "single_min_late"])
+def test_route_kernel_argmin_rules(case, reps):
+    """The route kernel's warp-redux argmin follows np.argmin on the masked
+    prediction vector (ramp/dispatch.py:118-119): NaN is the minimum, ties go
+    to the lowest index, -0.0 == +0.0; split-K configs are gated out when
+    kappa_ok is false.  Runs the route kernel alone (phases=1) on a table of
+    several hundred configs, so the reduction crosses warps."""
+    import torch
+
+    M = _M()
+    E, H, I, k, S = 16, 256, 256, 4, 6
+    from paper_2604_26039_b200.catalog import MoeGeometry
+    from paper_2604_26039_b200.config_space import enumerate_b200_configs
+
+    pool = enumerate_b200_configs(MoeGeometry(name="t", E=E, N=2 * I, K=H, top_k=k))
+    cols = {key: np.tile(v, reps) for key, v in pool.columns().items() if v is not None}
+    n = len(cols["bm"])
+    a = np.ones(n)
+    free = np.flatnonzero(cols["split_k"] == 1)  # configs the gate keeps
+    assert len(free) > 64
+    i0, i1, i2 = int(free[len(free) // 3]), int(free[len(free) // 2]), int(free[-1])
+    if case == "nan":
+        a[i1] = np.nan
+        a[i2] = 0.0
+    elif case == "tie":
+        a[i0] = a[i1] = 0.5
+    elif case == "signed_zero":
+        a[i1] = -0.0
+        a[i0] = 0.0
+    elif case == "single_min_late":
+        a[i2] = 0.75
+    table = M.DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
+                          group_m=cols["group_m"].astype(np.int64), mode=cols.get("mode"), kps=cols.get("kps"),
+                          h3=cols.get("h3"), a=a, b=0 * a, c=0 * a, d=0 * a, N=2 * I, kappa_ok=False, sm_count=148)
+    pred = np.where(cols["split_k"] > 1, np.inf, a + 0.0)
+    want = int(np.argmin(pred))
+    x, w1, w2, w, ids = random_moe(S, H, I, E, k, seed=3)
+    ws = M.Workspace(S, H, I, E, k)
+    M.fused_moe(torch.from_numpy(x).to("cuda", torch.bfloat16), torch.from_numpy(w1).to("cuda", torch.bfloat16),
+                torch.from_numpy(w2).to("cuda", torch.bfloat16), torch.from_numpy(w).cuda(),
+                torch.from_numpy(ids).cuda(), table, workspace=ws, phases=1)
+    torch.cuda.synchronize()
+    sel = ws.sel.cpu().numpy()
+    assert int(sel[0]) == want, (case, int(sel[0]), want)
+    assert int(sel[3]) == int(np.sum(cols["split_k"] == 1))  # evaluations = configs the gate kept
