@@ -432,8 +432,10 @@ def ep_leg(dev, world, rank, iters=10, warmup=3):
     torch.cuda.empty_cache()
     return {"workload": f"{EP_MODEL} MoE layer (E=256, top-8, d=7168, d_ff=2048) MXFP8, expert-parallel over "
                         f"{world} GPU(s): {per} experts/rank, {EP_TOKENS} tokens/rank, beta={EP_BETA}",
-            "exchange": f"NCCL all_to_all_single: token rows as {'MXFP8 (E4M3 + UE8M0 per 32)' if wire == 'fp8' else 'bf16'}"
-                        " + local ids/weights; combine of per-(token,rank) partial sums in bf16",
+            "exchange": ("none at world 1 (one rank owns every expert: the all-to-alls are identities and are "
+                         "skipped, no host read)") if world == 1 else
+                        (f"NCCL all_to_all_single: token rows as {'MXFP8 (E4M3 + UE8M0 per 32)' if wire == 'fp8' else 'bf16'}"
+                         " + local ids/weights; combine of per-(token,rank) partial sums in bf16"),
             "dispatch_wire_bytes_rank0": plan.wire_bytes,
             "dispatch_wire_bytes_if_bf16": int(len(plan.pair_token) * geom.K * 2),
             "world": world, "us_per_layer": us, "local_megakernel_us": local_us, "max_rows_per_rank": int(rows),

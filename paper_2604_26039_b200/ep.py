@@ -64,6 +64,19 @@ def dispatch(x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor, E: i
     per = E // world
     S, k = topk_ids.shape
     dev = x.device
+    if world == 1:
+        # One rank owns every expert: each token is one row and the exchanges
+        # are identities -- no collectives and no host read, so the layer
+        # stays asynchronous (the MXFP8 wire rounding is still applied, so
+        # the numerics match the multi-rank path).
+        pair_token = torch.arange(S, device=dev)
+        recv_x = x
+        if wire == "fp8":
+            from .quant import mx_dequantize, mx_quantize
+
+            recv_x = mx_dequantize(*mx_quantize(x)).to(x.dtype)
+        plan = EPPlan(send_counts=[S], recv_counts=[S], order=pair_token, pair_token=pair_token, wire_bytes=0)
+        return plan, recv_x, topk_ids.to(torch.int32), topk_w
     owner = expert_owner(topk_ids.long(), E, world)                     # [S, k]
     # unique (token, rank) pairs as a [world, S] mask: its row-major nonzeros
     # are ordered by destination rank then token (no sort, no device sync)
@@ -118,6 +131,8 @@ def dispatch(x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor, E: i
 
 def combine(plan: EPPlan, partial: torch.Tensor, S: int, group=None) -> torch.Tensor:
     """Return per-(token, rank) partial outputs to their origin and sum them."""
+    if dist.get_world_size(group) == 1:
+        return partial  # one row per token, already in token order
     back = torch.empty(sum(plan.send_counts), partial.shape[1], dtype=partial.dtype, device=partial.device)
     dist.all_to_all_single(back, partial.contiguous(), plan.send_counts, plan.recv_counts, group=group)
     out = torch.zeros(S, partial.shape[1], dtype=torch.float32, device=partial.device)

@@ -66,3 +66,18 @@ def test_ep_world2_matches_dense(E, S, k, wire):
         assert p.exitcode == 0
     for rank, err, scale in res:
         assert err <= 1e-4 * max(1.0, scale), (rank, err)
+
+
+@pytest.mark.parametrize("wire", ["bf16", "fp8"])
+def test_ep_world1_identity_path(wire):
+    """world_size 1: the exchange-free path equals the dense oracle."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    p = ctx.Process(target=_worker, args=(0, 1, port, 8, 11, 2, 32, 16, q, wire))
+    p.start()
+    rank, err, scale = q.get(timeout=120)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    assert err <= 1e-4 * max(1.0, scale), (rank, err)
+
