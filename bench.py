@@ -328,6 +328,19 @@ def mixtral_leg(dev):
                        device=dev)
     timer = MeasuredTimer(geom, flat, iters=3, device=dev)
     H, I = geom.K, geom.N // 2
+    # the fitted table (scripts/profile_b200.py --model Mixtral-8x7B), when shipped: the
+    # on-device dispatcher's pick over the whole pool, timed the same way
+    dtab = None
+    path = ROOT / "paper_2604_26039_b200" / "data" / f"coeffs_{MIX_MODEL}_b200.json"
+    if path.exists():
+        from paper_2604_26039_b200.cost_model import active_ids_of, parse_coeff_store, read_coeff_store
+        from paper_2604_26039_b200.dispatch import DispatchTable
+        from paper_2604_26039_b200.moe import Workspace, fused_moe
+
+        store = read_coeff_store(path)
+        _, sm, co = parse_coeff_store(store)
+        dtab = DispatchTable(model=MIX_MODEL, pool=pool, coefficients=co, sm_count=sm,
+                             active=active_ids_of(store)).device_table(device=dev)
     rows = []
     for S, beta in MIX_POINTS:
         hs = derive_seed(42, EVAL_HIST_DOMAIN, S, round(beta * 1000), 0)
@@ -342,11 +355,23 @@ def mixtral_leg(dev):
                      "tflops": round(6 * S * geom.top_k * H * I / t[i] / 1e6, 2), "gbs": round(nbytes / t[i] / 1e3, 1),
                      "best_without_split_k_us": round(float(no_sk), 2),
                      "cfg": {"id": c.id, "bm": c.bm, "ttn": c.ttn, "stg": c.stg, "split_k": c.split_k}})
+        if dtab is not None:
+            ws = Workspace(S, H, I, geom.E, geom.top_k, device=dev)
+            fused_moe(x, timer.w1, timer.w2, w, ids, dtab, -1, workspace=ws)
+            sel = dtab.pool_id(int(ws.sel[0].item()))
+            t_sel = float(timer.time_configs(x, ids, w, [sel])[0])
+            cs = pool.by_id(sel)
+            rows[-1]["dispatched"] = {"us": round(t_sel, 2), "vs_best_candidate": round(t_sel / float(t[i]), 4),
+                                      "cfg": {"id": cs.id, "bm": cs.bm, "ttn": cs.ttn, "stg": cs.stg,
+                                              "split_k": cs.split_k, "mode": cs.mode}}
     del timer
     torch.cuda.empty_cache()
     return {"workload": f"{MIX_MODEL} MoE layer (E=8, top-2, d=4096, d_ff=14336) BF16, large-K regime",
             "method": f"exhaustive search over {len(cand)} large-tile split-mode candidates per point "
-                      "(L2 flushed before each timed replay)", "points": rows}
+                      "(L2 flushed before each timed replay)"
+                      + ("; 'dispatched' = the on-device dispatcher's pick over the full pool with the fitted "
+                         f"table {path.name}, timed the same way" if dtab is not None else ""),
+            "points": rows}
 
 
 # ------------------------------------------------------------------ EP leg
