@@ -137,9 +137,16 @@ int ramp_dispatch_select(const int32_t* hist, int32_t E, const ramp_table_t* tab
  *   forced_cfg < 0   select on device from the live histogram (routing-aware)
  *   forced_cfg >= 0  run that config id (static dispatch / exhaustive sweep)
  *   sel_out          optional device int32[4]: {cfg, n_post_pad, n_work, n_eval}
- * workspace: >= ramp_fused_moe_workspace_size(...) bytes of device memory,
- *            zero-filled once before its first use (it carries the route
- *            kernel's completion flags between calls).
+ * workspace: >= ramp_fused_moe_workspace_size(S, ...) bytes of device memory,
+ *            zero-filled once before its first use.  The regions are laid out
+ *            for the largest S the buffer holds (not for this call's S), so a
+ *            workspace can serve every smaller batch; when the geometry
+ *            (H, I, E, top_k) or workspace_bytes change between calls on the
+ *            same buffer, the library re-zeroes it (stream-ordered memset)
+ *            before use.  int32 word 4 of the workspace is set to 1 by a call
+ *            whose topk_ids held an id outside [0, E) other than -1 (such
+ *            slots are skipped; the reference's ExpertHistogram raises
+ *            ValueError for them, ramp/routing.py:45-50).
  * Replaces the kernel that simulate_pool_times stands in for
  * (ramp/oracle.py:197-254) together with the select_config call before it. */
 size_t ramp_fused_moe_workspace_size(int32_t S, int32_t H, int32_t I, int32_t E, int32_t top_k);

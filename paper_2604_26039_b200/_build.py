@@ -44,7 +44,7 @@ def _stale(target: Path, deps: list[Path]) -> bool:
 
 def build(verbose: bool = False, force: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
-    # development builds (timeline probes): RAMP_EXTRA_NVCC="-DRAMP_JOBLOG" etc.
+    # development builds (timeline probes): RAMP_EXTRA_NVCC="-DRAMP_START_STAMPS" etc.
     extra = os.environ.get("RAMP_EXTRA_NVCC", "").split()
     headers = sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [PKG.parent / "include" / "ramp_b200.h"]
     objs = []

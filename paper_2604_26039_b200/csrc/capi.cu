@@ -4,7 +4,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "../../include/ramp_b200.h"
 #include "launch.h"
@@ -26,7 +28,7 @@ int cuda_fail(cudaError_t err, const char* where) {
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct WorkspaceLayout {
-  size_t ctrl, hist, sorted, tiles, done, acc, xs, act, acc_a, split_cnt, xq, xsf, actq, actsf, route, total;
+  size_t ctrl, hist, sorted, tiles, done, acc, xs, act, acc_a, split_cnt, xq, xsf, actq, actsf, total;
   int64_t capacity, rows;
 };
 
@@ -60,9 +62,59 @@ WorkspaceLayout layout_for(int32_t S, int32_t H, int32_t I, int32_t E, int32_t t
   w.xsf = take((size_t)mt_max * (H / 128 + 1) * 512);
   w.actq = take((size_t)w.rows * I);
   w.actsf = take((size_t)mt_max * (I / 128 + 1) * 512);
-  w.route = take(sizeof(int32_t) * 2 * (size_t)E);  // inline route: histogram + placement cursors
   w.total = off;
   return w;
+}
+
+// The layout a workspace of `bytes` bytes gets for a call of S tokens: the
+// regions are sized for the LARGEST token count the buffer holds, not for S,
+// so one workspace reused across batch sizes keeps every region at the same
+// offset and the zero-at-entry invariants of the read-and-clear regions
+// (fp32 output accumulator, split-K partials and counters) carry over from
+// call to call.  Returns total > bytes when even S does not fit.
+WorkspaceLayout layout_in(size_t bytes, int32_t S, int32_t H, int32_t I, int32_t E, int32_t top_k) {
+  WorkspaceLayout w = layout_for(S, H, I, E, top_k);
+  if (w.total > bytes) return w;
+  int64_t lo = S, hi = S > 0 ? S : 1;  // lo fits; grow hi until it does not
+  while (hi < (int64_t(1) << 28) && layout_for((int32_t)(2 * hi), H, I, E, top_k).total <= bytes) hi *= 2;
+  if (lo < hi) lo = hi;
+  hi = 2 * hi;  // does not fit (or is past the cap)
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) / 2;
+    if (layout_for((int32_t)mid, H, I, E, top_k).total <= bytes) lo = mid; else hi = mid;
+  }
+  return layout_for((int32_t)lo, H, I, E, top_k);
+}
+
+// A workspace whose layout key (geometry, size) changes between calls is
+// re-zeroed first: its regions move, and the new read-and-clear regions
+// would otherwise start on the old layout's data.  Tracked per buffer
+// address on the host (no device round trip; stream-ordered memset, which
+// is capturable).
+struct WsKey {
+  int32_t H, I, E, top_k;
+  size_t bytes;
+  bool operator==(const WsKey& o) const {
+    return H == o.H && I == o.I && E == o.E && top_k == o.top_k && bytes == o.bytes;
+  }
+};
+std::mutex g_ws_mu;
+std::unordered_map<const void*, WsKey> g_ws_keys;
+
+cudaError_t ensure_layout(void* ws, const WsKey& key, cudaStream_t st) {
+  bool reset = false;
+  {
+    std::lock_guard<std::mutex> g(g_ws_mu);
+    auto it = g_ws_keys.find(ws);
+    if (it == g_ws_keys.end()) {
+      if (g_ws_keys.size() > 4096) g_ws_keys.clear();
+      g_ws_keys.emplace(ws, key);  // first use: the caller zero-filled it (ABI contract)
+    } else if (!(it->second == key)) {
+      it->second = key;
+      reset = true;
+    }
+  }
+  return reset ? cudaMemsetAsync(ws, 0, key.bytes, st) : cudaSuccess;
 }
 
 int check_table(const ramp_table_t* t) {
@@ -165,12 +217,14 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
     return fail(RAMP_EINVAL, "null tensor");
   for (const void* p : {x, w1, w2, (const void*)out})
     if (reinterpret_cast<uintptr_t>(p) % 16 != 0) return fail(RAMP_EINVAL, "tensors must be 16-byte aligned");
-  const WorkspaceLayout L = layout_for(S, H, I, E, top_k);
+  const WorkspaceLayout L = layout_in(workspace_bytes, S, H, I, E, top_k);
   if (!workspace || workspace_bytes < L.total) return fail(RAMP_EINVAL, "workspace too small");
   if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
     return fail(RAMP_EINVAL, "workspace must be 256-byte aligned");
   auto* ws = static_cast<unsigned char*>(workspace);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaError_t err = ensure_layout(workspace, WsKey{H, I, E, top_k, workspace_bytes}, st); err != cudaSuccess)
+    return cuda_fail(err, "workspace reset");
   if (S == 0) {
     if (sel_out) {
       cudaError_t err = cudaMemsetAsync(sel_out, 0, 4 * sizeof(int32_t), st);
@@ -203,25 +257,13 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   ra.top_k = top_k;
   ra.pdl_early = ramp::pdl_mode() == 1;
   ra.pdl_prev = ramp::pdl_prev_enabled() ? 1 : 0;
-  // speculative weight prefetch (BF16): only when this call also runs the
-  // route kernel, which publishes the histogram early
-  // (decode sizes only: at prefill sizes the prefetch competes with the token
-  // gather for HBM and costs more than it hides, measured at S*k = 4096)
-  // The BF16 layer routes inside the megakernel (one launch); the FP8 path,
-  // router fusion and split-phase calls keep the separate route kernel.
-  const bool inline_route = !fp8 && !logits && phases == 3 && ramp::inline_route_enabled();
-  const bool prefetch = !inline_route && !fp8 && (phases & 1) && ramp::prefetch_cap() > 0 &&
-                        (int64_t)S * top_k <= 256;
-  ra.publish_hist = prefetch ? 1 : 0;
-  // early hand-off route -> megakernel (both launched by this call)
-  ra.early_flag = (phases == 3 && !inline_route && ramp::early_handoff_enabled()) ? ra.ctrl + 10 : nullptr;
   ra.logits = logits;
   ra.logits_bf16 = logits_bf16;
   ra.renorm = renorm;
   ra.w_out = w_out;
   const int zero_blocks = 0;
   cudaError_t err = cudaSuccess;
-  if ((phases & 1) && !inline_route) {
+  if (phases & 1) {
     err = ramp::launch_route(ra, zero_blocks, st);
     if (err != cudaSuccess) return cuda_fail(err, "route kernel");
   }
@@ -257,19 +299,6 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   ml.I = I;
   ml.E = E;
   ml.top_k = top_k;
-  ml.hist = ra.hist_out;
-  ml.pf_flag = ra.ctrl + 11;
-  ml.pf_cap = prefetch ? ramp::prefetch_cap() : 0;
-  ml.early_flag = ra.early_flag;
-  ml.inline_route = inline_route;
-  ml.forced_cfg = forced_cfg;
-  ml.topk_ids = topk_ids;
-  ml.tot = reinterpret_cast<int32_t*>(ws + L.route);
-  ml.cursor = ml.tot + E;
-  ml.gflag = ra.ctrl + 12;
-  ml.gcnt = ra.ctrl + 13;
-  ml.sel_out = sel_out;
-  ml.hist_out = ra.hist_out;
   const char* why = nullptr;
   err = ramp::launch_fused_moe(ml, st, &why);
   if (err != cudaSuccess) return why ? fail(RAMP_ECUDA, why) : cuda_fail(err, "fused_moe kernel");

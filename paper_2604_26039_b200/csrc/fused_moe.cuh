@@ -35,22 +35,7 @@
 #include <cstdint>
 
 #include "../../include/ramp_b200.h"
-#include "inline_route.cuh"
 
-// Opt-in experimental paths, compiled only into development builds
-// (RAMP_EXTRA_NVCC="-DRAMP_WITH_INLINE_ROUTE -DRAMP_WITH_PREFETCH"): the
-// default kernel leaves their code out, since every unexecuted block between
-// the hot ones costs instruction fetches on each CTA's cold start.
-#ifdef RAMP_WITH_INLINE_ROUTE
-constexpr bool kInlineRoute = true;
-#else
-constexpr bool kInlineRoute = false;
-#endif
-#ifdef RAMP_WITH_PREFETCH
-constexpr bool kSpecPrefetch = true;
-#else
-constexpr bool kSpecPrefetch = false;
-#endif
 #include "launch.h"
 #include "ptx.cuh"
 
@@ -133,35 +118,7 @@ struct MoeParams {
   ramp_table_t table;
   int32_t S, H, I, E, top_k, n_assign;
   unsigned long long* prof;    // optional per-CTA cycle counters [gridDim][16] (diagnostics)
-  unsigned long long* jlog;    // optional per-CTA job log [gridDim][kJobLog][4] (diagnostics)
-  // Speculative weight prefetch: the route kernel publishes the histogram
-  // (hist) and raises *pf_flag long before it finishes; the CTAs, already
-  // resident under PDL, pull the active experts' weights toward L2 meanwhile.
-  const int32_t* hist;         // [E]
-  const void* w1_base;         // raw expert weights (the TMA maps hold the same pointers)
-  const void* w2_base;
-  int32_t* pf_flag;            // raised by the route kernel, cleared at the end of this kernel
-  // Early hand-off from the route kernel (null: wait for its completion):
-  // raised once the config, tile_expert[] and the counters are final; the
-  // token-side consumers still wait for the route kernel's completion.
-  int32_t* early_flag;
-  int64_t pf_cap;              // bytes to prefetch at most (0: off)
-  // Inline route (inline_route.cuh): this kernel computes the histogram,
-  // dispatch and placement itself (no route kernel before it).
-  int32_t inline_route;
-  int32_t forced_cfg;
-  const int32_t* topk_ids;     // [n_assign]
-  int32_t* tot;                // [E] global histogram (cleared at the end of the call)
-  int32_t* cursor;             // [E] per-expert placement cursors (cleared at the end)
-  int32_t* gflag;              // generation flag of the grid barriers (monotonic)
-  int32_t* gcnt;               // [3] arrival counters: route A, gather C, end
-  int32_t* sel_out;            // optional [4]
-  int32_t* hist_out;           // optional [E]
 };
-constexpr int64_t kPrefetchCap = 64ll << 20;  // half the 126 MB L2
-// jobs logged per CTA: {job id, claimed, loads issued, epilogue done} (ns);
-// compiled in only with -DRAMP_JOBLOG (diagnostic build)
-constexpr int kJobLog = 16;
 
 // Start-path stamps (kTsCfg..kTsClaimed) only in -DRAMP_START_STAMPS builds:
 // even predicated-off checks in the per-job paths shift the FP8 epilogue's
@@ -216,7 +173,6 @@ struct CtrlSmem {
   int32_t fin;  // split-K: this CTA completed the (m, s) reduction
   int32_t epi_tok[128];
   float epi_w[128];
-  int16_t pf_act[512];  // active experts of the speculative prefetch (E <= 512)
 #ifdef RAMP_PROF_LAT
   unsigned long long t_issue[kMaxStages], t_commit[kMaxStages];
 #endif
@@ -380,101 +336,16 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   // staged in the (still unused) ring while the route kernel runs: once the
   // selection is visible the geometry needs no second global round trip.
   uint32_t* const cfg_words = reinterpret_cast<uint32_t*>(base + kCtrlBytes + kStageBytesScatter);
-  const bool staged_cfg = !(kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route)) && p.table.n_cfg <= kMaxStagedCfgs;
+  const bool staged_cfg = p.table.n_cfg <= kMaxStagedCfgs;
   if (staged_cfg)
     for (int i = threadIdx.x; i < p.table.n_cfg; i += blockDim.x) cfg_words[i] = pack_cfg(p.table, i);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = cs.tmem_base;
-  if (!kFp8 && (kSpecPrefetch && p.pf_cap > 0) && warp == 3) {
-    // Speculative L2 prefetch of the active experts' weights (W1 of every
-    // active expert in id order -- the order the first wave of phase-1 jobs
-    // reads them -- then W2), capped at pf_cap bytes and split evenly over
-    // the CTAs.  Starts as soon as the histogram is published, i.e. while the
-    // route kernel is still dispatching and aligning.
-    int spins = 0;
-    while (ld_acquire_gpu(p.pf_flag) == 0 && ++spins < (1 << 16)) __nanosleep(32);
-    if (spins < (1 << 16)) {
-      int16_t* act = cs.pf_act;
-      int n_act = 0;
-      for (int e0 = 0; e0 < p.E; e0 += 32) {
-        const int e = e0 + lane;
-        const bool a = e < p.E && __ldcg(p.hist + e) > 0;
-        const unsigned m = __ballot_sync(0xffffffffu, a);
-        if (a) act[n_act + __popc(m & ((1u << lane) - 1u))] = static_cast<int16_t>(e);
-        n_act += __popc(m);
-      }
-      __syncwarp();
-      const int64_t l1 = 2ll * p.I * p.H * 2, l2 = static_cast<int64_t>(p.H) * p.I * 2;
-      const int64_t total = static_cast<int64_t>(n_act) * (l1 + l2);
-      const int64_t cap = total < p.pf_cap ? total : p.pf_cap;
-      const int64_t per = (cap / gridDim.x + 4095) & ~4095ll;
-      const int64_t v0 = per * blockIdx.x, v1 = v0 + per < cap ? v0 + per : cap;
-      constexpr int64_t kChunk = 32 << 10;
-      const char* w1b = static_cast<const char*>(p.w1_base);
-      const char* w2b = static_cast<const char*>(p.w2_base);
-      for (int64_t v = v0 + lane * kChunk; v < v1; v += 32 * kChunk) {
-        int64_t len = v1 - v < kChunk ? v1 - v : kChunk;
-        const char* src;
-        if (v < n_act * l1) {
-          const int64_t k = v / l1, o = v % l1;
-          if (o + len > l1) len = l1 - o;
-          src = w1b + act[k] * l1 + o;
-        } else {
-          const int64_t w = v - n_act * l1, k = w / l2, o = w % l2;
-          if (o + len > l2) len = l2 - o;
-          src = w2b + act[k] * l2 + o;
-        }
-        bulk_prefetch_l2(src, static_cast<uint32_t>(len) & ~15u);
-      }
-    }
-  }
-  // Generation of this call's grid barriers (inline route); read before any
-  // CTA can arrive anywhere, so every CTA sees the same value.
-  const int g0 = (kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route)) ? ld_acquire_gpu(p.gflag) : 0;
-  int cfg, n_post_pad;
-  if (!kFp8 && (kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route))) {
-    const InlineRouteResult rr = inline_route<kMoeThreads>(
-        p.topk_ids, p.n_assign, p.E, p.top_k, p.forced_cfg, p.table, p.x, p.x_sorted, p.H,
-        const_cast<int32_t*>(p.sorted_ids), p.tot, p.cursor, p.gcnt, p.gcnt + 1, p.gflag, g0,
-        const_cast<int32_t*>(p.ctrl) + 4, const_cast<int32_t*>(p.tile_expert),
-        *reinterpret_cast<InlineRouteScratch*>(base + kCtrlBytes + kStageBytesScatter));
-    cfg = rr.cfg;
-    n_post_pad = rr.n_post_pad;
-    if (threadIdx.x == 0) {
-      gen_arrive(p.gcnt + 1, p.gflag, g0 + 2);  // rows gathered (the producers wait on it)
-      if (blockIdx.x == 0) {
-        int32_t* ctrl = const_cast<int32_t*>(p.ctrl);
-        ctrl[0] = cfg;
-        ctrl[1] = n_post_pad;
-        ctrl[2] = n_post_pad / p.table.bm[cfg];
-        ctrl[3] = rr.n_eval;
-        if (p.sel_out) {
-          p.sel_out[0] = cfg;
-          p.sel_out[1] = n_post_pad;
-          p.sel_out[2] = n_post_pad / p.table.bm[cfg];
-          p.sel_out[3] = rr.n_eval;
-        }
-      }
-    }
-    if (blockIdx.x == 0 && p.hist_out)
-      for (int e = threadIdx.x; e < p.E; e += blockDim.x)
-        p.hist_out[e] = reinterpret_cast<InlineRouteScratch*>(base + kCtrlBytes + kStageBytesScatter)->tot[e];
-    __syncthreads();  // the scratch (in the ring) is dead from here on
-  } else if (p.early_flag) {
-    // the config and M-tile map are published before the route kernel
-    // finishes placing the assignments: weights can start streaming now
-    if (threadIdx.x == 0)
-      while (ld_acquire_gpu(p.early_flag) == 0) __nanosleep(32);
-    __syncthreads();
-    cfg = __ldcg(p.ctrl);
-    n_post_pad = __ldcg(p.ctrl + 1);
-  } else {
-    pdl_wait();  // the route kernel's selection, alignment and gathered rows are now visible
-    cfg = p.ctrl[0];
-    n_post_pad = p.ctrl[1];
-  }
+  pdl_wait();  // the route kernel's selection and alignment are now visible
+  const int cfg = p.ctrl[0];
+  const int n_post_pad = p.ctrl[1];
   if (ts && threadIdx.x == 0) ts[kTsStart] = globaltimer();
 
   // --- runtime tile config chosen by the dispatcher (no host round trip)
@@ -533,8 +404,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   // Token blocks of <= 16 rows skip phase 0: their producer gathers the rows
   // straight from x with TMA gather4 (4 rows per instruction), so decode-size
   // calls need no grid barrier before the first MMA.
-  const bool direct_x = !kFp8 && bmN == 16 && !(kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route));
-  if (p.early_flag && warp >= 2 && (kFp8 || !direct_x)) pdl_wait();  // sorted_ids are final
+  const bool direct_x = !kFp8 && bmN == 16;
   if (kFp8 && warp >= 2) {
     // FP8: gather + quantise every row to MXFP8 (per-32 power-of-two scales)
     // into x_q and the per-M-tile scale atoms x_sf.
@@ -581,30 +451,12 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     named_bar_sync(2, 32 * kGatherWarps);
     if (warp == 2 && lane == 0) atomicAdd(p.gbar, 1);
   }
-  if (!kFp8 && warp >= 2 && !direct_x && !(kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route))) {
+  if (!kFp8 && warp >= 2 && !direct_x) {
     constexpr int kGatherWarps = 6, kUnroll = 8;
     const int row_vec = p.H / 8;  // 16-byte vectors per row
     const int gw = blockIdx.x * kGatherWarps + (warp - 2), nw = gridDim.x * kGatherWarps;
     const int4* xv = reinterpret_cast<const int4*>(p.x);
     int4* dv = reinterpret_cast<int4*>(p.x_sorted);
-#ifdef RAMP_AB_OLD_GATHER
-    for (int r = gw; r < n_post_pad; r += nw) {
-      const int asg = p.sorted_ids[r];
-      int4* d = dv + static_cast<int64_t>(r) * row_vec;
-      const int4* src = xv + static_cast<int64_t>(asg < p.n_assign ? asg / p.top_k : 0) * row_vec;
-      for (int c0 = lane; c0 < row_vec; c0 += 32 * kUnroll) {
-        int4 v[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          v[u] = make_int4(0, 0, 0, 0);
-          if (asg < p.n_assign && c0 + 32 * u < row_vec) v[u] = __ldg(src + c0 + 32 * u);
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u)
-          if (c0 + 32 * u < row_vec) d[c0 + 32 * u] = v[u];
-      }
-    }
-#else
     // This warp's rows are gw, gw + nw, ...: one coalesced load fetches the
     // assignments of the next 32 of them (no per-row dependent load), and two
     // rows move per iteration (16 x 16 B in flight per lane).
@@ -639,7 +491,6 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         }
       }
     }
-#endif
     __threadfence();
     named_bar_sync(2, 32 * kGatherWarps);
     if (warp == 2 && lane == 0) atomicAdd(p.gbar, 1);
@@ -682,12 +533,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     uint32_t js = 0, jph = 0;
     bool first_job = true, first_stamp = true;
     START_STAMP(lane == 0, kTsRole);
-#ifdef RAMP_JOBLOG
-    int n_claimed = 0;
-#endif
-    // direct_x reads sorted_ids itself: under the early hand-off it defers its
-    // token loads until the route kernel has completed
-    bool gathered = direct_x && !p.early_flag;
+    // direct_x gathers its token rows straight from x (no phase-0 barrier)
+    bool gathered = direct_x;
     while (true) {
       // claim the next job (dynamic, in global order) and publish it to the ring
       // the first job is static (job = CTA index: no claim round trip before
@@ -705,24 +552,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       __syncwarp();
       if (++js == 4) { js = 0; jph ^= 1; }
       if (j < 0) break;
-#ifdef RAMP_JOBLOG
-      unsigned long long* jl_row =
-          (p.jlog && n_claimed < kJobLog) ? p.jlog + (static_cast<size_t>(blockIdx.x) * kJobLog + n_claimed) * 4 : nullptr;
-      ++n_claimed;
-      if (jl_row && lane == 0) {
-        jl_row[0] = static_cast<unsigned long long>(j);
-        jl_row[1] = globaltimer();
-      }
-#endif
       START_STAMP(lane == 0 && first_stamp, kTsClaimed);
       const Job jb = G.job(j);
-      if ((kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route)) && !gathered) {
-        // inline route: the M-tile -> expert map is written by the owner CTAs
-        // before barrier C (weights cannot stream ahead of it in this mode)
-        gen_wait(p.gflag, g0 + 2);
-        fence_proxy_async_global();
-        gathered = true;
-      }
       const int e = warp_uniform(__ldcg(p.tile_expert + jb.m));
 #ifdef RAMP_START_STAMPS
       if (ts && lane == 0 && first_stamp) {
@@ -796,13 +627,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             ++npend;
             if (npend == u_stg || kb + u_kps >= kb1) {
               pc.lap();
-              if ((kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route))) {
-                gen_wait(p.gflag, g0 + 2);
-              } else if (direct_x) {
-                pdl_wait();  // early hand-off: the route kernel has completed, sorted_ids are final
-              } else {
-                while (ld_acquire_gpu(p.gbar) < (int)gridDim.x) __nanosleep(32);
-              }
+              while (ld_acquire_gpu(p.gbar) < (int)gridDim.x) __nanosleep(32);
               fence_proxy_async_global();
               c_dep += pc.lap();
               gathered = true;
@@ -903,9 +728,6 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           next();
         }
       }
-#ifdef RAMP_JOBLOG
-      if (jl_row && lane == 0) jl_row[2] = globaltimer();
-#endif
     }
     if (p.prof && lane == 0) {
       unsigned long long* pr = p.prof + blockIdx.x * kNumProf;
@@ -921,11 +743,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     };
     // kps is chosen on the device per call: one compiled copy of the role per
     // value (a runtime trip count in these loops costs ~30 % of the issue rate)
-#ifdef RAMP_AB_ONE_ROLE
-    if constexpr (true) {
-#else
     if constexpr (kFp8) {
-#endif
       role(KpsC<1>{});
     } else if (kps == 4) {
       role(KpsC<4>{});
@@ -1111,11 +929,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     };
     // kps is chosen on the device per call: one compiled copy of the role per
     // value (a runtime trip count in these loops costs ~30 % of the issue rate)
-#ifdef RAMP_AB_ONE_ROLE
-    if constexpr (true) {
-#else
     if constexpr (kFp8) {
-#endif
       role(KpsC<1>{});
     } else if (kps == 4) {
       role(KpsC<4>{});
@@ -1126,7 +940,6 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     }
   } else if (warp >= 4) {
     // ============================ epilogue ===============================
-    if (p.early_flag) pdl_wait();  // the epilogue reads sorted_ids: wait for the route kernel
     const int et = threadIdx.x - 128;  // TMEM lane == weight row of the 128-row MMA tile
     const uint32_t lane_off = static_cast<uint32_t>(et & ~31) << 16;
     uint32_t jl = 0, acc_cnt[2] = {0, 0}, chunk_cnt[2] = {0, 0};
@@ -1376,10 +1189,6 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         }
         c_scatter += pc.lap();
       }
-#ifdef RAMP_JOBLOG
-      if (p.jlog && et == 0 && jl < (uint32_t)kJobLog)
-        p.jlog[(static_cast<size_t>(blockIdx.x) * kJobLog + jl) * 4 + 3] = globaltimer();
-#endif
     }
     if (p.prof && et == 0) {
       unsigned long long* pr = p.prof + blockIdx.x * kNumProf;
@@ -1404,18 +1213,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
   if (threadIdx.x == 0) {
     if (ts) ts[kTsEndArrive] = globaltimer();
-    if ((kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route))) {
-      gen_arrive(p.gcnt + 2, p.gflag, g0 + 3);
-      gen_wait(p.gflag, g0 + 3);
-      // every CTA is done with this call's jobs: clear the per-call state
-      if (blockIdx.x == 0) atomicExch(p.job_counter, 0);
-    } else {
-      atomicAdd(p.gbar + 1, 1);
-      while (ld_acquire_gpu(p.gbar + 1) < (int)gridDim.x) __nanosleep(64);
-    }
-    // every CTA is past its prologue: re-arm the prefetch / hand-off flags for the next call
-    if (blockIdx.x == 0 && p.pf_flag) *p.pf_flag = 0;
-    if (blockIdx.x == 0 && p.early_flag) *p.early_flag = 0;
+    atomicAdd(p.gbar + 1, 1);
+    while (ld_acquire_gpu(p.gbar + 1) < (int)gridDim.x) __nanosleep(64);
     if (ts) ts[kTsEndPass] = globaltimer();
   }
   __syncthreads();
@@ -1434,14 +1233,6 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       o2[i] = pk;
       a4[i] = z;
     }
-  }
-  if ((kFp8 ? p.inline_route != 0 : (kInlineRoute && p.inline_route))) {
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < p.E; e += gridDim.x * blockDim.x) {
-      p.tot[e] = 0;
-      p.cursor[e] = 0;
-    }
-    const int n_mt = n_post_pad / G.bm;
-    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < n_mt; m += gridDim.x * blockDim.x) p.done[m] = 0;
   }
   if (ts && threadIdx.x == 0) ts[kTsFinal] = globaltimer();
 }

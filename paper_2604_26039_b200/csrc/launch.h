@@ -32,8 +32,6 @@ struct RouteArgs {
   const void* x;         // [S, H] bf16 tokens
   void* x_sorted;        // [rows, H] bf16, gathered by the helper blocks (null: skip)
   int32_t S, H, top_k;
-  int32_t publish_hist;  // write hist_out and raise ctrl[11] right after the histogram pass
-  int32_t* early_flag;   // raised (1) once config, tile_expert and counters are final (null: off)
   int32_t pdl_prev;      // launched as a PDL secondary of the previous kernel (waits before reading)
   int32_t pdl_early;     // trigger the dependent launch at entry (1) or after the alignment (0)
   // router fusion: when logits != null the route kernel first computes the
@@ -44,7 +42,6 @@ struct RouteArgs {
 };
 
 int pdl_mode();          // RAMP_PDL: 0 off, 1 trigger at route entry (default), 2 trigger at route exit
-int64_t prefetch_cap();  // RAMP_PREFETCH_MB: speculative weight prefetch budget (default 0 = off)
 
 cudaError_t launch_route(const RouteArgs& a, int zero_blocks, cudaStream_t stream);
 cudaError_t launch_align(const int32_t* ids, int64_t n, int E, int bm, int32_t* hist, int32_t* sorted_ids,
@@ -79,25 +76,9 @@ struct MoeLaunch {
   int64_t rows;     // capacity of x_sorted / act_g
   ramp_table_t table;
   int32_t S, H, I, E, top_k;
-  const int32_t* hist;  // speculative prefetch: published histogram, flag, byte cap (0 = off)
-  int32_t* pf_flag;
-  int64_t pf_cap;
-  int32_t* early_flag;  // the route kernel's early hand-off flag (null: wait for its completion)
-  // inline route (the megakernel routes itself; no route kernel, no PDL)
-  bool inline_route;
-  int32_t forced_cfg;
-  const int32_t* topk_ids;
-  int32_t* tot;
-  int32_t* cursor;
-  int32_t* gflag;
-  int32_t* gcnt;
-  int32_t* sel_out;
-  int32_t* hist_out;
 };
 
 bool pdl_prev_enabled();       // RAMP_PDL_PREV (default 0, measured neutral): route as PDL secondary of the previous kernel
-bool early_handoff_enabled();  // RAMP_EARLY (default 0: measured neutral)
-bool inline_route_enabled();  // RAMP_INLINE_ROUTE (default 0: the separate route kernel measured faster)
 
 extern unsigned long long* g_prof_buffer;  // diagnostics, see ramp_set_profile_buffer
 

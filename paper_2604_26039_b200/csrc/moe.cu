@@ -13,39 +13,9 @@ namespace ramp {
 
 unsigned long long* g_prof_buffer = nullptr;
 
-int64_t prefetch_cap() {
-#ifndef RAMP_WITH_PREFETCH
-  return 0;  // not compiled into this build
-#endif
-  static int64_t cap = [] {
-    const char* v = getenv("RAMP_PREFETCH_MB");
-    return (v ? atoll(v) : 0ll) << 20;
-  }();
-  return cap;
-}
-
 bool pdl_prev_enabled() {
   static bool on = [] {
     const char* v = getenv("RAMP_PDL_PREV");
-    return v ? atoi(v) != 0 : false;
-  }();
-  return on;
-}
-
-bool early_handoff_enabled() {
-  static bool on = [] {
-    const char* v = getenv("RAMP_EARLY");
-    return v ? atoi(v) != 0 : false;
-  }();
-  return on;
-}
-
-bool inline_route_enabled() {
-#ifndef RAMP_WITH_INLINE_ROUTE
-  return false;  // not compiled into this build
-#endif
-  static bool on = [] {
-    const char* v = getenv("RAMP_INLINE_ROUTE");
     return v ? atoi(v) != 0 : false;
   }();
   return on;
@@ -248,22 +218,6 @@ cudaError_t launch_fused_moe(const MoeLaunch& l, cudaStream_t stream, const char
   p.top_k = l.top_k;
   p.n_assign = l.S * l.top_k;
   p.prof = g_prof_buffer;
-  p.jlog = g_prof_buffer ? g_prof_buffer + 149 * 32 : nullptr;
-  p.hist = l.hist;
-  p.w1_base = l.w1;
-  p.w2_base = l.w2;
-  p.pf_flag = l.pf_flag;
-  p.pf_cap = l.pf_cap;
-  p.early_flag = l.early_flag;
-  p.inline_route = l.inline_route ? 1 : 0;
-  p.forced_cfg = l.forced_cfg;
-  p.topk_ids = l.topk_ids;
-  p.tot = l.tot;
-  p.cursor = l.cursor;
-  p.gflag = l.gflag;
-  p.gcnt = l.gcnt;
-  p.sel_out = l.sel_out;
-  p.hist_out = l.hist_out;
   // Programmatic dependent launch: the megakernel's prologue (barrier init,
   // TMEM allocation, descriptor prefetch) may overlap the route kernel's tail.
   cudaLaunchAttribute pdl[1];
@@ -275,8 +229,7 @@ cudaError_t launch_fused_moe(const MoeLaunch& l, cudaStream_t stream, const char
   cfg.dynamicSmemBytes = kSmemLimit;
   cfg.stream = stream;
   cfg.attrs = pdl;
-  // the inline route has no primary kernel to overlap with
-  cfg.numAttrs = (pdl_mode() && !l.inline_route) ? 1 : 0;
+  cfg.numAttrs = pdl_mode() ? 1 : 0;
   err = l.fp8 ? cudaLaunchKernelEx(&cfg, fused_moe_kernel<true>, maps, p)
               : cudaLaunchKernelEx(&cfg, fused_moe_kernel<false>, maps, p);
   if (err != cudaSuccess) return err;

@@ -56,17 +56,6 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
   __syncthreads();
   block_count(a.topk_ids, a.n_assign, a.E, s, &st.bad, kGating);
   stamp(1);
-  if (a.publish_hist && a.hist_out && (threadIdx.x >> 5) == kRouteWarps - 1) {
-    // publish the histogram now: the megakernel CTAs (already resident under
-    // PDL) start prefetching the active experts' weights while we dispatch
-#pragma unroll 1
-    for (int e = threadIdx.x & 31; e < a.E; e += 32) a.hist_out[e] = s.hist[e];
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) {
-      __threadfence();
-      st_release_gpu(a.ctrl + 11, 1);
-    }
-  }
   int sel = a.forced_cfg;
   int n_eval = 0;
   // Device StepCache (ramp/dispatch.py:40-54): a selection cached for this
@@ -133,10 +122,8 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
   const bool table_landed = kDispatch && s.ca && cached < 0;
   const int bm = table_landed ? s.cubm[s.cubm_idx[sel]] : a.table.bm[sel];
   int32_t* n_post_pad = a.ctrl + 1;
-  // Early hand-off: once the padded offsets and tile_expert[] are final, the
-  // megakernel only needs the config, the M-tile map and its counters to
-  // start streaming weights; the placement of the assignments (and the token
-  // gather behind it) follows.
+  // Once the padded offsets and tile_expert[] are final: the selection
+  // record and the megakernel's per-call counters.
   auto publish = [&](int npp) {
     const int ntiles = div_pos(npp, bm);
     if (a.done)
@@ -149,11 +136,6 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
       a.ctrl[7] = 0;  // megakernel job counter
       a.ctrl[8] = 0;  // megakernel grid barrier 0 (rows gathered)
       a.ctrl[9] = 0;  // megakernel grid barrier 1 (all jobs reduced)
-    }
-    if (a.early_flag) {
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) st_release_gpu(a.early_flag, 1);
     }
   };
   if (kDispatch && overlap) {
@@ -189,13 +171,6 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
 template <bool kGating, bool kDispatch>
 __global__ void __launch_bounds__(kRouteThreads, 1)
     route_kernel(const RouteArgs a) {
-#ifdef RAMP_ROUTE_TWICE
-  // development probe: a first (idempotent) pass warms the instruction cache;
-  // slot 15 keeps the true kernel start
-  if (a.prof && threadIdx.x == 0) a.prof[15] = globaltimer();
-  route_body<kGating, kDispatch>(a);
-  __syncthreads();
-#endif
   route_body<kGating, kDispatch>(a);
 }
 

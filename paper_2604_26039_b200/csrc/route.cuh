@@ -619,8 +619,7 @@ struct NoPublish {
 
 // `on_offsets(n_post_pad)` runs (in every thread, after a block barrier) as
 // soon as the padded offsets and tile_expert[] are final -- before the
-// bm-dependent placement of the assignments -- so the route kernel can hand
-// the selected config and the M-tile map to the megakernel early.
+// bm-dependent placement of the assignments.
 template <class Publish = NoPublish>
 __device__ inline void block_place(int64_t n, int E, int bm, RouteSmem& s, int* warp_tot,
                                    int32_t* __restrict__ sorted_ids, int32_t* __restrict__ tile_expert,

@@ -182,7 +182,12 @@ def workspace_bytes(S: int, H: int, I: int, E: int, top_k: int) -> int:
 class Workspace:
     """Reusable device workspace for `fused_moe`: route outputs, the fp32
     accumulator, expert-sorted tokens and split-mode activations.  Zeroed
-    once at allocation (it carries the route kernel's flags between calls)."""
+    once at allocation.  One workspace serves every call whose shape fits:
+    the library lays its regions out for the largest token count the buffer
+    holds (so a smaller S reuses the same offsets), and re-zeroes it itself
+    when the geometry (H, I, E, top_k) changes between calls."""
+
+    CTRL_BAD_IDS = 4  # int32 word of the control block: set by a call whose ids left [-1, E)
 
     def __init__(self, S: int, H: int, I: int, E: int, top_k: int, device="cuda"):
         self.key = (S, H, I, E, top_k)
@@ -192,6 +197,20 @@ class Workspace:
 
     def fits(self, S: int, H: int, I: int, E: int, top_k: int) -> bool:
         return self.buf.numel() >= workspace_bytes(S, H, I, E, top_k)
+
+    def invalid_ids(self) -> bool:
+        """True if the last call on this workspace saw a top-k id outside
+        [0, E) other than -1 (those slots were skipped).  Reads one device
+        word (synchronises the current stream)."""
+        w = self.buf[4 * self.CTRL_BAD_IDS:4 * self.CTRL_BAD_IDS + 4].view(torch.int32)
+        return bool(int(w.item()) != 0)
+
+
+def _raise_if_invalid_ids(ws: Workspace, E: int) -> None:
+    # the reference's ExpertHistogram rejects out-of-range experts with a
+    # ValueError (ramp/routing.py:45-50); the device flags them and skips them
+    if ws.invalid_ids():
+        raise ValueError(f"topk_ids hold expert ids outside [0, {E}) (other than -1, a non-local EP slot)")
 
 
 def fused_moe(
@@ -205,6 +224,7 @@ def fused_moe(
     out: torch.Tensor | None = None,
     workspace: Workspace | None = None,
     phases: int = 3,
+    validate: bool = False,
 ) -> torch.Tensor:
     """Fused MoE layer forward, BF16:
 
@@ -217,6 +237,9 @@ def fused_moe(
     the exhaustive sweep).  The selection record {cfg, n_post_pad, n_mtiles,
     n_eval} is left in `workspace.sel` (device int32[4]).  `phases` = 1 / 2
     runs only the route kernel / only the megakernel (ramp_fused_moe_bf16_ex).
+    Ids outside [0, E) other than -1 are skipped on the device and flagged;
+    `validate=True` checks the flag after the call and raises ValueError, as
+    the reference's ExpertHistogram does (costs one stream synchronisation).
     """
     lib = _lib.load()
     S, H = hidden_states.shape
@@ -247,6 +270,8 @@ def fused_moe(
             workspace.sel.data_ptr(), workspace.buf.data_ptr(), workspace.buf.numel(), int(phases), _stream(),
         )
     )
+    if validate and phases & 1:
+        _raise_if_invalid_ids(workspace, E)
     return out
 
 
@@ -318,6 +343,7 @@ def fused_moe_fp8(
     out: torch.Tensor | None = None,
     workspace: Workspace | None = None,
     phases: int = 3,
+    validate: bool = False,
 ) -> torch.Tensor:
     """Fused MoE layer forward, block-scaled FP8 (W8A8 MXFP8).
 
@@ -327,7 +353,7 @@ def fused_moe_fp8(
     per 32 features) and the SwiGLU activation the same way, multiplies with
     kind::mxf8f6f4.block_scale MMAs and accumulates in fp32; the output is
     bf16.  The table must be an FP8 pool (enumerate_b200_configs(...,
-    dtype="fp8")); `forced_cfg` / `phases` as in `fused_moe`.
+    dtype="fp8")); `forced_cfg` / `phases` / `validate` as in `fused_moe`.
     """
     lib = _lib.load()
     S, H = hidden_states.shape
@@ -364,6 +390,8 @@ def fused_moe_fp8(
             workspace.buf.numel(), int(phases), _stream(),
         )
     )
+    if validate and phases & 1:
+        _raise_if_invalid_ids(workspace, E)
     return out
 
 

@@ -1,0 +1,39 @@
+"""compute-sanitizer over one BF16 and one MXFP8 layer call:
+memcheck (out-of-bounds / misaligned accesses), racecheck (shared-memory
+hazards) and synccheck (barrier misuse) on the route kernel and the
+persistent megakernel, whose cross-CTA release/acquire counters, grid
+barriers and read-and-clear workspace are the risky parts.  Each run also
+checks its results against the oracle (scripts/sanitize_case.py)."""
+
+from __future__ import annotations
+
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _sanitizer():
+    for c in (shutil.which("compute-sanitizer"), "/usr/local/cuda/bin/compute-sanitizer"):
+        if c and Path(c).exists():
+            return c
+    pytest.fail("compute-sanitizer not found")
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+@pytest.mark.parametrize("dtype", ["bf16", "fp8"])
+def test_compute_sanitizer(tool, dtype):
+    cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "99",
+           sys.executable, str(ROOT / "scripts" / "sanitize_case.py"), "--dtype", dtype]
+    if tool == "racecheck":
+        cmd[3:3] = ["--racecheck-report", "hazard"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
+    tail = (res.stdout + res.stderr)[-3000:]
+    assert res.returncode == 0, tail
+    assert "sanitize_case ok" in res.stdout, tail
+    assert "ERROR SUMMARY: 0 errors" in res.stdout + res.stderr, tail
