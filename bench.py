@@ -384,10 +384,14 @@ EP_BETA = 0.5
 def ep_leg(dev, world, rank, iters=10, warmup=3):
     """BASELINE configs[4]: DeepSeek-V3 MoE layer (E=256, top-8, d=7168,
     d_ff=2048), MXFP8, expert-parallel over the `world` ranks of this run:
-    NCCL all-to-all dispatch of token rows to expert owners, the megakernel
-    on each rank's E/world experts (on-device dispatch over the FP8 pool with
-    the EP8 local table), NCCL all-to-all combine.  Every rank runs it (the
-    exchanges are collectives); the layer time is the max over ranks."""
+    the library's own NCCL communicator (ramp_ep_dispatch: pack kernel + one
+    grouped all-to-all of fixed-capacity MXFP8 blocks), the FP8 megakernel on
+    each rank's E/world experts straight off the wire (on-device dispatch over
+    the FP8 pool with the EP8 local table), ramp_ep_combine (all-to-all back +
+    reduce kernel).  No host synchronisation anywhere, so the layer is
+    captured and replayed as a CUDA graph.  At world 1 the same exchange runs
+    over a one-rank communicator, next to the identity shortcut (no exchange).
+    Every rank runs it; the layer time is the max over ranks."""
     import torch
     import torch.distributed as dist
 
@@ -419,54 +423,158 @@ def ep_leg(dev, world, rank, iters=10, warmup=3):
     hist = sample_histogram(geom.E, EP_TOKENS, geom.top_k, EP_BETA, hs).histogram
     x, ids, w = make_inputs(geom, hist, hs, dev)
     local_fn = ep.make_local_megakernel(weights, dtab)
-    group = None
+    comm = ep.EPComm()
+    side = torch.cuda.Stream(device=dev)
 
-    # MXFP8 token rows on the wire when there is a wire (N > 1); at N = 1 the
-    # exchange is a local copy and the quantise/expand kernels would only add time
-    wire = "fp8" if world > 1 else "bf16"
+    def timed(fn):
+        """Graph of 4 back-to-back layer calls; median per-call time, max over ranks."""
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                fn()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(4):
+                    fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        ts = []
+        for _ in range(iters):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3 / 4)
+        t = torch.tensor([float(np.median(ts))], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
-    def layer():
-        return ep.ep_moe_layer(x, ids, w, geom.E, local_fn, group=group, wire=wire)
-
-    for _ in range(warmup):
-        layer()
+    us = timed(lambda: ep.ep_moe_layer(x, ids, w, geom.E, local_fn, wire="fp8", comm=comm))
+    plan, rx, rids, rw = ep.dispatch(x, ids, w, geom.E, wire="fp8", comm=comm)
+    local_us = timed(lambda: local_fn(rx, rids, rw))
+    ident_us = timed(lambda: ep.ep_moe_layer(x, ids, w, geom.E, local_fn, wire="fp8")) if world == 1 else None
     torch.cuda.synchronize()
-    dist.barrier()
-    ts, local = [], []
-    for _ in range(iters):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        layer()
-        e1.record()
-        torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1) * 1e3)
-    # the local megakernel alone on this rank's received rows
-    plan, rx, rids, rw = ep.dispatch(x, ids, w, geom.E, group, wire=wire)
-    for _ in range(iters):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        local_fn(rx, rids, rw)
-        e1.record()
-        torch.cuda.synchronize()
-        local.append(e0.elapsed_time(e1) * 1e3)
-    t = torch.tensor([float(np.median(ts)), float(np.median(local)), float(rx.shape[0])], device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    us, local_us, rows = (float(v) for v in t.tolist())
+    overflow = int(plan.overflow.item())
+    rows = torch.tensor([float(plan.counts.sum().item())], device=dev)
+    dist.all_reduce(rows, op=dist.ReduceOp.MAX)
+    comm.close()
     flops = world * 6 * EP_TOKENS * geom.top_k * geom.K * (geom.N // 2)
     del weights
     torch.cuda.empty_cache()
-    return {"workload": f"{EP_MODEL} MoE layer (E=256, top-8, d=7168, d_ff=2048) MXFP8, expert-parallel over "
-                        f"{world} GPU(s): {per} experts/rank, {EP_TOKENS} tokens/rank, beta={EP_BETA}",
-            "exchange": ("none at world 1 (one rank owns every expert: the all-to-alls are identities and are "
-                         "skipped, no host read)") if world == 1 else
-                        (f"NCCL all_to_all_single: token rows as {'MXFP8 (E4M3 + UE8M0 per 32)' if wire == 'fp8' else 'bf16'}"
-                         " + local ids/weights; combine of per-(token,rank) partial sums in bf16"),
-            "dispatch_wire_bytes_rank0": plan.wire_bytes,
-            "dispatch_wire_bytes_if_bf16": int(len(plan.pair_token) * geom.K * 2),
-            "world": world, "us_per_layer": us, "local_megakernel_us": local_us, "max_rows_per_rank": int(rows),
-            "tflops": flops / us / 1e6, "timing": "CUDA events per layer call (includes the split-size host read), "
-                                                 "median of iters, max over ranks",
-            "coeffs": path.name}
+    out = {"workload": f"{EP_MODEL} MoE layer (E=256, top-8, d=7168, d_ff=2048) MXFP8, expert-parallel over "
+                       f"{world} GPU(s): {per} experts/rank, {EP_TOKENS} tokens/rank, beta={EP_BETA}",
+           "exchange": "ramp_ep_dispatch / ramp_ep_combine: pack kernel + one grouped NCCL all-to-all of "
+                       "fixed-capacity blocks (MXFP8 rows + local ids/weights; no host read), the FP8 megakernel "
+                       "on the MXFP8 rows as they arrived, NCCL all-to-all back + reduce kernel",
+           "world": world, "us_per_layer": us, "local_megakernel_us": local_us,
+           "exchange_overhead": us / local_us, "rows_sent_max": int(rows.item()), "overflow": overflow,
+           "dispatch_wire_bytes": plan.wire_bytes, "tflops": flops / us / 1e6,
+           "timing": "CUDA graph of 4 layer calls, median of iters, max over ranks", "coeffs": path.name}
+    if world == 1:
+        out["identity_us_per_layer"] = ident_us
+        out["note"] = ("world 1: the exchange runs over a one-rank NCCL communicator (self send/recv); "
+                       "identity_us_per_layer = the no-exchange shortcut. The local table is the EP8 fit "
+                       "(32 local experts) applied to 256 local experts")
+    return out
+
+
+# ------------------------------------------------------------------ report helpers
+def load_peaks():
+    """MEASURED_PEAKS.json (driver-written) or the profiling guide's fallbacks."""
+    pk_path = ROOT / "MEASURED_PEAKS.json"
+    peaks = json.loads(pk_path.read_text()) if pk_path.exists() else {}
+    src = "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    return float(peaks.get("hbm_gbs", 6650.0)), float(peaks.get("bf16_tflops", 2250.0)), src
+
+
+def roofline_summary(geom, pts, per_point, step_us, k3_bytes, k3_time):
+    """The layer roofline over the sweep.  Per point, the roofline time is
+    max(algorithmic bytes / HBM peak, FLOP / dense BF16 peak) (SURVEY.md 8d);
+    frac = sum of roofline times / the CUDA-event time of the whole step
+    (route kernel, prologue and megakernel of all 27 layer calls), and
+    achieved = frac x peak, the HBM-equivalent bandwidth of the step.  The
+    megakernel-only window (globaltimer, route kernel excluded) is kept
+    separately."""
+    hbm, tf, src = load_peaks()
+    t_roof, t_bytes, fr = 0.0, 0.0, []
+    for pt, r in zip(pts, per_point):
+        b = layer_bytes(geom, pt["hist"], pt["S"])
+        f = layer_flops(geom, pt["S"])
+        tr = max(b / hbm / 1e3, f / tf / 1e6)  # us
+        t_roof += tr
+        t_bytes += b / hbm / 1e3
+        fr.append(tr / r["us"])
+    frac = t_roof / step_us
+    n_hbm = sum(1 for pt in pts if layer_bytes(geom, pt["hist"], pt["S"]) / hbm / 1e3 >=
+                layer_flops(geom, pt["S"]) / tf / 1e6)
+    out = {"bound": "hbm", "achieved": frac * hbm, "peak": hbm, "unit": "GB/s", "frac": frac,
+           "traffic": None, "kernel": "route_kernel + fused_moe_kernel<0> (whole layer)",
+           "peak_source": src, "tensor_peak_tflops": tf,
+           "points_hbm_bound": n_hbm, "points_tensor_bound": len(pts) - n_hbm,
+           "bytes_only_frac": t_bytes / step_us, "per_point_geomean_frac": float(np.exp(np.mean(np.log(fr)))),
+           "megakernel_window_frac": (k3_bytes / k3_time / 1e3) / hbm,
+           "note": "frac = sum over the 27 points of max(bytes/hbm_peak, flop/bf16_peak) / CUDA-event step time; "
+                   "achieved = frac * peak (HBM-equivalent GB/s); megakernel_window_frac = algorithmic bytes / "
+                   "megakernel globaltimer window (route kernel excluded)"}
+    tr_path = ROOT / "profiles" / "sweep_traffic.json"
+    if tr_path.exists():
+        t = json.loads(tr_path.read_text())
+        out["traffic"] = t.get("dram_bytes_per_launch")
+        out["traffic_vs_algorithmic"] = t.get("dram_over_algorithmic")
+        out["traffic_source"] = t.get("source")
+    return out
+
+
+def write_per_point(per_point):
+    """The per-point detail goes to a file (the JSON line stays short)."""
+    d = ROOT / "gpurun_out" if (ROOT / "gpurun_out").is_dir() else ROOT
+    path = d / "bench_per_point.json"
+    try:
+        path.write_text(json.dumps(per_point, indent=1) + "\n")
+    except OSError:
+        return None
+    return str(path.relative_to(ROOT))
+
+
+def cpu_baseline(geom, pts, table):
+    """The CPU reference arms, timed on this box's host cores (bounded):
+    the fp32 oracle of the layer with every thread and with one thread, and
+    the reference's numpy dispatch path (ramp.select_config restated in
+    oracle/ramp_ref.select_np) on the same table and histograms as the device
+    dispatcher."""
+    from oracle.ramp_ref import select_np
+    from threadpoolctl import threadpool_limits
+
+    w1c, w2c = cpu_weights(geom)
+    run_cpu_sweep(geom, pts[:2], w1c, w2c)
+    f, t, n = run_cpu_sweep(geom, pts, w1c, w2c, budget_s=20.0)
+    out = {"value": f / t / 1e12, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
+           "sample": f"first {n} of {len(pts)} sweep points (fp32 numpy oracle, oracle/moe_ref.py)"}
+    with threadpool_limits(limits=1):
+        f1, t1, n1 = run_cpu_sweep(geom, pts, w1c, w2c, budget_s=8.0)
+    out["single_thread"] = {"value": f1 / t1 / 1e12, "unit": "TFLOP/s", "cores": 1,
+                            "sample": f"first {n1} sweep points, BLAS limited to 1 thread (threadpoolctl)"}
+    cols = table.pool.columns()
+    act = table._active
+    args = dict(bm=cols["bm"][act], ttn=cols["ttn"][act], split_k=cols["split_k"][act], a=table._a[act],
+                b=table._b[act], c=table._c[act], d=table._d[act], N=geom.N, sm=table.sm_count,
+                kappa_ok=bool(table._kappa_ok), ntile=cols["ntile"][act], omega_max=table._omega_max,
+                lam=None if table._lam is None else table._lam[act])
+    ts = []
+    for pt in pts:
+        counts = np.asarray(pt["hist"].counts)
+        select_np(counts=counts, **args)
+        t0 = time.perf_counter()
+        for _ in range(20):
+            select_np(counts=counts, **args)
+        ts.append((time.perf_counter() - t0) / 20 * 1e6)
+    out["dispatch"] = {"us_per_call_median": float(np.median(ts)), "us_per_call_max": float(np.max(ts)),
+                       "candidates": int(act.sum()), "cores": 1,
+                       "impl": "ramp.select_config's numpy path (pool_grids -> gate -> predict_batch -> argmin), "
+                               "oracle/ramp_ref.select_np, on the bench table and the 27 sweep histograms; "
+                               "the device dispatcher runs inside the route kernel (no host round trip)"}
+    return out
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -651,12 +759,24 @@ def ours(args, geom):
                                  sm_count=table.sm_count).device_table(device=dev)
         timer = MeasuredTimer(geom, full_tab, w1=copies[0][0], w2=copies[0][1], iters=9, device=dev)
         points = [(pt["S"], pt["beta"]) for pt in pts]
-        spd = speedup_ra_vs_static(table, pool, geom, timer, points=points, seeds_per_point=1)
-        reg = evaluate_regret(table, pool, geom, timer, test_points=points, seeds_per_point=1)
+        t_ra = time.time()
+        ns = args.regret_seeds
+        spd = speedup_ra_vs_static(table, pool, geom, timer, points=points, seeds_per_point=ns)
+        reg = evaluate_regret(table, pool, geom, timer, test_points=points, seeds_per_point=ns)
+        agg = reg.aggregate()
         ra = {"ra_vs_static_geomean": spd.geomean, "per_beta": spd.aggregate()["per_beta_geomean"],
-              "regret_mean_pct": reg.mean * 100, "regret_max_pct": reg.max * 100, "points": len(points),
+              "regret_mean_pct": reg.mean * 100, "regret_max_pct": reg.max * 100,
+              "regret_sweep_only_mean_pct": agg["sweep_only_mean"] * 100,
+              "regret_sweep_only_max_pct": agg["sweep_only_max"] * 100,
+              "points": len(points), "seeds_per_point": ns, "records": len(reg.records),
+              "winners_curse_retimed": agg["retimed"],
+              "method": "regret = selected / exhaustive best - 1 over every pool config, L2 flushed per replay; "
+                        "when the pick is not the sweep's winner both are re-timed side by side with 4x the "
+                        "replays and the faster is the best (deviation from ramp.evaluate_regret, which uses the "
+                        "sweep minimum: reported as regret_sweep_only_*)",
               "worst": [{"S": r.S, "beta": r.beta, "regret_pct": round(r.regret * 100, 2), "sel": r.selected_id,
-                         "best": r.best_id} for r in sorted(reg.records, key=lambda r: -r.regret)[:4]]}
+                         "best": r.best_id} for r in sorted(reg.records, key=lambda r: -r.regret)[:3]],
+              "wall_s": round(time.time() - t_ra, 1)}
 
     # ---------------- e2e through the public API with host buffers
     pinned = []
@@ -726,11 +846,7 @@ def ours(args, geom):
     # ---------------- CPU baseline (oracle port, bounded sample)
     cpu = None
     if not args.no_cpu:
-        w1c, w2c = cpu_weights(geom)
-        run_cpu_sweep(geom, pts[:2], w1c, w2c)
-        f, t, n = run_cpu_sweep(geom, pts, w1c, w2c, budget_s=20.0)
-        cpu = {"value": f / t / 1e12, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"first {n} of {len(pts)} sweep points (fp32 numpy oracle, oracle/moe_ref.py)"}
+        cpu = cpu_baseline(geom, pts, table)
 
     mix = None
     if not args.no_mixtral:
@@ -746,16 +862,8 @@ def ours(args, geom):
         except Exception as exc:  # noqa: BLE001 - reported in the line, never fatal for the main metric
             fp8 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
-    peaks = {}
-    pk_path = ROOT / "MEASURED_PEAKS.json"
-    if pk_path.exists():
-        peaks = json.loads(pk_path.read_text())
-    peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = k3_bytes / k3_time / 1e3  # GB/s over the sweep (bytes-weighted)
-    traffic = None
-    tr_path = ROOT / "profiles" / "k3_traffic.json"
-    if tr_path.exists():
-        traffic = json.loads(tr_path.read_text()).get("traffic_bytes_per_launch")
+    roof = roofline_summary(geom, pts, per_point, ms / args.steps * 1e3, k3_bytes, k3_time)
+    pp_path = write_per_point(per_point)
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -767,9 +875,7 @@ def ours(args, geom):
                    "parallelism": "replicas" if world > 1 else "single GPU", "coeffs": coeff_path.name},
         "gpu_launches": 2 * len(pts) * args.steps,
         "us_per_layer_geomean": geo_us,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "fused_moe_bf16_kernel",
-                     "note": "algorithmic bytes / megakernel time summed over the sweep; peak = measured hbm_gbs"},
+        "roofline": roof,
         "clocks": clocks.summary(),
         "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "how": "public fused_moe() per layer from pinned host inputs (x, topk ids, topk weights) to a pinned "
@@ -777,7 +883,8 @@ def ours(args, geom):
                        "neighbouring layers' compute"},
         "cpu_baseline": cpu,
         "dispatch": ra,
-        "per_point": per_point,
+        "per_point_us": [[r["S"], r["beta"], r["us"]] for r in per_point],
+        "per_point_file": pp_path,
         "fp8": fp8,
         "mixtral": mix,
         "ep": ep_res,
@@ -798,6 +905,8 @@ def main():
     ap.add_argument("--no-fp8", action="store_true", help="skip the Qwen3 FP8 side measurement")
     ap.add_argument("--no-ep", action="store_true", help="skip the DeepSeek-V3 expert-parallel side measurement")
     ap.add_argument("--no-mixtral", action="store_true", help="skip the Mixtral large-K side measurement")
+    ap.add_argument("--regret-seeds", type=int, default=3,
+                    help="routing seeds per sweep point in the regret / RA-vs-static evaluation (reference: 3)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -187,15 +187,25 @@ int ramp_fused_moe_gating_bf16(const void* x, const void* w1, const void* w2, co
  * w1_q [E,2I,H] / w2_q [E,H,I] e4m3; w1_sf / w2_sf their scale atoms tiled as
  * [rows/128][K/128][512 B] (paper_2604_26039_b200/quant.py tile_scales);
  * tokens arrive in bf16 and are quantised on the fly (per token, per 32).
- * The table must hold FP8 configs (split mode, bm >= 16, ttn >= 256,
- * ramp_config_smem_bytes_fp8 > 0).  d_ff must be a multiple of 256.
+ * The table must hold FP8 configs (split mode, ttn >= 256,
+ * ramp_config_smem_bytes_fp8_kps > 0).  d_ff must be a multiple of 256.
  * Replaces the W8A8 FP8 kernel of the paper. */
 int ramp_fused_moe_fp8(const void* x, const void* w1_q, const uint8_t* w1_sf, const void* w2_q,
                        const uint8_t* w2_sf, const float* topk_w, const int32_t* topk_ids, int32_t S, int32_t H,
                        int32_t I, int32_t E, int32_t top_k, const ramp_table_t* table, int32_t forced_cfg,
                        void* out, int32_t* sel_out, void* workspace, size_t workspace_bytes, int32_t phases,
                        void* stream);
+/* Same layer with the tokens already in MXFP8 -- x_q [S,H] e4m3 and x_sf
+ * [S,H/32] UE8M0 row-major, e.g. straight off the RAMP_EP_WIRE_MXFP8
+ * exchange: the megakernel's phase 0 moves them instead of quantising. */
+int ramp_fused_moe_fp8_prequant(const uint8_t* x_q, const uint8_t* x_sf, const void* w1_q, const uint8_t* w1_sf,
+                                const void* w2_q, const uint8_t* w2_sf, const float* topk_w, const int32_t* topk_ids,
+                                int32_t S, int32_t H, int32_t I, int32_t E, int32_t top_k, const ramp_table_t* table,
+                                int32_t forced_cfg, void* out, int32_t* sel_out, void* workspace,
+                                size_t workspace_bytes, int32_t phases, void* stream);
 int64_t ramp_config_smem_bytes_fp8(int32_t bm, int32_t ttn, int32_t stg);
+/* Same with kps k-blocks (128 K-elements each) per stage (1 or 2); 0 if not realisable. */
+int64_t ramp_config_smem_bytes_fp8_kps(int32_t bm, int32_t ttn, int32_t stg, int32_t kps);
 
 /* Shared-memory bytes the megakernel needs for (bm, ttn, stg, mode); 0 if the
  * configuration is not realisable on this part (pool admissibility test,
@@ -214,6 +224,49 @@ int64_t ramp_config_smem_bytes_kps(int32_t bm, int32_t ttn, int32_t stg, int32_t
  * (buffer: >= 149 * 32 + 148 * 16 * 4 entries).
  * Pass null to switch it off.  Not used on the timed path. */
 void ramp_set_profile_buffer(unsigned long long* dev_buf);
+
+/* ---------------------------------------------------------------------------
+ * Expert parallelism (north_star (4); SURVEY.md 8b ramp_ep_dispatch/combine,
+ * replacing the eager torch exchange the reference-side integration would
+ * otherwise write).  Rank r of `world` owns experts [r*E/world, (r+1)*E/world).
+ * Every exchange moves fixed-capacity blocks -- `cap` rows per destination
+ * (cap = S never drops a pair) -- so no split size is read on the host and
+ * the layer is CUDA-graph capturable:
+ *   send_x   [world][cap][H] bf16, or e4m3 with send_sf [world][cap][H/32]
+ *            UE8M0 (RAMP_EP_WIRE_MXFP8: 0.52x the bytes; the FP8 megakernel
+ *            consumes it directly, ramp_fused_moe_fp8_prequant)
+ *   send_ids [world][cap][k] rank-local expert ids, -1 = another rank's slot
+ *            or a padding row (skipped by the route kernel: no work)
+ *   send_w   [world][cap][k] fp32 weights (0 on -1 slots)
+ *   pos      [S][world] row of (token, rank) in the send blocks, -1 = none
+ *   counts   [world] rows sent; *overflow = 1 if some rank needed > cap rows
+ * Receive buffers have the same shapes (block s came from rank s).
+ */
+#define RAMP_EP_WIRE_BF16 0
+#define RAMP_EP_WIRE_MXFP8 1
+typedef struct ramp_ep_comm ramp_ep_comm;
+
+/* pack only (the exchange is left to the caller, e.g. torch.distributed) */
+int ramp_ep_pack(const void* x, const int32_t* topk_ids, const float* topk_w, int32_t S, int32_t H, int32_t E,
+                 int32_t top_k, int32_t world, int32_t cap, int32_t wire, void* send_x, uint8_t* send_sf,
+                 int32_t* send_ids, float* send_w, int32_t* pos, int32_t* counts, int32_t* overflow, void* stream);
+/* out[t] = sum over ranks d (in rank order) of back[d][pos[t][d]] (fp32 sum, bf16 out) */
+int ramp_ep_reduce(const void* back, const int32_t* pos, int32_t S, int32_t H, int32_t world, int32_t cap,
+                   void* out, void* stream);
+/* NCCL communicator (libnccl.so.2 loaded at run time): rank 0 gets the
+ * 128-byte id, every rank passes it to ramp_ep_comm_init. */
+int ramp_ep_get_unique_id(unsigned char* out128);
+int ramp_ep_comm_init(ramp_ep_comm** comm, const unsigned char* id128, int32_t world, int32_t rank);
+int ramp_ep_comm_destroy(ramp_ep_comm* comm);
+/* pack + one grouped NCCL all-to-all of x (+ scales), ids and weights */
+int ramp_ep_dispatch(ramp_ep_comm* comm, const void* x, const int32_t* topk_ids, const float* topk_w, int32_t S,
+                     int32_t H, int32_t E, int32_t top_k, int32_t cap, int32_t wire, void* send_x, uint8_t* send_sf,
+                     int32_t* send_ids, float* send_w, int32_t* pos, int32_t* counts, int32_t* overflow,
+                     void* recv_x, uint8_t* recv_sf, int32_t* recv_ids, float* recv_w, void* stream);
+/* NCCL all-to-all of the partial outputs [world*cap][H] bf16 back into
+ * back[world][cap][H], then ramp_ep_reduce into out[S][H] */
+int ramp_ep_combine(ramp_ep_comm* comm, const void* partial, void* back, const int32_t* pos, int32_t S, int32_t H,
+                    int32_t cap, void* out, void* stream);
 
 #ifdef __cplusplus
 }

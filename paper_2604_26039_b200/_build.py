@@ -25,7 +25,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relax
 # The route TU evaluates the fp64 cost model; -fmad=false keeps every product
 # and sum separately rounded, matching numpy's evaluation (ramp/cost_model.py:114).
 PER_FILE = {"route.cu": ["-fmad=false"]}
-SOURCES = ["route.cu", "moe.cu", "capi.cu"]
+SOURCES = ["route.cu", "moe.cu", "ep.cu", "capi.cu"]
 
 
 def nvcc() -> str:
@@ -62,7 +62,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             if verbose:
                 print(res.stderr)
     if force or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"]
+        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-ldl"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)

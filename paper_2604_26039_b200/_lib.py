@@ -43,6 +43,7 @@ SIGNATURES = {
     ),
 }
 SIGNATURES["ramp_config_smem_bytes_fp8"] = (ctypes.c_int64, [ctypes.c_int32] * 3)
+SIGNATURES["ramp_config_smem_bytes_fp8_kps"] = (ctypes.c_int64, [ctypes.c_int32] * 4)
 SIGNATURES["ramp_config_smem_bytes_kps"] = (ctypes.c_int64, [ctypes.c_int32] * 5)
 SIGNATURES["ramp_fused_moe_gating_bf16"] = (
     ctypes.c_int,
@@ -53,6 +54,18 @@ SIGNATURES["ramp_fused_moe_fp8"] = (
     ctypes.c_int,
     [ctypes.c_void_p] * 7 + [ctypes.c_int32] * 5 + [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
                                                     ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32, ctypes.c_void_p])
+SIGNATURES["ramp_fused_moe_fp8_prequant"] = (
+    ctypes.c_int,
+    [ctypes.c_void_p] * 8 + [ctypes.c_int32] * 5 + [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                                                    ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32, ctypes.c_void_p])
+_vp, _i32 = ctypes.c_void_p, ctypes.c_int32
+SIGNATURES["ramp_ep_pack"] = (ctypes.c_int, [_vp] * 3 + [_i32] * 7 + [_vp] * 8)
+SIGNATURES["ramp_ep_reduce"] = (ctypes.c_int, [_vp, _vp] + [_i32] * 4 + [_vp, _vp])
+SIGNATURES["ramp_ep_get_unique_id"] = (ctypes.c_int, [_vp])
+SIGNATURES["ramp_ep_comm_init"] = (ctypes.c_int, [ctypes.POINTER(_vp), _vp, _i32, _i32])
+SIGNATURES["ramp_ep_comm_destroy"] = (ctypes.c_int, [_vp])
+SIGNATURES["ramp_ep_dispatch"] = (ctypes.c_int, [_vp] * 4 + [_i32] * 6 + [_vp] * 12)
+SIGNATURES["ramp_ep_combine"] = (ctypes.c_int, [_vp] * 4 + [_i32] * 3 + [_vp, _vp])
 SIGNATURES["ramp_fused_moe_bf16_ex"] = (
     ctypes.c_int, SIGNATURES["ramp_fused_moe_bf16"][1][:-1] + [ctypes.c_int32, ctypes.c_void_p])
 

@@ -57,7 +57,8 @@ WorkspaceLayout layout_for(int32_t S, int32_t H, int32_t I, int32_t E, int32_t t
   w.act = take(2 * (size_t)w.rows * I);
   w.acc_a = take(4 * (size_t)w.rows * 2 * I);
   w.split_cnt = take(sizeof(int32_t) * w.capacity);
-  const int64_t mt_max = w.capacity / 16 + 1;  // FP8 configs use bm >= 16
+  // FP8 scale atoms per M-tile: n_post_pad / bm <= n_assign / bm + E M-tiles, bm >= 4
+  const int64_t mt_max = n_assign / 4 + E + 1;
   w.xq = take((size_t)w.rows * H);
   w.xsf = take((size_t)mt_max * (H / 128 + 1) * 512);
   w.actq = take((size_t)w.rows * I);
@@ -164,8 +165,15 @@ int64_t ramp_config_smem_bytes_kps(int32_t bm, int32_t ttn, int32_t stg, int32_t
 }
 
 int64_t ramp_config_smem_bytes_fp8(int32_t bm, int32_t ttn, int32_t stg) {
-  if (bm < 16 || ttn < 256 || (ttn / 128) * ramp::bm_mma_host(bm) > 448) return 0;
-  return ramp::config_smem_bytes(bm, ttn, stg, 1, true);
+  return ramp_config_smem_bytes_fp8_kps(bm, ttn, stg, 1);
+}
+
+int64_t ramp_config_smem_bytes_fp8_kps(int32_t bm, int32_t ttn, int32_t stg, int32_t kps) {
+  // accumulators below the TMEM scale-factor columns; kps 1 or 2 with at most
+  // 16 scale atoms per stage
+  if (bm < 4 || ttn < 256 || (ttn / 128) * ramp::bm_mma_host(bm) > ramp::kSfCol) return 0;
+  if (kps != 1 && (kps != 2 || kps * (ttn / 128 + 1) > 16)) return 0;
+  return ramp::config_smem_bytes(bm, ttn, stg, 1, true, kps);
 }
 
 int ramp_moe_align(const int32_t* topk_ids, int64_t n_assign, int32_t E, int32_t bm, int32_t* hist,
@@ -203,7 +211,7 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
                       int32_t top_k, const ramp_table_t* table, int32_t forced_cfg, void* out, int32_t* sel_out,
                       void* workspace, size_t workspace_bytes, int32_t phases, void* stream, bool fp8,
                       const void* logits = nullptr, int32_t logits_bf16 = 0, int32_t renorm = 0,
-                      float* w_out = nullptr) {
+                      float* w_out = nullptr, const uint8_t* xsf_in = nullptr) {
   if (phases < 1 || phases > 3) return fail(RAMP_EINVAL, "phases must be 1 (route), 2 (megakernel) or 3");
   if (int rc = check_table(table)) return rc;
   if (S < 0) return fail(RAMP_EINVAL, "S must be >= 0");
@@ -293,6 +301,8 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   ml.x_sf = ws + L.xsf;
   ml.act_q = ws + L.actq;
   ml.act_sf = ws + L.actsf;
+  ml.xq_in = xsf_in ? static_cast<const uint8_t*>(x) : nullptr;  // x holds e4m3 rows then
+  ml.xsf_in = xsf_in;
   ml.table = *table;
   ml.S = S;
   ml.H = H;
@@ -343,6 +353,123 @@ int ramp_fused_moe_fp8(const void* x, const void* w1_q, const uint8_t* w1_sf, co
   if (I % 256 != 0) return fail(RAMP_EINVAL, "FP8 path needs d_ff a multiple of 256");
   return fused_impl(x, w1_q, w1_sf, w2_q, w2_sf, topk_w, topk_ids, S, H, I, E, top_k, table, forced_cfg, out,
                     sel_out, workspace, workspace_bytes, phases, stream, true);
+}
+
+int ramp_fused_moe_fp8_prequant(const uint8_t* x_q, const uint8_t* x_sf, const void* w1_q, const uint8_t* w1_sf,
+                                const void* w2_q, const uint8_t* w2_sf, const float* topk_w, const int32_t* topk_ids,
+                                int32_t S, int32_t H, int32_t I, int32_t E, int32_t top_k, const ramp_table_t* table,
+                                int32_t forced_cfg, void* out, int32_t* sel_out, void* workspace,
+                                size_t workspace_bytes, int32_t phases, void* stream) {
+  if (S > 0 && (!w1_sf || !w2_sf || !x_sf)) return fail(RAMP_EINVAL, "null scale-factor tensor");
+  if (reinterpret_cast<uintptr_t>(x_sf) % 4 != 0) return fail(RAMP_EINVAL, "x_sf must be 4-byte aligned");
+  if (I % 256 != 0) return fail(RAMP_EINVAL, "FP8 path needs d_ff a multiple of 256");
+  return fused_impl(x_q, w1_q, w1_sf, w2_q, w2_sf, topk_w, topk_ids, S, H, I, E, top_k, table, forced_cfg, out,
+                    sel_out, workspace, workspace_bytes, phases, stream, true, nullptr, 0, 0, nullptr, x_sf);
+}
+
+// ------------------------------------------------------------ expert parallelism
+struct ramp_ep_comm {
+  void* nccl;
+  int32_t world, rank;
+};
+
+static int ep_check(const void* x, const int32_t* topk_ids, const float* topk_w, int32_t S, int32_t H, int32_t E,
+                    int32_t top_k, int32_t world, int32_t cap, int32_t wire) {
+  if (world < 1 || world > 32) return fail(RAMP_EINVAL, "world must be in [1, 32]");
+  if (E < 1 || E % world != 0) return fail(RAMP_EINVAL, "E must be a positive multiple of world");
+  if (S < 0 || cap < 0) return fail(RAMP_EINVAL, "S and cap must be >= 0");
+  if (top_k < 1 || top_k > E) return fail(RAMP_EINVAL, "top_k must be in [1, E]");
+  if (H < 128 || H % 128 != 0) return fail(RAMP_EINVAL, "H (d_model) must be a positive multiple of 128");
+  if (wire != RAMP_EP_WIRE_BF16 && wire != RAMP_EP_WIRE_MXFP8) return fail(RAMP_EINVAL, "unknown wire format");
+  if (S > 0 && (!x || !topk_ids || !topk_w)) return fail(RAMP_EINVAL, "null tensor");
+  if (reinterpret_cast<uintptr_t>(x) % 16 != 0) return fail(RAMP_EINVAL, "x must be 16-byte aligned");
+  return RAMP_OK;
+}
+
+int ramp_ep_pack(const void* x, const int32_t* topk_ids, const float* topk_w, int32_t S, int32_t H, int32_t E,
+                 int32_t top_k, int32_t world, int32_t cap, int32_t wire, void* send_x, uint8_t* send_sf,
+                 int32_t* send_ids, float* send_w, int32_t* pos, int32_t* counts, int32_t* overflow, void* stream) {
+  if (int rc = ep_check(x, topk_ids, topk_w, S, H, E, top_k, world, cap, wire)) return rc;
+  if (!send_x || !send_ids || !send_w || !pos || !counts || !overflow ||
+      (wire == RAMP_EP_WIRE_MXFP8 && !send_sf))
+    return fail(RAMP_EINVAL, "null send buffer");
+  if (reinterpret_cast<uintptr_t>(send_x) % 16 != 0) return fail(RAMP_EINVAL, "send_x must be 16-byte aligned");
+  ramp::EpPackArgs a{topk_ids, topk_w, x, S, H, top_k, E, world, cap, send_x, send_sf, send_ids, send_w,
+                     pos, counts, overflow};
+  cudaError_t err = ramp::launch_ep_pack(a, wire == RAMP_EP_WIRE_MXFP8, static_cast<cudaStream_t>(stream));
+  if (err != cudaSuccess) return cuda_fail(err, "ramp_ep_pack");
+  return RAMP_OK;
+}
+
+int ramp_ep_reduce(const void* back, const int32_t* pos, int32_t S, int32_t H, int32_t world, int32_t cap,
+                   void* out, void* stream) {
+  if (world < 1 || world > 32 || S < 0 || cap < 0 || H < 128 || H % 128 != 0)
+    return fail(RAMP_EINVAL, "bad geometry");
+  if (S > 0 && (!back || !pos || !out)) return fail(RAMP_EINVAL, "null tensor");
+  if (reinterpret_cast<uintptr_t>(back) % 16 != 0 || reinterpret_cast<uintptr_t>(out) % 16 != 0)
+    return fail(RAMP_EINVAL, "tensors must be 16-byte aligned");
+  cudaError_t err = ramp::launch_ep_combine(back, pos, S, H, world, cap, out, static_cast<cudaStream_t>(stream));
+  if (err != cudaSuccess) return cuda_fail(err, "ramp_ep_reduce");
+  return RAMP_OK;
+}
+
+int ramp_ep_get_unique_id(unsigned char* out128) {
+  if (!out128) return fail(RAMP_EINVAL, "null id buffer");
+  const char* why = nullptr;
+  if (ramp::nccl_unique_id(out128, &why) != 0) return fail(RAMP_ECUDA, std::string("NCCL: ") + (why ? why : "?"));
+  return RAMP_OK;
+}
+
+int ramp_ep_comm_init(ramp_ep_comm** comm, const unsigned char* id128, int32_t world, int32_t rank) {
+  if (!comm || !id128) return fail(RAMP_EINVAL, "null argument");
+  if (world < 1 || world > 32 || rank < 0 || rank >= world) return fail(RAMP_EINVAL, "bad world / rank");
+  const char* why = nullptr;
+  void* c = ramp::nccl_comm_init(id128, world, rank, &why);
+  if (!c) return fail(RAMP_ECUDA, std::string("ncclCommInitRank: ") + (why ? why : "?"));
+  *comm = new ramp_ep_comm{c, world, rank};
+  return RAMP_OK;
+}
+
+int ramp_ep_comm_destroy(ramp_ep_comm* comm) {
+  if (!comm) return RAMP_OK;
+  ramp::nccl_comm_destroy(comm->nccl);
+  delete comm;
+  return RAMP_OK;
+}
+
+int ramp_ep_dispatch(ramp_ep_comm* comm, const void* x, const int32_t* topk_ids, const float* topk_w, int32_t S,
+                     int32_t H, int32_t E, int32_t top_k, int32_t cap, int32_t wire, void* send_x, uint8_t* send_sf,
+                     int32_t* send_ids, float* send_w, int32_t* pos, int32_t* counts, int32_t* overflow,
+                     void* recv_x, uint8_t* recv_sf, int32_t* recv_ids, float* recv_w, void* stream) {
+  if (!comm) return fail(RAMP_EINVAL, "null communicator");
+  if (!recv_x || !recv_ids || !recv_w || (wire == RAMP_EP_WIRE_MXFP8 && !recv_sf))
+    return fail(RAMP_EINVAL, "null receive buffer");
+  const int32_t P = comm->world;
+  if (int rc = ramp_ep_pack(x, topk_ids, topk_w, S, H, E, top_k, P, cap, wire, send_x, send_sf, send_ids, send_w,
+                            pos, counts, overflow, stream))
+    return rc;
+  const bool fp8 = wire == RAMP_EP_WIRE_MXFP8;
+  const void* snd[4] = {send_x, send_ids, send_w, send_sf};
+  void* rcv[4] = {recv_x, recv_ids, recv_w, recv_sf};
+  const size_t bytes[4] = {(size_t)cap * H * (fp8 ? 1 : 2), (size_t)cap * top_k * 4, (size_t)cap * top_k * 4,
+                           (size_t)cap * (H / 32)};
+  const char* why = nullptr;
+  if (ramp::nccl_all_to_all(comm->nccl, P, snd, rcv, bytes, fp8 ? 4 : 3, static_cast<cudaStream_t>(stream), &why))
+    return fail(RAMP_ECUDA, std::string("NCCL dispatch: ") + (why ? why : "?"));
+  return RAMP_OK;
+}
+
+int ramp_ep_combine(ramp_ep_comm* comm, const void* partial, void* back, const int32_t* pos, int32_t S, int32_t H,
+                    int32_t cap, void* out, void* stream) {
+  if (!comm) return fail(RAMP_EINVAL, "null communicator");
+  if (!partial || !back) return fail(RAMP_EINVAL, "null buffer");
+  const void* snd[1] = {partial};
+  void* rcv[1] = {back};
+  const size_t bytes[1] = {(size_t)cap * H * 2};
+  const char* why = nullptr;
+  if (ramp::nccl_all_to_all(comm->nccl, comm->world, snd, rcv, bytes, 1, static_cast<cudaStream_t>(stream), &why))
+    return fail(RAMP_ECUDA, std::string("NCCL combine: ") + (why ? why : "?"));
+  return ramp_ep_reduce(back, pos, S, H, comm->world, cap, out, stream);
 }
 
 }  // extern "C"

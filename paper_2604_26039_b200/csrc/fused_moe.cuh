@@ -61,10 +61,11 @@ __host__ __device__ inline int stage_bytes(int bm, int ttn, int kps = 1) {
   return (raw + 1023) / 1024 * 1024;
 }
 // FP8 (MXFP8) stages also carry the 512-byte scale-factor atoms of the nA
-// weight tiles and of the token tile.
-__host__ __device__ inline int stage_bytes_fp8(int bm, int ttn) {
+// weight tiles and of the token tile of each of their kps k-blocks (after all
+// operand tiles; split phase 3 uses 2 x kps of them: W2 then act).
+__host__ __device__ inline int stage_bytes_fp8(int bm, int ttn, int kps = 1) {
   const int nA = ttn >= 256 ? ttn / 128 : 1;
-  const int raw = nA * kSubTileBytes + bm_mma(bm) * 128 + (nA + 1) * 512;
+  const int raw = kps * (nA * kSubTileBytes + bm_mma(bm) * 128 + (nA + 1) * 512);
   return (raw + 1023) / 1024 * 1024;
 }
 __host__ __device__ inline int act_bytes(int bm, int ttn, int mode) {
@@ -74,10 +75,9 @@ __host__ __device__ inline int act_bytes(int bm, int ttn, int mode) {
 // ramp/config_space.py:122-124): 1 KB alignment slack, control block,
 // scatter transpose buffer, stg ring stages, fused mode's bf16 act tile.
 __host__ __device__ inline int moe_smem_bytes(int bm, int ttn, int stg, int mode, bool fp8 = false, int kps = 1) {
-  return 1024 + kCtrlBytes + kStageBytesScatter + stg * (fp8 ? stage_bytes_fp8(bm, ttn) : stage_bytes(bm, ttn, kps)) +
+  return 1024 + kCtrlBytes + kStageBytesScatter + stg * (fp8 ? stage_bytes_fp8(bm, ttn, kps) : stage_bytes(bm, ttn, kps)) +
          (fp8 ? 0 : act_bytes(bm, ttn, mode));
 }
-constexpr int kSfCol = 480;  // TMEM columns 480.. hold the scale factors of the FP8 MMAs
 __host__ __device__ inline int bmn_index(int bmN) { return bmN <= 16 ? 0 : bmN <= 32 ? 1 : bmN <= 64 ? 2 : 3; }
 
 struct MoeMaps {
@@ -115,6 +115,8 @@ struct MoeParams {
   uint8_t* x_sf;               // [M-tiles][H/128][512]
   uint8_t* act_q;              // [rows, I] quantised SwiGLU activations
   uint8_t* act_sf;             // [M-tiles][I/128][512]
+  const uint8_t* xq_in;        // optional: tokens already MXFP8, [S, H] e4m3 (then x is unused)
+  const uint8_t* xsf_in;       //           and their scales [S, H/32] UE8M0, row-major
   ramp_table_t table;
   int32_t S, H, I, E, top_k, n_assign;
   unsigned long long* prof;    // optional per-CTA cycle counters [gridDim][16] (diagnostics)
@@ -381,12 +383,14 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   G.n_hj = pdiv<kFp8>(G.n_hc, G.n3);
   G.total = G.nJobA + (G.mode == kModeSplit ? G.n_mtiles * G.n_hj * G.sk : 0);
   G.dbl = !kFp8 && G.mode == kModeSplit && G.nA * G.bmN <= 256;
-  // k-blocks per stage (BF16 only); every job's k-range must split into whole stages
-  G.kps = kFp8 ? 1 : cf.kps;
+  // k-blocks per stage; every job's k-range must split into whole stages
+  // (FP8: at most 16 scale atoms per stage)
+  G.kps = cf.kps;
   if (G.kps != 2 && G.kps != 4) G.kps = 1;
+  if (kFp8 && (G.kps > 2 || G.kps * (G.nA + 1) > 16)) G.kps = 1;  // FP8 roles: kps 1 and 2
   if (pdiv<kFp8>(G.kbH, G.sk) % G.kps != 0 || (G.mode == kModeSplit && pdiv<kFp8>(G.kbI, G.sk) % G.kps != 0)) G.kps = 1;
   const int bmN = G.bmN, nA = G.nA, kps = G.kps;
-  const int sbytes = kFp8 ? stage_bytes_fp8(G.bm, ttn) : stage_bytes(G.bm, ttn, kps);
+  const int sbytes = kFp8 ? stage_bytes_fp8(G.bm, ttn, kps) : stage_bytes(G.bm, ttn, kps);
   const int tok_off = kps * nA * kSubTileBytes;  // token tiles follow the stage's weight boxes
   const uint32_t act_addr = ring_addr + stg * sbytes;
   unsigned char* act_ptr = base + kCtrlBytes + kStageBytesScatter + stg * sbytes;
@@ -395,7 +399,10 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   const CUtensorMap* tm_w1 =
       kFp8 ? &maps.w1q[G.n_i == 256 ? 1 : 0] : &maps.w1[G.n_i == 256 ? 2 : G.n_i == 128 ? 1 : 0];
   const CUtensorMap* tm_w2 = kFp8 ? &maps.w2q : &maps.w2;
-  const int sf_off = nA * kSubTileBytes + bmN * 128;  // FP8: scale atoms after the operand tiles
+  // FP8: scale atoms after the operand tiles; phase 1 atom slot t * kps + q
+  // (t < nA: weight tile t, t = nA: tokens; q = k-block within the stage),
+  // split phase 3 slot q (W2) and kps + q (act)
+  const int sf_off = kps * (nA * kSubTileBytes + bmN * 128);
 
   // ---- phase 0: gather the token rows of every M-tile into expert-sorted
   // order (warps 2-7 of every CTA, 8 x 16-byte loads in flight per lane),
@@ -408,42 +415,95 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   if (kFp8 && warp >= 2) {
     // FP8: gather + quantise every row to MXFP8 (per-32 power-of-two scales)
     // into x_q and the per-M-tile scale atoms x_sf.
-    constexpr int kGatherWarps = 6;
-    const int row_vec = p.H / 8;  // 8 bf16 per lane-chunk; 4 consecutive lanes = one 32-group
+    // A lane quantises 8 features (one 16-byte load, one 8-byte store); 4
+    // lanes form a 32-group and 16 lanes a 128-wide k-block, whose 4 scale
+    // bytes are consecutive in the atom (one 4-byte store).  kUnroll loads
+    // per lane are in flight before the first store: the row sources are
+    // L2-resident and this pass gates every token tile (grid barrier 0).
+    constexpr int kGatherWarps = 6, kUnroll = 8;
+    const int row_vec = p.H / 8;  // multiple of 16 (H % 128 == 0)
     const int gw = blockIdx.x * kGatherWarps + (warp - 2), nw = gridDim.x * kGatherWarps;
     const int4* xv = reinterpret_cast<const int4*>(p.x);
-    for (int r = gw; r < n_post_pad; r += nw) {
-      const int asg = p.sorted_ids[r];
-      const int m = r / G.bm, jr = r % G.bm;
-      const int4* src = xv + static_cast<int64_t>(asg < p.n_assign ? asg / p.top_k : 0) * row_vec;
-      for (int c = lane; c < row_vec; c += 32) {
-        int4 v = make_int4(0, 0, 0, 0);
-        if (asg < p.n_assign) v = __ldg(src + c);
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&v);
-        float f[8];
+    for (int r0 = gw; r0 < n_post_pad; r0 += 32 * nw) {
+      const int rl = r0 + lane * nw;
+      const int asg_l = rl < n_post_pad ? __ldcg(p.sorted_ids + rl) : p.n_assign;
+      const int nrows = min(32, (n_post_pad - r0 + nw - 1) / nw);
+      for (int q = 0; q < nrows; ++q) {
+        const int asg = __shfl_sync(0xffffffffu, asg_l, q);
+        const int r = r0 + q * nw;
+        const int m = r / G.bm, jr = r - m * G.bm;
+        const int4* src = xv + static_cast<int64_t>(asg < p.n_assign ? asg / p.top_k : 0) * row_vec;
+        uint8_t* dst = p.x_q + static_cast<int64_t>(r) * p.H;
+        uint8_t* sf_row = p.x_sf + static_cast<int64_t>(m) * G.kbH * 512 + (jr & 31) * 16 + (jr >> 5) * 4;
+        if (p.xq_in != nullptr) {
+          // tokens that arrived already in MXFP8 (the EP wire): copy the
+          // e4m3 bytes (16 per lane-chunk) and move the row-major scales
+          // (4 bytes per k-block) into this M-tile's atoms
+          const int row16 = p.H / 16;
+          const int64_t src_row = asg < p.n_assign ? asg / p.top_k : -1;
+          const int4* qsrc = reinterpret_cast<const int4*>(p.xq_in) + (src_row < 0 ? 0 : src_row) * row16;
+          int4* qdst = reinterpret_cast<int4*>(dst);
+          for (int c0 = lane; c0 < row16; c0 += 32 * kUnroll) {
+            int4 v[kUnroll];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float2 t = __bfloat1622float2(h2[u]);
-          f[2 * u] = t.x;
-          f[2 * u + 1] = t.y;
+            for (int u = 0; u < kUnroll; ++u) {
+              v[u] = make_int4(0, 0, 0, 0);
+              if (c0 + 32 * u < row16 && src_row >= 0) v[u] = __ldg(qsrc + c0 + 32 * u);
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+              if (c0 + 32 * u < row16) qdst[c0 + 32 * u] = v[u];
+          }
+          for (int kb = lane; kb < G.kbH; kb += 32) {
+            const uint32_t sc =
+                src_row < 0 ? 0u : __ldg(reinterpret_cast<const uint32_t*>(p.xsf_in + src_row * (p.H / 32)) + kb);
+            *reinterpret_cast<uint32_t*>(sf_row + static_cast<int64_t>(kb) * 512) = sc;
+          }
+          continue;
         }
-        float amax = 0.f;
+        for (int c0 = lane; c0 < row_vec; c0 += 32 * kUnroll) {
+          int4 v[kUnroll];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) amax = fmaxf(amax, fabsf(f[u]));
-        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
-        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
-        const int ex = amax > 0.f ? max(-127, min(127, (int)ceilf(log2f(amax / 448.0f)))) : -127;
-        const float inv = exp2f(static_cast<float>(-ex));
-        uint2 q;
-        q.x = static_cast<uint32_t>(e4m3x2_from_float(f[0] * inv, f[1] * inv)) |
-              (static_cast<uint32_t>(e4m3x2_from_float(f[2] * inv, f[3] * inv)) << 16);
-        q.y = static_cast<uint32_t>(e4m3x2_from_float(f[4] * inv, f[5] * inv)) |
-              (static_cast<uint32_t>(e4m3x2_from_float(f[6] * inv, f[7] * inv)) << 16);
-        *reinterpret_cast<uint2*>(p.x_q + static_cast<int64_t>(r) * p.H + c * 8) = q;
-        if ((lane & 3) == 0) {
-          const int g = c >> 2;  // 32-element group index along H
-          p.x_sf[(static_cast<int64_t>(m) * G.kbH + (g >> 2)) * 512 + (jr & 31) * 16 + (jr >> 5) * 4 + (g & 3)] =
-              static_cast<uint8_t>(ex + 127);
+          for (int u = 0; u < kUnroll; ++u) {
+            v[u] = make_int4(0, 0, 0, 0);
+            if (c0 + 32 * u < row_vec && asg < p.n_assign) v[u] = __ldg(src + c0 + 32 * u);
+          }
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int c = c0 + 32 * u;
+            if (c - lane >= row_vec) break;  // warp-uniform
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+            float f[8];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const float2 t2 = __bfloat1622float2(h2[t]);
+              f[2 * t] = t2.x;
+              f[2 * t + 1] = t2.y;
+            }
+            uint32_t am = 0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) am = max(am, __float_as_uint(fabsf(f[t])));
+            am = max(am, __shfl_xor_sync(0xffffffffu, am, 1));
+            am = max(am, __shfl_xor_sync(0xffffffffu, am, 2));
+            const int ex = mx_exponent(am);
+            const float inv = mx_inv_scale(ex);
+            uint2 qv;
+            qv.x = static_cast<uint32_t>(e4m3x2_from_float(f[0] * inv, f[1] * inv)) |
+                   (static_cast<uint32_t>(e4m3x2_from_float(f[2] * inv, f[3] * inv)) << 16);
+            qv.y = static_cast<uint32_t>(e4m3x2_from_float(f[4] * inv, f[5] * inv)) |
+                   (static_cast<uint32_t>(e4m3x2_from_float(f[6] * inv, f[7] * inv)) << 16);
+            const bool in = c < row_vec;  // row_vec may be an odd multiple of 16
+            if (in) *reinterpret_cast<uint2*>(dst + c * 8) = qv;
+            // the 4 group exponents of this lane's k-block (lanes 16h .. 16h+15)
+            const int b16 = lane & 16;
+            const uint32_t e0 = __shfl_sync(0xffffffffu, ex + 127, b16);
+            const uint32_t e1 = __shfl_sync(0xffffffffu, ex + 127, b16 + 4);
+            const uint32_t e2 = __shfl_sync(0xffffffffu, ex + 127, b16 + 8);
+            const uint32_t e3 = __shfl_sync(0xffffffffu, ex + 127, b16 + 12);
+            if (in && (lane & 15) == 0)
+              *reinterpret_cast<uint32_t*>(sf_row + static_cast<int64_t>(c >> 4) * 512) =
+                  e0 | (e1 << 8) | (e2 << 16) | (e3 << 24);
+          }
         }
       }
     }
@@ -563,7 +623,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
 #endif
       const int row0 = jb.m * G.bm;
       if (jb.kind == 0) {
-        const uint32_t tx1 = u_kps * (nA * kSubTileBytes + bmN * 128) + (kFp8 ? (nA + 1) * 512 : 0);
+        const uint32_t tx1 = u_kps * (nA * kSubTileBytes + bmN * 128 + (kFp8 ? (nA + 1) * 512 : 0));
         const int wrow = jb.s * G.n_i;
         const int kb0 = G.kb_lo(jb), kb1 = G.kb_hi(jb);
         int first_pending = 0, npend = 0;
@@ -594,7 +654,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           for (int q = 0; q < u_kps; ++q)
             tma_load_2d(sb + u_tok + q * bmN * 128, tm_xs, full, (kb + q) * kKb, row0, pol_x);
           if constexpr (kFp8)
-            bulk_g2s(sb + sf_off + nA * 512, p.x_sf + (static_cast<int64_t>(jb.m) * G.kbH + kb) * 512, 512, full);
+            bulk_g2s(sb + sf_off + nA * u_kps * 512, p.x_sf + (static_cast<int64_t>(jb.m) * G.kbH + kb) * 512,
+                     u_kps * 512, full);
         };
         START_STAMP(lane == 0 && first_stamp, kTsFirstIssue);  // first stage slot is free
         first_stamp = false;
@@ -611,7 +672,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
                 const int half = nA / 2;
                 const int64_t rb = (static_cast<int64_t>(e) * 2 * p.I + (t < half ? 0 : p.I) + wrow +
                                     (t % half) * 128) / 128;
-                bulk_g2s(sb + sf_off + t * 512, p.w1_sf + (rb * G.kbH + kb) * 512, 512, full);
+                bulk_g2s(sb + sf_off + t * u_kps * 512, p.w1_sf + (rb * G.kbH + kb) * 512, u_kps * 512, full);
               }
             }
             if (gathered) {
@@ -664,11 +725,11 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         // Split phase 3: weights stream immediately; the act rows wait for
         // every phase-1 job of this M-tile (release/acquire on done[m]).
         const int n3 = warp_uniform(G.n3);
-        const uint32_t tx = u_kps * (n3 * kSubTileBytes + bmN * 128) + (kFp8 ? 2 * 512 : 0);
+        const uint32_t tx = u_kps * (n3 * kSubTileBytes + bmN * 128 + (kFp8 ? 2 * 512 : 0));
         const int wrow = e * p.H + jb.hc * n3 * 128;
         const int kb0 = G.kb_lo(jb), kb1 = G.kb_hi(jb);
-        // act tiles sit after the stage's weight area (FP8: right after the one W2 box)
-        const int a_off = kFp8 ? kSubTileBytes : u_tok;
+        // act tiles sit after the stage's weight area
+        const int a_off = u_tok;
         int first_pending = 0, npend = 0;
         bool ready = false;
         // Pull this job's whole W2 slice toward L2 now: while the act rows are
@@ -683,8 +744,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           for (int q = 0; q < u_kps; ++q)
             tma_load_2d(sb + a_off + q * bmN * 128, tm_act, full, (kb + q) * kKb, row0, pol_x);
           if constexpr (kFp8)
-            bulk_g2s(sb + kSubTileBytes + bmN * 128 + 512, p.act_sf + (static_cast<int64_t>(jb.m) * G.kbI + kb) * 512,
-                     512, full);
+            bulk_g2s(sb + sf_off + u_kps * 512, p.act_sf + (static_cast<int64_t>(jb.m) * G.kbI + kb) * 512,
+                     u_kps * 512, full);
         };
         for (int kb = kb0; kb < kb1; kb += u_kps) {
           acquire();
@@ -701,8 +762,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
                   tma_load_2d(sb + (q * n3 + t) * kSubTileBytes, tm_w2, full, (kb + q) * kKb, wrow + t * 128, pol_w);
             }
             if constexpr (kFp8)
-              bulk_g2s(sb + kSubTileBytes + bmN * 128, p.w2_sf + (static_cast<int64_t>(wrow / 128) * G.kbI + kb) * 512,
-                       512, full);
+              bulk_g2s(sb + sf_off, p.w2_sf + (static_cast<int64_t>(wrow / 128) * G.kbI + kb) * 512, u_kps * 512, full);
             if (ready) load_act(sb, full, kb);
           }
           __syncwarp();
@@ -743,9 +803,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     };
     // kps is chosen on the device per call: one compiled copy of the role per
     // value (a runtime trip count in these loops costs ~30 % of the issue rate)
-    if constexpr (kFp8) {
-      role(KpsC<1>{});
-    } else if (kps == 4) {
+    if (!kFp8 && kps == 4) {
       role(KpsC<4>{});
     } else if (kps == 2) {
       role(KpsC<2>{});
@@ -819,18 +877,21 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         for (int kb = kb0; kb < kb1; kb += u_kps) {
           const uint32_t sb = wait_full();
           const uint64_t da = sw128_kmajor_desc(sb);
-          const uint64_t db = sw128_kmajor_desc(sb + (kFp8 ? nA * kSubTileBytes : u_tok));
+          const uint64_t db = sw128_kmajor_desc(sb + u_tok);
           if (elect_one()) {
             if constexpr (kFp8) {
               // scale atoms smem -> TMEM; in-order with the MMAs that read them
-              for (int t = 0; t <= nA; ++t) tmem_cp_sf(u_tmem + kSfCol + 4 * t, sf_atom_desc(sb + sf_off + t * 512));
-              for (int t = 0; t < nA; ++t) {
+              const int n_atoms = (nA + 1) * u_kps;
+              for (int a = 0; a < n_atoms; ++a) tmem_cp_sf(u_tmem + kSfCol + 4 * a, sf_atom_desc(sb + sf_off + a * 512));
+              for (int q = 0; q < u_kps; ++q)
+                for (int t = 0; t < nA; ++t) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                  mma_mxf8(acc + t * bmN, da + ((t * kSubTileBytes + k * 32) >> 4), db + ((k * 32) >> 4),
-                           idesc_mxf8(128, bmN, k), ((kb - kb0) | k) != 0,
-                           (uint32_t(k) << 30) | (u_tmem + kSfCol + 4 * t), (uint32_t(k) << 30) | (u_tmem + kSfCol + 4 * nA));
-              }
+                  for (int k = 0; k < 4; ++k)
+                    mma_mxf8(acc + t * bmN, da + ((((q * nA + t) * kSubTileBytes) + k * 32) >> 4),
+                             db + ((q * bmN * 128 + k * 32) >> 4), idesc_mxf8(128, bmN, k), ((kb - kb0) | q | k) != 0,
+                             (uint32_t(k) << 30) | (u_tmem + kSfCol + 4 * (t * u_kps + q)),
+                             (uint32_t(k) << 30) | (u_tmem + kSfCol + 4 * (nA * u_kps + q)));
+                }
             } else {
               for (int q = 0; q < u_kps; ++q)
                 for (int t = 0; t < nA; ++t) {
@@ -880,16 +941,18 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         for (int kb = kb0; kb < kb1; kb += u_kps) {
           const uint32_t sb = wait_full();
           const uint64_t da = sw128_kmajor_desc(sb);
-          const uint64_t db = sw128_kmajor_desc(sb + (kFp8 ? kSubTileBytes : u_tok));
+          const uint64_t db = sw128_kmajor_desc(sb + u_tok);
           if (elect_one()) {
             if constexpr (kFp8) {
-              const uint32_t sfs = sb + kSubTileBytes + bmN * 128;
-              tmem_cp_sf(u_tmem + kSfCol, sf_atom_desc(sfs));
-              tmem_cp_sf(u_tmem + kSfCol + 4, sf_atom_desc(sfs + 512));
+              for (int a = 0; a < 2 * u_kps; ++a) tmem_cp_sf(u_tmem + kSfCol + 4 * a, sf_atom_desc(sb + sf_off + a * 512));
+              for (int q = 0; q < u_kps; ++q) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                mma_mxf8(acc, da + ((k * 32) >> 4), db + ((k * 32) >> 4), idesc_mxf8(128, bmN, k), ((kb - kb0) | k) != 0,
-                         (uint32_t(k) << 30) | (u_tmem + kSfCol), (uint32_t(k) << 30) | (u_tmem + kSfCol + 4));
+                for (int k = 0; k < 4; ++k)
+                  mma_mxf8(acc, da + ((q * kSubTileBytes + k * 32) >> 4), db + ((q * bmN * 128 + k * 32) >> 4),
+                           idesc_mxf8(128, bmN, k), ((kb - kb0) | q | k) != 0,
+                           (uint32_t(k) << 30) | (u_tmem + kSfCol + 4 * q),
+                           (uint32_t(k) << 30) | (u_tmem + kSfCol + 4 * (u_kps + q)));
+              }
             } else if (n3 == 1) {  // the common case keeps its compile-time trip count
               for (int q = 0; q < u_kps; ++q) {
 #pragma unroll
@@ -929,9 +992,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     };
     // kps is chosen on the device per call: one compiled copy of the role per
     // value (a runtime trip count in these loops costs ~30 % of the issue rate)
-    if constexpr (kFp8) {
-      role(KpsC<1>{});
-    } else if (kps == 4) {
+    if (!kFp8 && kps == 4) {
       role(KpsC<4>{});
     } else if (kps == 2) {
       role(KpsC<2>{});
@@ -980,22 +1041,29 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           if constexpr (kFp8) {
             // MXFP8 act for the FP8 phase-3 MMA: the warp's 32 lanes hold 32
             // consecutive features = one scale group per token
-            const int col = jb.s * G.n_i + f;
+            // (one redux per token for the group amax; the 16 x 32 bytes are
+            // transposed through this warp's 512 B of tbuf so that every lane
+            // stores 16 contiguous bytes of one token row)
+            const int l = et & 31;
+            const int col0 = jb.s * G.n_i + f - l;  // first feature of the warp's group
+            uint8_t* wbuf = reinterpret_cast<uint8_t*>(tbuf) + (et >> 5) * 512;
+            uint32_t my_sf = 0;
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
               const float a = silu_mul(g[q], u[q]);
-              float amax = fabsf(a);
-#pragma unroll
-              for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-              const int ex = amax > 0.f ? max(-127, min(127, (int)ceilf(log2f(amax / 448.0f)))) : -127;
-              const int jj = j0 + q;
-              if (jj < G.bm) {
-                p.act_q[static_cast<int64_t>(row0 + jj) * p.I + col] = e4m3_from_float(a * exp2f(static_cast<float>(-ex)));
-                if ((et & 31) == 0)
-                  p.act_sf[(static_cast<int64_t>(jb.m) * G.kbI + (col >> 7)) * 512 + (jj & 31) * 16 + (jj >> 5) * 4 +
-                           ((col >> 5) & 3)] = static_cast<uint8_t>(ex + 127);
-              }
+              const int ex = mx_exponent(warp_amax_bits(a));
+              wbuf[q * 32 + l] = e4m3_from_float(a * mx_inv_scale(ex));
+              if (l == q) my_sf = static_cast<uint32_t>(ex + 127);
             }
+            __syncwarp();
+            const int tq = l >> 1;
+            if (j0 + tq < G.bm)
+              *reinterpret_cast<int4*>(p.act_q + static_cast<int64_t>(row0 + j0 + tq) * p.I + col0 + (l & 1) * 16) =
+                  *reinterpret_cast<const int4*>(wbuf + tq * 32 + (l & 1) * 16);
+            if (l < 16 && j0 + l < G.bm)
+              p.act_sf[(static_cast<int64_t>(jb.m) * G.kbI + (col0 >> 7)) * 512 + ((j0 + l) & 31) * 16 +
+                       ((j0 + l) >> 5) * 4 + ((col0 >> 5) & 3)] = static_cast<uint8_t>(my_sf);
+            __syncwarp();
             return;
           }
           if (G.mode == kModeFused) {

@@ -10,6 +10,9 @@ namespace ramp {
 
 constexpr int kMaxBm = 128;  // largest token block the megakernel supports
 inline int bm_mma_host(int bm) { return bm <= 16 ? 16 : (bm + 15) / 16 * 16; }
+// TMEM columns kSfCol..511 hold the FP8 MMAs' scale factors (4 columns per
+// 512-byte atom, up to 16 atoms per stage); FP8 accumulators stay below.
+constexpr int kSfCol = 448;
 
 struct RouteArgs {
   const int32_t* topk_ids;
@@ -73,6 +76,8 @@ struct MoeLaunch {
   uint8_t* x_sf;    // [M-tiles][H/128][512]
   void* act_q;      // [rows, I] e4m3
   uint8_t* act_sf;  // [M-tiles][I/128][512]
+  const uint8_t* xq_in;   // optional pre-quantised tokens [S, H] e4m3 (FP8 path)
+  const uint8_t* xsf_in;  // and their row-major scales [S, H/32]
   int64_t rows;     // capacity of x_sorted / act_g
   ramp_table_t table;
   int32_t S, H, I, E, top_k;
@@ -83,6 +88,34 @@ bool pdl_prev_enabled();       // RAMP_PDL_PREV (default 0, measured neutral): r
 extern unsigned long long* g_prof_buffer;  // diagnostics, see ramp_set_profile_buffer
 
 cudaError_t launch_fused_moe(const MoeLaunch& l, cudaStream_t stream, const char** why);
+
+// expert-parallel exchange kernels (csrc/ep.cu)
+struct EpPackArgs {
+  const int32_t* ids;   // [S, k] global expert ids (outside [0, E): ignored)
+  const float* w;       // [S, k]
+  const void* x;        // [S, H] bf16
+  int32_t S, H, k, E, world, cap;
+  void* send_x;         // [world][cap][H] bf16, or e4m3 bytes (MXFP8 wire)
+  uint8_t* send_sf;     // [world][cap][H/32] UE8M0 (MXFP8 wire)
+  int32_t* send_ids;    // [world][cap][k] rank-local ids, -1 = another rank's slot / padding row
+  float* send_w;        // [world][cap][k]
+  int32_t* pos;         // [S][world] send row of (token, rank), -1 = not sent
+  int32_t* counts;      // [world] rows sent to each rank
+  int32_t* overflow;    // set to 1 when a rank needs more than cap rows (those pairs are dropped)
+};
+cudaError_t launch_ep_pack(const EpPackArgs& a, bool fp8_wire, cudaStream_t stream);
+cudaError_t launch_ep_combine(const void* back, const int32_t* pos, int32_t S, int32_t H, int32_t world,
+                              int32_t cap, void* out, cudaStream_t stream);
+// NCCL, loaded at run time (dlopen of the process's libnccl.so.2: torch's when torch is loaded)
+struct NcclApi;
+const NcclApi* nccl_api(const char** why);
+int nccl_unique_id(unsigned char out[128], const char** why);
+void* nccl_comm_init(const unsigned char id[128], int world, int rank, const char** why);
+int nccl_comm_destroy(void* comm);
+// grouped send/recv of `world` equal blocks of `block_bytes` (block d of
+// send goes to rank d, block s of recv comes from rank s); n_bufs pairs in one group
+int nccl_all_to_all(void* comm, int world, const void* const* send, void* const* recv, const size_t* block_bytes,
+                    int n_bufs, cudaStream_t stream, const char** why);
 int64_t config_smem_bytes(int bm, int ttn, int stg, int mode, bool fp8, int kps = 1);
 
 }  // namespace ramp

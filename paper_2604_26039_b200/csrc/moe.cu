@@ -81,7 +81,7 @@ int64_t config_smem_bytes(int bm, int ttn, int stg, int mode, bool fp8, int kps)
   if (bm < 1 || bm > kMaxBm || (ttn != 128 && ttn != 256 && ttn != 512) || stg < 1 || stg > kMaxStages)
     return 0;
   if (mode != kModeFused && mode != kModeSplit) return 0;
-  if (kps != 1 && (fp8 || (kps != 2 && kps != 4))) return 0;
+  if (kps != 1 && (kps != 2 && kps != 4)) return 0;
   const int b = moe_smem_bytes(bm, ttn, stg, mode, fp8, kps);
   return b <= kSmemLimit ? b : 0;
 }
@@ -210,6 +210,8 @@ cudaError_t launch_fused_moe(const MoeLaunch& l, cudaStream_t stream, const char
   p.x_sf = l.x_sf;
   p.act_q = static_cast<uint8_t*>(l.act_q);
   p.act_sf = l.act_sf;
+  p.xq_in = l.xq_in;
+  p.xsf_in = l.xsf_in;
   p.table = l.table;
   p.S = l.S;
   p.H = l.H;

@@ -236,13 +236,29 @@ __host__ __device__ constexpr uint32_t idesc_mxf8(uint32_t M, uint32_t N, uint32
 }
 __device__ __forceinline__ uint8_t e4m3_from_float(float v) {
   uint16_t r;
-  asm volatile("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(0.0f), "f"(v));
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(0.0f), "f"(v));
   return static_cast<uint8_t>(r & 0xFF);
 }
 __device__ __forceinline__ uint16_t e4m3x2_from_float(float lo, float hi) {
   uint16_t r;
-  asm volatile("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
   return r;
+}
+// MXFP8 scale of one 32-group: the smallest ex with amax <= 448 * 2^ex, i.e.
+// exactly ceil(log2(amax / 448)) clamped to UE8M0's [-127, 127], from the
+// bits of amax (non-negative): amax = m * 2^e with m in [1, 2), and
+// 448 = 1.75 * 2^8, so ex = e - 8 when m <= 1.75 and e - 7 otherwise.
+__device__ __forceinline__ int mx_exponent(uint32_t amax_bits) {
+  if (amax_bits == 0) return -127;
+  const int e = static_cast<int>(amax_bits >> 23) - 127;
+  const int ex = e - 8 + ((amax_bits & 0x7FFFFFu) > 0x600000u ? 1 : 0);
+  return max(-127, min(127, ex));
+}
+// 2^-ex as a float, exact for ex in [-127, 126] (amax of finite fp32 gives ex <= 121)
+__device__ __forceinline__ float mx_inv_scale(int ex) { return __uint_as_float(static_cast<uint32_t>(127 - ex) << 23); }
+// warp-wide max of non-negative floats: their bit patterns order as unsigned integers
+__device__ __forceinline__ uint32_t warp_amax_bits(float v) {
+  return __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(v)));
 }
 
 // Instruction descriptor, kind::f16: fp32 accumulate, bf16 A and B, both K-major.

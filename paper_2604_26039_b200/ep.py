@@ -2,44 +2,62 @@
 
 Rank r of a P-rank group owns experts [r*E/P, (r+1)*E/P).  One MoE layer:
 
-  1. dispatch: every (token, expert) assignment is routed to the owner rank
-     of its expert.  Assignments of one token bound for the same rank are
-     merged into one row (the token is sent once per destination rank, with up
-     to k (local expert, weight) pairs), so the wire carries unique
-     (token, rank) pairs -- the "pre-reduce per (token, rank)" of SURVEY §8e.
+  1. dispatch: every (token, expert) assignment goes to the owner rank of its
+     expert.  Assignments of one token bound for the same rank are merged
+     into one row (the token is sent once per destination rank, with its k
+     slots as rank-local expert ids, -1 for the other ranks' slots), so the
+     wire carries unique (token, rank) pairs -- the "pre-reduce per
+     (token, rank)" of SURVEY §8e.
   2. the owner runs the fused-MoE megakernel on its local experts: the
-     received rows are its tokens, their local expert ids / weights its top-k
-     (slots of other ranks' experts carry expert -1 and weight 0; the route
-     kernel skips them, so they cost no work);
+     received rows are its tokens (slots with expert -1 are skipped by the
+     route kernel, so they cost no work);
   3. combine: the per-(token, rank) partial outputs travel back and are
-     summed into the origin tokens.
+     summed, in rank order, into the origin tokens.
 
-The exchanges are NCCL all-to-alls (torch.distributed.all_to_all_single over
-NVLink 5 / NVSwitch); the split sizes need one small host read of the
-per-destination counts (exchanged with an all-to-all of int64 counts first;
-the (token, rank) pairs come from a [world, S] mask whose nonzeros are read
-with the already-known size, so that read is the only device sync).
-The local computation is pluggable (`local_fn`), which lets the gloo CPU tests
-check the routing, packing and combine arithmetic against a dense oracle.
+Every buffer on the wire has a FIXED capacity -- `cap` rows per destination
+(cap = S by default, which never drops a pair; rows past a destination's
+count carry ids -1) -- so no split size is ever read on the host: the whole
+layer is asynchronous and CUDA-graph capturable.  The pack (step 1's
+row/slot construction, bf16 or MXFP8 rows) and the reduce (step 3's sum)
+are device kernels of libramp_b200 (`ramp_ep_pack` / `ramp_ep_reduce`,
+csrc/ep.cu).  The exchanges run either through this library's own NCCL
+communicator (`EPComm`: `ramp_ep_dispatch` / `ramp_ep_combine`, one grouped
+NCCL send/recv per direction, the C ABI a reference-side integration binds)
+or through `torch.distributed.all_to_all_single` on the packed buffers (any
+backend; what the gloo CPU tests drive, with the oracle's restatement of the
+two kernels injected as `kernels=`).
+
+With the MXFP8 wire the received rows stay MXFP8 (e4m3 + one UE8M0 scale per
+32 features, 0.52x the bf16 bytes) and feed the FP8 megakernel directly
+(`moe.fused_moe_fp8` with a pre-quantised pair): the wire's quantisation IS
+the megakernel's operand quantisation, nothing is expanded back to bf16.
 """
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import torch
 import torch.distributed as dist
+
+from . import _lib
+
+WIRES = {"bf16": 0, "fp8": 1}  # RAMP_EP_WIRE_BF16 / RAMP_EP_WIRE_MXFP8
 
 
 @dataclass
 class EPPlan:
     """Send-side bookkeeping of one dispatch (kept for the combine)."""
 
-    send_counts: list[int]
-    recv_counts: list[int]
-    order: torch.Tensor        # unique (token, rank) pairs sorted by destination rank
-    pair_token: torch.Tensor   # origin token of every sent row (sorted order)
-    wire_bytes: int = 0        # token-row payload this rank sent (dispatch direction)
+    world: int
+    cap: int
+    wire: str
+    pos: torch.Tensor | None       # [S, world] int32: row of (token, rank) in the send blocks, -1 = not sent
+    counts: torch.Tensor | None    # [world] int32 (device): rows sent to each rank
+    overflow: torch.Tensor | None  # [1] int32 (device): 1 if some rank needed more than cap rows
+    wire_bytes: int = 0            # bytes this rank puts on the wire per dispatch (fixed blocks)
+    identity: bool = False         # world 1, no exchange: the layer ran on the inputs directly
 
 
 def expert_owner(ids: torch.Tensor, E: int, world: int) -> torch.Tensor:
@@ -47,110 +65,185 @@ def expert_owner(ids: torch.Tensor, E: int, world: int) -> torch.Tensor:
     return torch.div(ids, per, rounding_mode="floor")
 
 
+def _row_bytes(H: int, wire: str) -> int:
+    return H + H // 32 if wire == "fp8" else 2 * H
+
+
+class DeviceKernels:
+    """The pack / reduce kernels of libramp_b200 (csrc/ep.cu).  CUDA tensors
+    only; there is no CPU path."""
+
+    def pack(self, x, topk_ids, topk_w, E: int, world: int, cap: int, wire: str):
+        lib = _lib.load()
+        S, H = x.shape
+        k = topk_ids.shape[1]
+        dev = x.device
+        for name, t, dt in (("x", x, torch.bfloat16), ("topk_ids", topk_ids, torch.int32),
+                            ("topk_w", topk_w, torch.float32)):
+            if t.dtype != dt or not t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous {dt} CUDA tensor (there is no CPU path)")
+        fp8 = wire == "fp8"
+        send_x = torch.empty(world * cap, H, dtype=torch.uint8 if fp8 else torch.bfloat16, device=dev)
+        send_sf = torch.empty(world * cap, H // 32, dtype=torch.uint8, device=dev) if fp8 else None
+        send_ids = torch.empty(world * cap, k, dtype=torch.int32, device=dev)
+        send_w = torch.empty(world * cap, k, dtype=torch.float32, device=dev)
+        pos = torch.empty(S, world, dtype=torch.int32, device=dev)
+        counts = torch.empty(world, dtype=torch.int32, device=dev)
+        overflow = torch.zeros(1, dtype=torch.int32, device=dev)
+        _lib.check(lib.ramp_ep_pack(x.data_ptr(), topk_ids.data_ptr(), topk_w.data_ptr(), S, H, E, k, world, cap,
+                                    WIRES[wire], send_x.data_ptr(), send_sf.data_ptr() if fp8 else None,
+                                    send_ids.data_ptr(), send_w.data_ptr(), pos.data_ptr(), counts.data_ptr(),
+                                    overflow.data_ptr(), _stream()))
+        return send_x, send_sf, send_ids, send_w, pos, counts, overflow
+
+    def reduce(self, back, pos, world: int, cap: int):
+        lib = _lib.load()
+        S = pos.shape[0]
+        H = back.shape[1]
+        if back.dtype != torch.bfloat16 or not back.is_cuda or not back.is_contiguous():
+            raise ValueError("partial outputs must be a contiguous bf16 CUDA tensor")
+        out = torch.empty(S, H, dtype=torch.bfloat16, device=back.device)
+        _lib.check(lib.ramp_ep_reduce(back.data_ptr(), pos.data_ptr(), S, H, world, cap, out.data_ptr(), _stream()))
+        return out
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+class EPComm:
+    """libramp_b200's own NCCL communicator over a torch.distributed group
+    (rank 0 creates the NCCL unique id, the group broadcasts it).  With it,
+    dispatch / combine are single C-ABI calls (pack + one grouped NCCL
+    all-to-all; all-to-all + reduce), capturable in a CUDA graph."""
+
+    def __init__(self, group=None):
+        lib = _lib.load()
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _lib.check(lib.ramp_ep_get_unique_id(uid))
+        obj = [uid.raw]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(obj, src=src, group=group)
+        self._comm = ctypes.c_void_p()
+        _lib.check(lib.ramp_ep_comm_init(ctypes.byref(self._comm), obj[0], self.world, self.rank))
+
+    @property
+    def handle(self):
+        return self._comm
+
+    def close(self):
+        if self._comm:
+            _lib.load().ramp_ep_comm_destroy(self._comm)
+            self._comm = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter teardown
+            pass
+
+
 def dispatch(x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor, E: int, group=None,
-             wire: str = "bf16"):
-    """Route token rows to expert owners.  Returns (plan, recv_x [R, H],
-    recv_ids [R, k] local expert ids, recv_w [R, k]).
+             wire: str = "bf16", cap: int | None = None, comm: EPComm | None = None, kernels=None,
+             exchange: str = "auto"):
+    """Route token rows to expert owners.
 
-    wire = "fp8" sends the token rows as MXFP8 -- E4M3 plus
-    one UE8M0 scale per 32 features, the operand format of the FP8 megakernel,
-    H + H/32 bytes per row instead of 2H -- and the receiver expands them back
-    exactly (E4M3 x 2^k is representable in bf16); the FP8 megakernel then
-    re-derives the same per-32 scales in its gather.  The combine stays bf16."""
-    if wire not in ("bf16", "fp8"):
+    Returns (plan, recv_x, recv_ids [P*cap, k] rank-local expert ids, recv_w
+    [P*cap, k]); recv_x is [P*cap, H] bf16, or the pair (e4m3 bytes
+    [P*cap, H], UE8M0 scales [P*cap, H/32]) with wire="fp8".  Block s of the
+    received rows came from rank s; rows past its count have ids -1.
+
+    exchange="auto" takes the identity shortcut at world 1 (every expert is
+    local: the layer runs on the inputs, no pack, no collective);
+    "always" packs and exchanges at every world size (the measured path)."""
+    if wire not in WIRES:
         raise ValueError(f"wire must be bf16 or fp8, got {wire!r}")
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    per = E // world
-    S, k = topk_ids.shape
+    if exchange not in ("auto", "always"):
+        raise ValueError(f"exchange must be 'auto' or 'always', got {exchange!r}")
+    world = comm.world if comm is not None else dist.get_world_size(group)
+    if E % world:
+        raise ValueError(f"E={E} does not split over {world} ranks")
+    S, H = x.shape
+    k = topk_ids.shape[1]
+    if world == 1 and exchange == "auto" and comm is None:
+        plan = EPPlan(world=1, cap=S, wire=wire, pos=None, counts=None, overflow=None, identity=True)
+        return plan, x, topk_ids, topk_w
+    cap = S if cap is None else int(cap)
+    if cap < 0:
+        raise ValueError("cap must be >= 0")
+    fp8 = wire == "fp8"
     dev = x.device
-    if world == 1:
-        # One rank owns every expert: each token is one row and the exchanges
-        # are identities -- no collectives and no host read, so the layer
-        # stays asynchronous (the MXFP8 wire rounding is still applied, so
-        # the numerics match the multi-rank path).
-        pair_token = torch.arange(S, device=dev)
-        recv_x = x
-        if wire == "fp8":
-            from .quant import mx_dequantize, mx_quantize
-
-            recv_x = mx_dequantize(*mx_quantize(x)).to(x.dtype)
-        plan = EPPlan(send_counts=[S], recv_counts=[S], order=pair_token, pair_token=pair_token, wire_bytes=0)
-        return plan, recv_x, topk_ids.to(torch.int32), topk_w
-    owner = expert_owner(topk_ids.long(), E, world)                     # [S, k]
-    # unique (token, rank) pairs as a [world, S] mask: its row-major nonzeros
-    # are ordered by destination rank then token (no sort, no device sync)
-    mask = torch.zeros(world, S, dtype=torch.bool, device=dev)
-    mask[owner, torch.arange(S, device=dev)[:, None].expand(S, k)] = True
-    send_counts = mask.sum(1)
-    recv_counts = torch.empty_like(send_counts)
-    dist.all_to_all_single(recv_counts, send_counts, group=group)
-    counts = torch.cat([send_counts, recv_counts]).tolist()              # the one host read
-    sc, rc = counts[:world], counts[world:]
-    pairs = torch.nonzero_static(mask.reshape(-1), size=sum(sc)).squeeze(1)
-    pair_rank = torch.div(pairs, S, rounding_mode="floor")
-    pair_token = pairs % S
-    # per sent row: the token's assignments that live on that rank (others -> weight 0)
-    row_owner = owner[pair_token]                                        # [P, k]
-    hit = row_owner == pair_rank[:, None]
-    # slots of other ranks' experts carry -1: the route kernel skips them
-    row_ids = torch.where(hit, topk_ids[pair_token].long() - pair_rank[:, None] * per, -1)
-    row_w = torch.where(hit, topk_w[pair_token], torch.zeros((), dtype=topk_w.dtype, device=dev))
-    send_x = x[pair_token].contiguous()
-    R = sum(rc)
-    H = x.shape[1]
-    if wire == "fp8":
-        from .quant import GROUP, mx_dequantize, mx_quantize
-
-        q, sf = mx_quantize(send_x)
-        recv_q = torch.empty(R, H, dtype=torch.uint8, device=dev)
-        recv_sf = torch.empty(R, H // GROUP, dtype=torch.uint8, device=dev)
-        dist.all_to_all_single(recv_q, q.view(torch.uint8).contiguous(), rc, sc, group=group)
-        dist.all_to_all_single(recv_sf, sf.contiguous(), rc, sc, group=group)
-        recv_x = mx_dequantize(recv_q.view(torch.float8_e4m3fn), recv_sf).to(x.dtype)
-        wire_bytes = int(send_x.shape[0]) * (H + H // GROUP)
+    recv_x = torch.empty(world * cap, H, dtype=torch.uint8 if fp8 else x.dtype, device=dev)
+    recv_sf = torch.empty(world * cap, H // 32, dtype=torch.uint8, device=dev) if fp8 else None
+    recv_ids = torch.empty(world * cap, k, dtype=torch.int32, device=dev)
+    recv_w = torch.empty(world * cap, k, dtype=torch.float32, device=dev)
+    if comm is not None:
+        lib = _lib.load()
+        send_x = torch.empty_like(recv_x)
+        send_sf = torch.empty_like(recv_sf) if fp8 else None
+        send_ids, send_w = torch.empty_like(recv_ids), torch.empty_like(recv_w)
+        pos = torch.empty(S, world, dtype=torch.int32, device=dev)
+        counts = torch.empty(world, dtype=torch.int32, device=dev)
+        overflow = torch.zeros(1, dtype=torch.int32, device=dev)
+        for name, t, dt in (("x", x, torch.bfloat16), ("topk_ids", topk_ids, torch.int32),
+                            ("topk_w", topk_w, torch.float32)):
+            if t.dtype != dt or not t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous {dt} CUDA tensor (there is no CPU path)")
+        _lib.check(lib.ramp_ep_dispatch(
+            comm.handle, x.data_ptr(), topk_ids.data_ptr(), topk_w.data_ptr(), S, H, E, k, cap, WIRES[wire],
+            send_x.data_ptr(), send_sf.data_ptr() if fp8 else None, send_ids.data_ptr(), send_w.data_ptr(),
+            pos.data_ptr(), counts.data_ptr(), overflow.data_ptr(), recv_x.data_ptr(),
+            recv_sf.data_ptr() if fp8 else None, recv_ids.data_ptr(), recv_w.data_ptr(), _stream()))
     else:
-        recv_x = torch.empty(R, H, dtype=x.dtype, device=dev)
-        dist.all_to_all_single(recv_x, send_x, rc, sc, group=group)
-        wire_bytes = int(send_x.numel() * send_x.element_size())
-    if topk_w.dtype == torch.float32:
-        # local ids (int32) and weights (fp32 bits) travel as one [P, k, 2] int32 exchange
-        meta = torch.stack([row_ids.to(torch.int32), row_w.contiguous().view(torch.int32)], dim=-1).contiguous()
-        recv_meta = torch.empty(R, k, 2, dtype=torch.int32, device=dev)
-        dist.all_to_all_single(recv_meta, meta, rc, sc, group=group)
-        recv_ids = recv_meta[..., 0].contiguous()
-        recv_w = recv_meta[..., 1].contiguous().view(torch.float32)
-    else:
-        recv_ids = torch.empty(R, k, dtype=torch.int32, device=dev)
-        recv_w = torch.empty(R, k, dtype=topk_w.dtype, device=dev)
-        dist.all_to_all_single(recv_ids, row_ids.to(torch.int32).contiguous(), rc, sc, group=group)
-        dist.all_to_all_single(recv_w, row_w.contiguous(), rc, sc, group=group)
-    plan = EPPlan(send_counts=sc, recv_counts=rc, order=pairs, pair_token=pair_token, wire_bytes=wire_bytes)
-    return plan, recv_x, recv_ids, recv_w
+        kernels = kernels or DeviceKernels()
+        send_x, send_sf, send_ids, send_w, pos, counts, overflow = kernels.pack(x, topk_ids, topk_w, E, world, cap,
+                                                                                wire)
+        # equal blocks of cap rows: no split sizes to exchange first
+        dist.all_to_all_single(recv_x, send_x, group=group)
+        if fp8:
+            dist.all_to_all_single(recv_sf, send_sf, group=group)
+        dist.all_to_all_single(recv_ids, send_ids, group=group)
+        dist.all_to_all_single(recv_w, send_w, group=group)
+    plan = EPPlan(world=world, cap=cap, wire=wire, pos=pos, counts=counts, overflow=overflow,
+                  wire_bytes=world * cap * (_row_bytes(H, wire) + 8 * k))
+    return plan, ((recv_x, recv_sf) if fp8 else recv_x), recv_ids, recv_w
 
 
-def combine(plan: EPPlan, partial: torch.Tensor, S: int, group=None) -> torch.Tensor:
-    """Return per-(token, rank) partial outputs to their origin and sum them."""
-    if dist.get_world_size(group) == 1:
+def combine(plan: EPPlan, partial: torch.Tensor, group=None, comm: EPComm | None = None, kernels=None) -> torch.Tensor:
+    """Return the per-(token, rank) partial outputs [P*cap, H] to their origin
+    ranks and sum them (rank order, fp32) into [S, H]."""
+    if plan.identity:
         return partial  # one row per token, already in token order
-    back = torch.empty(sum(plan.send_counts), partial.shape[1], dtype=partial.dtype, device=partial.device)
-    dist.all_to_all_single(back, partial.contiguous(), plan.send_counts, plan.recv_counts, group=group)
-    out = torch.zeros(S, partial.shape[1], dtype=torch.float32, device=partial.device)
-    out.index_add_(0, plan.pair_token, back.float())
-    return out.to(partial.dtype)
+    back = torch.empty_like(partial)
+    if comm is not None:
+        lib = _lib.load()
+        S = plan.pos.shape[0]
+        H = partial.shape[1]
+        out = torch.empty(S, H, dtype=partial.dtype, device=partial.device)
+        _lib.check(lib.ramp_ep_combine(comm.handle, partial.data_ptr(), back.data_ptr(), plan.pos.data_ptr(), S, H,
+                                       plan.cap, out.data_ptr(), _stream()))
+        return out
+    dist.all_to_all_single(back, partial.contiguous(), group=group)
+    return (kernels or DeviceKernels()).reduce(back, plan.pos, plan.world, plan.cap)
 
 
-def ep_moe_layer(x, topk_ids, topk_w, E: int, local_fn, group=None, wire: str = "bf16"):
+def ep_moe_layer(x, topk_ids, topk_w, E: int, local_fn, group=None, wire: str = "bf16", cap: int | None = None,
+                 comm: EPComm | None = None, kernels=None, exchange: str = "auto"):
     """dispatch -> local_fn(recv_x, recv_ids, recv_w) -> combine."""
-    plan, rx, rids, rw = dispatch(x, topk_ids, topk_w, E, group, wire=wire)
+    plan, rx, rids, rw = dispatch(x, topk_ids, topk_w, E, group, wire=wire, cap=cap, comm=comm, kernels=kernels,
+                                  exchange=exchange)
     partial = local_fn(rx, rids, rw)
-    return combine(plan, partial, x.shape[0], group)
+    return combine(plan, partial, group, comm=comm, kernels=kernels)
 
 
 def make_local_megakernel(weights, table, workspace_cache: dict | None = None):
     """local_fn running the B200 megakernel on this rank's experts.
     `weights` is (w1_local, w2_local) bf16 or a quant.MxFp8Weights of the
-    local experts (then `table` must be an FP8 pool's)."""
+    local experts (then `table` must be an FP8 pool's).  The FP8 megakernel
+    also takes the MXFP8 wire's (e4m3, scales) rows as they arrived."""
     from .moe import Workspace, fused_moe, fused_moe_fp8
 
     cache = workspace_cache if workspace_cache is not None else {}
@@ -163,16 +256,17 @@ def make_local_megakernel(weights, table, workspace_cache: dict | None = None):
         I = two_i // 2
 
     def run(rx, rids, rw):
-        if rx.shape[0] == 0:
-            return torch.zeros(0, rx.shape[1], dtype=rx.dtype, device=rx.device)
-        key = (rx.shape[0], rids.shape[1])
+        rows = (rx[0] if isinstance(rx, tuple) else rx).shape[0]
+        if rows == 0:
+            return torch.zeros(0, H, dtype=torch.bfloat16, device=rids.device)
+        key = (rows, rids.shape[1])
         ws = cache.get(key)
         if ws is None:
-            ws = cache[key] = Workspace(rx.shape[0], H, I, E_l, rids.shape[1], device=rx.device)
+            ws = cache[key] = Workspace(rows, H, I, E_l, rids.shape[1], device=rids.device)
         if fp8:
-            return fused_moe_fp8(rx.contiguous(), weights, rw.float().contiguous(), rids.contiguous(), table,
-                                 workspace=ws)
-        return fused_moe(rx.contiguous(), w1_local, w2_local, rw.float().contiguous(), rids.contiguous(), table,
-                         workspace=ws)
+            return fused_moe_fp8(rx, weights, rw, rids, table, workspace=ws)
+        if isinstance(rx, tuple):
+            raise ValueError("the BF16 megakernel takes bf16 rows: use wire='bf16' (or an FP8 table)")
+        return fused_moe(rx, w1_local, w2_local, rw, rids, table, workspace=ws)
 
     return run

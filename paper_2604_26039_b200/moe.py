@@ -138,14 +138,15 @@ class DeviceTable:
         return ctypes.byref(self.struct)
 
     def fp8_compatible(self) -> bool:
-        """Every config runnable by the FP8 megakernel (split mode, no split-K,
-        bm >= 16, ttn >= 256, ramp_config_smem_bytes_fp8 > 0)."""
+        """Every config runnable by the FP8 megakernel (split mode, ttn >= 256,
+        ramp_config_smem_bytes_fp8_kps > 0)."""
         ok = getattr(self, "_fp8_ok", None)
         if ok is not None:
             return ok
         lib = _lib.load()
-        self._fp8_ok = all(int(m) == 1 and int(sk) == 1 and lib.ramp_config_smem_bytes_fp8(int(bm), int(t), int(st)) > 0
-                           for bm, t, st, sk, m in zip(self.bm, self.ttn, self.stg, self.split_k, self.mode))
+        kps = self.kps if self.kps is not None else np.ones(len(self.bm), dtype=np.int64)
+        self._fp8_ok = all(int(m) == 1 and lib.ramp_config_smem_bytes_fp8_kps(int(bm), int(t), int(st), int(kp)) > 0
+                           for bm, t, st, m, kp in zip(self.bm, self.ttn, self.stg, self.mode, kps))
         return self._fp8_ok
 
 
@@ -350,18 +351,32 @@ def fused_moe_fp8(
     `weights` is a quant.MxFp8Weights (E4M3 experts + UE8M0 scale atoms, from
     prepare_mxfp8_weights or prepare_block128_weights).  hidden_states stay
     bf16 [S, H]; the megakernel quantises each gathered token row (one scale
-    per 32 features) and the SwiGLU activation the same way, multiplies with
+    per 32 features) -- or hidden_states is a pair (x_q [S, H] e4m3 / uint8,
+    x_sf [S, H/32] uint8 UE8M0) of tokens already in that format (e.g. off the
+    MXFP8 expert-parallel wire), which phase 0 then only moves -- and the
+    SwiGLU activation the same way, multiplies with
     kind::mxf8f6f4.block_scale MMAs and accumulates in fp32; the output is
     bf16.  The table must be an FP8 pool (enumerate_b200_configs(...,
     dtype="fp8")); `forced_cfg` / `phases` / `validate` as in `fused_moe`.
     """
     lib = _lib.load()
+    x_sf = None
+    if isinstance(hidden_states, (tuple, list)):
+        hidden_states, x_sf = hidden_states
+        if hidden_states.dtype == torch.float8_e4m3fn:
+            hidden_states = hidden_states.view(torch.uint8)
     S, H = hidden_states.shape
     E, H1, I = weights.shape
     k = topk_ids.shape[1]
     if H1 != H:
         raise ValueError(f"shape mismatch: x {tuple(hidden_states.shape)}, experts d_model {H1}")
-    for name, t, dt in (("hidden_states", hidden_states, torch.bfloat16),
+    extra = ()
+    if x_sf is not None:
+        if tuple(x_sf.shape) != (S, H // 32):
+            raise ValueError("x_sf must be [S, H/32] (one UE8M0 scale per 32 features)")
+        extra = (("x_sf", x_sf, torch.uint8),)
+    for name, t, dt in (("hidden_states", hidden_states, torch.uint8 if x_sf is not None else torch.bfloat16),
+                        *extra,
                         ("w1_q", weights.w1_q, torch.float8_e4m3fn), ("w2_q", weights.w2_q, torch.float8_e4m3fn),
                         ("w1_sf", weights.w1_sf, torch.uint8), ("w2_sf", weights.w2_sf, torch.uint8),
                         ("topk_weights", topk_weights, torch.float32), ("topk_ids", topk_ids, torch.int32)):
@@ -382,14 +397,14 @@ def fused_moe_fp8(
         out = torch.empty(S, H, dtype=torch.bfloat16, device=hidden_states.device)
     if workspace is None or not workspace.fits(S, H, I, E, k):
         workspace = Workspace(S, H, I, E, k, device=hidden_states.device)
-    _lib.check(
-        lib.ramp_fused_moe_fp8(
-            hidden_states.data_ptr(), weights.w1_q.data_ptr(), weights.w1_sf.data_ptr(), weights.w2_q.data_ptr(),
+    tail = (weights.w1_q.data_ptr(), weights.w1_sf.data_ptr(), weights.w2_q.data_ptr(),
             weights.w2_sf.data_ptr(), topk_weights.data_ptr(), topk_ids.data_ptr(), S, H, I, E, k, table.ref,
             table.table_index(int(forced_cfg)), out.data_ptr(), workspace.sel.data_ptr(), workspace.buf.data_ptr(),
-            workspace.buf.numel(), int(phases), _stream(),
-        )
-    )
+            workspace.buf.numel(), int(phases), _stream())
+    if x_sf is None:
+        _lib.check(lib.ramp_fused_moe_fp8(hidden_states.data_ptr(), *tail))
+    else:
+        _lib.check(lib.ramp_fused_moe_fp8_prequant(hidden_states.data_ptr(), x_sf.data_ptr(), *tail))
     if validate and phases & 1:
         _raise_if_invalid_ids(workspace, E)
     return out

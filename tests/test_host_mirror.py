@@ -264,6 +264,10 @@ def test_b4_host_select_matches_oracle():
         want, _ = R.select(cfgs, coeffs, counts.tolist(), g.N, 148, True, ntile=cols["ntile"].tolist(),
                            omega_max=float("inf"), lam=lam)
         assert table.host_select(ExpertHistogram(tuple(int(c) for c in counts))) == want
+        co4 = np.array(coeffs)
+        got = R.select_np(cols["bm"], cols["ttn"], cols["split_k"], co4[:, 0], co4[:, 1], co4[:, 2], co4[:, 3],
+                          counts, g.N, 148, True, ntile=cols["ntile"], omega_max=float("inf"), lam=np.array(lam))
+        assert got[0] == want
 
 
 def test_b4_fit_recovers_planted_model():

@@ -101,6 +101,21 @@ def test_select_matches_reference(entry):
     np.testing.assert_allclose(got, want, rtol=5e-16, atol=0)
 
 
+@pytest.mark.parametrize("entry", range(3))
+def test_vectorised_select_matches_reference(entry):
+    """select_np (the timed CPU dispatch baseline) picks what ramp.select_config
+    picked, with the same evaluation count, on the reference's fitted tables."""
+    tab = golden("tables.json")[entry]
+    E, N, K = _geom_ENK(tab["geom"])
+    pool = R.reference_pool(E, N, K, elem=2 if tab["hw"] == "b200" else 1)
+    co = np.array([c[:4] for c in tab["coeffs"]], dtype=np.float64)
+    cols = {k: np.array([c[k] for c in pool]) for k in ("bm", "ttn", "split_k")}
+    for pick in tab["picks"]:
+        got = R.select_np(cols["bm"], cols["ttn"], cols["split_k"], co[:, 0], co[:, 1], co[:, 2], co[:, 3],
+                          pick["counts"], N, tab["sm_count"], K / 128 >= 48)
+        assert got == (pick["selected"], pick["evaluations"])
+
+
 def test_fit_matches_reference():
     for f in golden("fits.json"):
         got = R.fit(f["g"], f["t"], 132, f["variant"])

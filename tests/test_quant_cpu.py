@@ -96,5 +96,19 @@ def test_fp8_pool_and_table_gate():
                         c=np.zeros(n), d=np.zeros(n), N=g.N, kappa_ok=False, sm_count=148, device="cpu")
         assert t.fp8_compatible() is want
         if dtype == "fp8":
-            assert all(c.mode == 1 and c.split_k == 1 and c.bm >= 16 and c.ttn >= 256 for c in pool)
-            assert all(0 < b200_smem_bytes_fp8(c.bm, c.ttn, c.stg) <= 232448 for c in pool)
+            # split mode, ttn >= 256; every bm of the BF16 space, kps 1/2 and
+            # split-K for the small token blocks (the polymorphic FP8 space)
+            assert all(c.mode == 1 and c.ttn >= 256 and c.kps in (1, 2) for c in pool)
+            assert {c.bm for c in pool} == {4, 8, 16, 32, 64, 128}
+            assert {c.kps for c in pool} == {1, 2} and {c.split_k for c in pool} == {1, 2}
+            assert all(0 < b200_smem_bytes_fp8(c.bm, c.ttn, c.stg, c.kps) <= 232448 for c in pool)
+            assert len(pool) >= 100
+            lib_sizes = {(c.bm, c.ttn, c.stg, c.kps): b200_smem_bytes_fp8(c.bm, c.ttn, c.stg, c.kps) for c in pool}
+            from paper_2604_26039_b200 import _lib
+            try:
+                lib = _lib.load()
+            except Exception:  # noqa: BLE001 - the C ABI test covers loading
+                lib = None
+            if lib is not None:
+                for (bm, ttn, stg, kps), b in lib_sizes.items():
+                    assert lib.ramp_config_smem_bytes_fp8_kps(bm, ttn, stg, kps) == b
