@@ -209,6 +209,47 @@ def reference_arm(args, geom):
 
 
 # ------------------------------------------------------------------ FP8 leg
+def fp8_row_errors(geom, wq, x, ids, w, out, n_rows=16, seed=0):
+    """Norm-wise relative error of the MXFP8 layer on a sample of output rows
+    against (a) plain fp32 math on the dequantised expert weights (tokens and
+    activations unquantised: north_star's "vs the reference's fp32 output")
+    and (b) the same math with the tokens and SwiGLU activations quantised per
+    32 exactly as the kernel does (what is left: accumulation order, bf16 out)."""
+    import torch
+
+    from paper_2604_26039_b200.quant import GROUP, mx_dequantize, quantize_tokens_ref, untile_scales
+
+    H, I, k = geom.K, geom.N // 2, geom.top_k
+    S = x.shape[0]
+    rows = np.random.default_rng(seed).choice(S, size=min(n_rows, S), replace=False)
+    r1, r2 = 2 * I // 128, H // 128
+    cache = {}
+
+    def expert(e):
+        if e not in cache:
+            s1 = untile_scales(wq.w1_sf[e * r1:(e + 1) * r1]).reshape(2 * I, H // GROUP)
+            s2 = untile_scales(wq.w2_sf[e * r2:(e + 1) * r2]).reshape(H, I // GROUP)
+            cache[e] = (mx_dequantize(wq.w1_q[e], s1), mx_dequantize(wq.w2_q[e], s2))
+        return cache[e]
+
+    ref32 = torch.zeros(len(rows), H, device=x.device)
+    refq = torch.zeros_like(ref32)
+    xf = x.float()
+    for r, t in enumerate(rows):
+        xq = quantize_tokens_ref(xf[t][None])[0]
+        for j in range(k):
+            d1, d2 = expert(int(ids[t, j]))
+            h = d1 @ xf[t]
+            ref32[r] += float(w[t, j]) * (d2 @ (torch.nn.functional.silu(h[:I]) * h[I:]))
+            hq = d1 @ xq
+            aq = quantize_tokens_ref((torch.nn.functional.silu(hq[:I]) * hq[I:])[None])[0]
+            refq[r] += float(w[t, j]) * (d2 @ aq)
+    o = out.float()[rows]
+    return {"rows": len(rows), "vs_fp32": float((o - ref32).norm() / ref32.norm()),
+            "vs_mx_emulation": float((o - refq).norm() / refq.norm())}
+
+
+
 FP8_MODEL = "Qwen3-30B-A3B"
 FP8_BATCHES = (1, 8, 32, 128, 512, 2048)
 FP8_BETAS = (0.5, 0.55)  # 12 / 15 of 128 experts active: BASELINE configs[2]'s 8-14% skew
@@ -279,9 +320,13 @@ def fp8_leg(dev):
             rows.append({"S": S, "beta": beta, "active": a, "us": round(us, 2),
                          "tflops": round(6 * S * k * H * I / us / 1e6, 2), "gbs": round(nbytes / us / 1e3, 1),
                          "cfg": {"id": c.id, "bm": c.bm, "ttn": c.ttn, "stg": c.stg, "group_m": int(c.group_m)}})
+    # accuracy on the last point's routing (full geometry, sampled rows)
+    acc = fp8_row_errors(geom, copies[0], x, ids, w,
+                         moe.fused_moe_fp8(x, copies[0], w, ids, dtab, -1, workspace=ws))
+    acc["point"] = {"S": rows[-1]["S"], "beta": rows[-1]["beta"]}
     del copies
     torch.cuda.empty_cache()
-    return {"workload": f"{FP8_MODEL} MoE layer (E=128, top-8, d=2048, d_ff=768) MXFP8 W8A8, skewed routing "
+    return {"accuracy": acc, "workload": f"{FP8_MODEL} MoE layer (E=128, top-8, d=2048, d_ff=768) MXFP8 W8A8, skewed routing "
                         f"beta in {FP8_BETAS} (12/15 of 128 experts active), on-device dispatch over the FP8 pool",
             "dtype": "e4m3 x e4m3 (UE8M0 per 32) -> fp32", "l2": f"{FP8_COPIES} rotating weight copies",
             "timing": f"graph of {2 * FP8_COPIES} back-to-back layer calls, median replay time / calls",
@@ -454,6 +499,10 @@ def ep_leg(dev, world, rank, iters=10, warmup=3):
     plan, rx, rids, rw = ep.dispatch(x, ids, w, geom.E, wire="fp8", comm=comm)
     local_us = timed(lambda: local_fn(rx, rids, rw))
     ident_us = timed(lambda: ep.ep_moe_layer(x, ids, w, geom.E, local_fn, wire="fp8")) if world == 1 else None
+    acc = None
+    if world == 1:  # every expert is local: sample rows of the exchanged layer against fp32
+        acc = fp8_row_errors(geom, weights, x, ids, w,
+                             ep.ep_moe_layer(x, ids, w, geom.E, local_fn, wire="fp8", comm=comm))
     torch.cuda.synchronize()
     overflow = int(plan.overflow.item())
     rows = torch.tensor([float(plan.counts.sum().item())], device=dev)
@@ -471,6 +520,8 @@ def ep_leg(dev, world, rank, iters=10, warmup=3):
            "exchange_overhead": us / local_us, "rows_sent_max": int(rows.item()), "overflow": overflow,
            "dispatch_wire_bytes": plan.wire_bytes, "tflops": flops / us / 1e6,
            "timing": "CUDA graph of 4 layer calls, median of iters, max over ranks", "coeffs": path.name}
+    if acc is not None:
+        out["accuracy"] = acc
     if world == 1:
         out["identity_us_per_layer"] = ident_us
         out["note"] = ("world 1: the exchange runs over a one-rank NCCL communicator (self send/recv); "
@@ -523,6 +574,18 @@ def roofline_summary(geom, pts, per_point, step_us, k3_bytes, k3_time):
         out["traffic"] = t.get("dram_bytes_per_launch")
         out["traffic_vs_algorithmic"] = t.get("dram_over_algorithmic")
         out["traffic_source"] = t.get("source")
+    return out
+
+
+def compact_leg(leg, keys):
+    """A side leg for the JSON line: its summary fields plus one short row per
+    point (the full records go to the per-point file)."""
+    if not isinstance(leg, dict) or "points" not in leg:
+        return leg
+    out = {k: v for k, v in leg.items() if k not in ("points", "workload", "method", "timing", "dtype", "l2")}
+    out["workload"] = leg.get("workload", "")[:120]
+    out["points_" + "_".join(keys)] = [[r.get(k) for k in keys] + ([r["dispatched"]["us"]] if "dispatched" in r else [])
+                                       for r in leg["points"]]
     return out
 
 
@@ -863,7 +926,7 @@ def ours(args, geom):
             fp8 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     roof = roofline_summary(geom, pts, per_point, ms / args.steps * 1e3, k3_bytes, k3_time)
-    pp_path = write_per_point(per_point)
+    pp_path = write_per_point({"olmoe": per_point, "fp8": fp8, "mixtral": mix})
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -885,8 +948,8 @@ def ours(args, geom):
         "dispatch": ra,
         "per_point_us": [[r["S"], r["beta"], r["us"]] for r in per_point],
         "per_point_file": pp_path,
-        "fp8": fp8,
-        "mixtral": mix,
+        "fp8": compact_leg(fp8, ("S", "beta", "us", "tflops")),
+        "mixtral": compact_leg(mix, ("S", "beta", "us")),
         "ep": ep_res,
     }
     print(json.dumps(line), flush=True)

@@ -56,9 +56,10 @@ WorkspaceLayout layout_for(int32_t S, int32_t H, int32_t I, int32_t E, int32_t t
   w.xs = take(2 * (size_t)w.rows * H);
   w.act = take(2 * (size_t)w.rows * I);
   w.acc_a = take(4 * (size_t)w.rows * 2 * I);
-  w.split_cnt = take(sizeof(int32_t) * w.capacity);
-  // FP8 scale atoms per M-tile: n_post_pad / bm <= n_assign / bm + E M-tiles, bm >= 4
+  // M-tiles: n_post_pad / bm <= n_assign / bm + E, bm >= 4
   const int64_t mt_max = n_assign / 4 + E + 1;
+  // split-K arrival counters, one per (M-tile, stripe): stripes = I / (ttn/2) <= I / 64
+  w.split_cnt = take(sizeof(int32_t) * (size_t)mt_max * (I / 64 + 1));
   w.xq = take((size_t)w.rows * H);
   w.xsf = take((size_t)mt_max * (H / 128 + 1) * 512);
   w.actq = take((size_t)w.rows * I);

@@ -238,7 +238,8 @@ struct Job {
 struct Geometry {
   int mode, bm, bmN, nA, n_i, stripes, n_mtiles, n_hc, kbH, kbI, nJobA, total, group_m, sk, kps;
   int n3, n_hj;  // split phase 3: 128-row H chunks per job (shared act tile), jobs per M-tile
-  bool dbl;  // TMEM double buffering across jobs (split mode, fits in 256 columns)
+  bool dbl;      // TMEM double buffering across jobs (split mode)
+  int dbl_cols;  // jobs whose accumulator fits in this many columns alternate between two buffers
   __device__ __forceinline__ Job job(int j) const {
     Job r;
     if (j < nJobA) {
@@ -258,6 +259,14 @@ struct Geometry {
     }
     return r;
   }
+  // TMEM accumulator buffer of the jl-th job of this CTA: jobs whose
+  // accumulator fits in dbl_cols columns alternate between buffers 0 and 1
+  // (column offset 256), so the epilogue drains one while the MMAs fill the
+  // other; wider ones always use buffer 0.  MMA and epilogue roles agree.
+  __device__ __forceinline__ int acc_buf(const Job& jb, uint32_t jl) const {
+    const int cols = (jb.kind ? n3 : nA) * bmN;
+    return dbl && cols <= dbl_cols ? static_cast<int>(jl & 1u) : 0;
+  }
   // k-block range [lo, hi) of a job's reduction (H for phase 1, I for phase 3)
   __device__ __forceinline__ int kb_lo(const Job& jb) const { return jb.kq * (jb.kind ? kbI : kbH) / sk; }
   __device__ __forceinline__ int kb_hi(const Job& jb) const { return (jb.kq + 1) * (jb.kind ? kbI : kbH) / sk; }
@@ -267,28 +276,47 @@ struct Geometry {
 // which is silu's limit, and its ~2 ulp error is far below the bf16 rounding.
 __device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.0f + __expf(-g)) * u; }
 
-// Scatter-reduce 16 token columns of a [128 x bm] TMEM accumulator block into
-// out (fp32): scale by the top-k weight, transpose through shared memory so
-// each lane owns 4 consecutive rows, then one 16-byte vector reduction.
-__device__ __forceinline__ void scatter16(const float (&v)[16], int j0, int bm, int et, float* tbuf,
-                                          const CtrlSmem& cs, float* out, int H, int h0) {
+// 4x4 transpose within each lane quad: lane b (= lane & 3) holds x[j] =
+// M[b][j] on entry and M[j][b] on exit (two shuffle rounds, 4 shuffles).
+__device__ __forceinline__ void quad_transpose(float (&x)[4], int b) {
 #pragma unroll
-  for (int q = 0; q < 16; ++q) tbuf[q * 128 + et] = v[q] * cs.epi_w[j0 + q < bm ? j0 + q : 0];
-  named_bar_sync(1, 128);
-  const int w = et >> 5, l = et & 31;
+  for (int m = 1; m <= 2; m <<= 1) {
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int q = w * 4 + r;
-    const int j = j0 + q;
-    if (j < bm) {
-      const int tok = cs.epi_tok[j];
-      if (tok >= 0) {
-        const float4 x = *reinterpret_cast<const float4*>(tbuf + q * 128 + 4 * l);
-        red_add_v4_f32(out + static_cast<size_t>(tok) * H + h0 + 4 * l, x);
-      }
+    for (int j = 0; j < 4; ++j) {
+      if (j & m) continue;
+      const bool hi = b & m;
+      const float send = hi ? x[j] : x[j + m];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, m);
+      if (hi) x[j] = recv; else x[j + m] = recv;
     }
   }
-  named_bar_sync(1, 128);
+}
+
+// Scatter-reduce 16 token columns of a [128 x bm] TMEM accumulator block into
+// out (fp32) as 16-byte vector reductions, without shared memory or a
+// barrier: thread et holds row h0 + et for tokens j0..j0+15; after scaling by
+// the top-k weights, a 4x4 register transpose inside every lane quad gives
+// lane 4a+b the rows 4a..4a+3 of its quad for tokens b, b+4, b+8, b+12 --
+// four red.global.add.v4.f32 per lane, 128-byte contiguous per token row.
+__device__ __forceinline__ void scatter16(const float (&v)[16], int j0, int bm, int et, const CtrlSmem& cs,
+                                          float* out, int H, int h0) {
+  const int b = et & 3;
+  const int hrow = h0 + (et & ~3);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float x[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int q = j0 + 4 * c + j;
+      x[j] = v[4 * c + j] * cs.epi_w[q < bm ? q : 0];
+    }
+    quad_transpose(x, b);
+    const int q = j0 + 4 * c + b;
+    if (q < bm) {
+      const int tok = cs.epi_tok[q];
+      if (tok >= 0) red_add_v4_f32(out + static_cast<size_t>(tok) * H + hrow, make_float4(x[0], x[1], x[2], x[3]));
+    }
+  }
 }
 
 template <bool kFp8>
@@ -382,7 +410,10 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   }
   G.n_hj = pdiv<kFp8>(G.n_hc, G.n3);
   G.total = G.nJobA + (G.mode == kModeSplit ? G.n_mtiles * G.n_hj * G.sk : 0);
-  G.dbl = !kFp8 && G.mode == kModeSplit && G.nA * G.bmN <= 256;
+  // every job fits in buffer 0 (columns < 256, disjoint from buffer 1); FP8:
+  // buffer 1 (columns 256..) must also stay below the scale-factor columns
+  G.dbl = G.mode == kModeSplit && G.nA * G.bmN <= 256;
+  G.dbl_cols = kFp8 ? kSfCol - 256 : 256;
   // k-blocks per stage; every job's k-range must split into whole stages
   // (FP8: at most 16 scale atoms per stage)
   G.kps = cf.kps;
@@ -861,7 +892,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       if (j < 0) break;
       ++items;
       const Job jb = G.job(j);
-      const int r = G.dbl ? (jl & 1) : 0;
+      const int r = G.acc_buf(jb, jl);
       const uint32_t acc = u_tmem + r * 256;
       pc.lap();
       if (G.mode == kModeSplit) {
@@ -1015,18 +1046,22 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       if (++js == 4) { js = 0; jph ^= 1; }
       if (j < 0) break;
       const Job jb = G.job(j);
-      const int r = G.dbl ? (jl & 1) : 0;
+      const int r = G.acc_buf(jb, jl);
       const uint32_t acc = tmem + lane_off + r * 256;
       const int row0 = jb.m * G.bm;
       pc.lap();
-      named_bar_sync(1, 128);  // previous job's readers of epi_tok / epi_w are done
-      for (int q = et; q < G.bm; q += 128) {
-        const int a = p.sorted_ids[row0 + q];
-        const bool valid = a < p.n_assign;
-        cs.epi_tok[q] = valid ? a / p.top_k : -1;
-        cs.epi_w[q] = valid ? __ldg(p.topk_w + a) : 0.0f;
+      // token rows and top-k weights of the M-tile, for the jobs that
+      // scatter (split mode's phase-1 jobs only write act: no setup)
+      if (jb.kind == 1 || G.mode == kModeFused) {
+        named_bar_sync(1, 128);  // previous job's readers of epi_tok / epi_w are done
+        for (int q = et; q < G.bm; q += 128) {
+          const int a = p.sorted_ids[row0 + q];
+          const bool valid = a < p.n_assign;
+          cs.epi_tok[q] = valid ? a / p.top_k : -1;
+          cs.epi_w[q] = valid ? __ldg(p.topk_w + a) : 0.0f;
+        }
+        named_bar_sync(1, 128);
       }
-      named_bar_sync(1, 128);
       c_meta += pc.lap();
       mbar_wait(smem_u32(&cs.acc_full[r]), acc_cnt[r] & 1);
       START_STAMP(jl == 0 && et == 0, kTsFirstAcc);
@@ -1141,24 +1176,23 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             if (nA == 1) return lane_row < 64 ? jb.s * 64 + lane_row : p.I + jb.s * 64 + (lane_row - 64);
             return (t < nA / 2 ? 0 : p.I) + jb.s * G.n_i + (t % (nA / 2)) * 128 + lane_row;
           };
-          const int w4 = et >> 5, l4 = et & 31;
+          // (same quad register transpose as scatter16: no smem, no barrier)
+          const int b4 = et & 3;
           for (int t = 0; t < nA; ++t) {
-            const int c4 = col_of(t, 4 * l4);
+            const int c4 = col_of(t, et & ~3);
             for (int j0 = 0; j0 < G.bm; j0 += 16) {
               float v[16];
               tmem_ld16(acc + t * bmN + j0, v);
               tmem_ld_wait();
 #pragma unroll
-              for (int q = 0; q < 16; ++q) tbuf[q * 128 + et] = v[q];
-              named_bar_sync(1, 128);
-#pragma unroll
-              for (int rr = 0; rr < 4; ++rr) {
-                const int q = w4 * 4 + rr, jj = j0 + q;
+              for (int cq = 0; cq < 4; ++cq) {
+                float x4[4] = {v[4 * cq], v[4 * cq + 1], v[4 * cq + 2], v[4 * cq + 3]};
+                quad_transpose(x4, b4);
+                const int jj = j0 + 4 * cq + b4;
                 if (jj < G.bm)
                   red_add_v4_f32(p.acc_a + static_cast<size_t>(row0 + jj) * two_i + c4,
-                                 *reinterpret_cast<const float4*>(tbuf + q * 128 + 4 * l4));
+                                 make_float4(x4[0], x4[1], x4[2], x4[3]));
               }
-              named_bar_sync(1, 128);
             }
           }
         }
@@ -1183,8 +1217,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
                 tc_fence_before();
                 mbar_arrive(smem_u32(&cs.chunk_empty[b]));
               }
-              scatter16(v, j0, G.bm, et, tbuf, cs, p.out_acc, p.H, hc * 128);
-              if (two) scatter16(v1, j0 + 16, G.bm, et, tbuf, cs, p.out_acc, p.H, hc * 128);
+              scatter16(v, j0, G.bm, et, cs, p.out_acc, p.H, hc * 128);
+              if (two) scatter16(v1, j0 + 16, G.bm, et, cs, p.out_acc, p.H, hc * 128);
             }
             ++chunk_cnt[b];
             c_scatter += pc.lap();
@@ -1251,8 +1285,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
               tc_fence_before();
               mbar_arrive(smem_u32(&cs.acc_empty[r]));
             }
-            scatter16(v, j0, G.bm, et, tbuf, cs, p.out_acc, p.H, col0);
-            if (two) scatter16(v1, j0 + 16, G.bm, et, tbuf, cs, p.out_acc, p.H, col0);
+            scatter16(v, j0, G.bm, et, cs, p.out_acc, p.H, col0);
+            if (two) scatter16(v1, j0 + 16, G.bm, et, cs, p.out_acc, p.H, col0);
           }
         }
         c_scatter += pc.lap();

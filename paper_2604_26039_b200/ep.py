@@ -135,15 +135,11 @@ class EPComm:
         return self._comm
 
     def close(self):
+        """ncclCommDestroy.  CUDA graphs that captured this communicator's
+        exchanges must be destroyed first (NCCL waits for their operations)."""
         if self._comm:
             _lib.load().ramp_ep_comm_destroy(self._comm)
             self._comm = ctypes.c_void_p()
-
-    def __del__(self):
-        try:
-            self.close()
-        except Exception:  # noqa: BLE001 - interpreter teardown
-            pass
 
 
 def dispatch(x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor, E: int, group=None,

@@ -32,8 +32,11 @@ def mx_quantize(t: torch.Tensor, group: int = GROUP):
     if t.shape[-1] % group:
         raise ValueError(f"last dim {t.shape[-1]} must be a multiple of {group}")
     x = t.float().reshape(*t.shape[:-1], t.shape[-1] // group, group)
-    amax = x.abs().amax(dim=-1, keepdim=True).clamp_min(2.0 ** -120)
-    exp = torch.ceil(torch.log2(amax / E4M3_MAX)).clamp(-127, 127)
+    amax = x.abs().amax(dim=-1, keepdim=True)
+    # exactly ceil(log2(amax / 448)) (the megakernel's rule, csrc/ptx.cuh
+    # mx_exponent): amax = m * 2^e with m in [0.5, 1), 448 = 0.875 * 2^9
+    m, e = torch.frexp(amax)
+    exp = torch.where(amax > 0, e - 9 + (m > 0.875).to(e.dtype), torch.full_like(e, -127)).clamp(-127, 127).float()
     q = (x / torch.exp2(exp)).clamp(-E4M3_MAX, E4M3_MAX).to(torch.float8_e4m3fn)
     sf = (exp.squeeze(-1) + 127).to(torch.uint8)
     return q.reshape(t.shape), sf

@@ -24,9 +24,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--points", default="1:0.2,16:0.5,128:0.5,1024:0.2")
 ap.add_argument("--cfgs", default="8,128,8,0,1,1,1;16,256,6,0,1,1,1;64,256,4,0,1,1,1;128,256,4,0,1,1,1")
 ap.add_argument("--iters", type=int, default=9)
+ap.add_argument("--model", default="OLMoE-1B-7B")
+ap.add_argument("--dtype", default="bf16", choices=("bf16", "fp8"))
 a = ap.parse_args()
-geom = BASELINE_MODELS["OLMoE-1B-7B"]
-pool = enumerate_b200_configs(geom, HardwareModel.b200(), phase3_chunks=True)
+geom = BASELINE_MODELS[a.model]
+fp8 = a.dtype == "fp8"
+pool = enumerate_b200_configs(geom, HardwareModel.b200(), dtype=a.dtype, phase3_chunks=not fp8)
 cols = pool.columns()
 n = len(pool)
 flat = DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
@@ -40,7 +43,12 @@ for w in want:
     if not m:
         raise SystemExit(f"config {w} not in the pool")
     ids.append(m[0])
-timer = MeasuredTimer(geom, flat, iters=a.iters)
+if fp8:
+    from paper_2604_26039_b200.sweep import make_fp8_weights
+
+    timer = MeasuredTimer(geom, flat, iters=a.iters, fp8_weights=make_fp8_weights(geom))
+else:
+    timer = MeasuredTimer(geom, flat, iters=a.iters)
 for spec in a.points.split(","):
     S, beta = int(spec.split(":")[0]), float(spec.split(":")[1])
     hs = derive_seed(42, EVAL_HIST_DOMAIN, S, round(beta * 1000), 0)

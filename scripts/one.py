@@ -27,23 +27,32 @@ ap.add_argument("--H", type=int, default=2048)
 ap.add_argument("--I", type=int, default=1024)
 ap.add_argument("--k", type=int, default=8)
 ap.add_argument("--prof", action="store_true")
+ap.add_argument("--fp8", action="store_true", help="the MXFP8 megakernel (FP8 pool)")
+ap.add_argument("--kps", type=int, default=1)
 a = ap.parse_args()
 E, H, I, k, S = a.E, a.H, a.I, a.k, a.S
 gen = torch.Generator(device="cuda").manual_seed(0)
 w1 = (torch.randn(E, 2 * I, H, device="cuda", generator=gen) / H ** 0.5).to(torch.bfloat16)
 w2 = (torch.randn(E, H, I, device="cuda", generator=gen) / I ** 0.5).to(torch.bfloat16)
-pool = enumerate_b200_configs(MoeGeometry(name="p", E=E, N=2 * I, K=H, top_k=k))
+pool = enumerate_b200_configs(MoeGeometry(name="p", E=E, N=2 * I, K=H, top_k=k), dtype="fp8" if a.fp8 else "bf16")
 cols = pool.columns()
 n = len(pool)
 table = M.DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
                       group_m=cols["group_m"].astype(np.int64), mode=cols.get("mode"), kps=cols.get("kps"), h3=cols.get("h3"), a=np.ones(n), b=np.zeros(n), c=np.zeros(n),
                       d=np.zeros(n), N=2 * I, kappa_ok=False, sm_count=148)
-cfg = [c.id for c in pool if (c.bm, c.ttn, c.stg, int(c.group_m), c.mode, c.split_k) == (a.bm, a.ttn, a.stg, a.gm, a.mode, a.sk)][0]
+cfg = [c.id for c in pool if (c.bm, c.ttn, c.stg, int(c.group_m), c.mode, c.split_k, c.kps) ==
+       (a.bm, a.ttn, a.stg, a.gm, a.mode, a.sk, a.kps)][0]
+if a.fp8:
+    from paper_2604_26039_b200.quant import prepare_mxfp8_weights
+    wq = prepare_mxfp8_weights(w1, w2)
+    run = lambda: M.fused_moe_fp8(x, wq, w, ids, table, cfg, workspace=ws)  # noqa: E731
+else:
+    run = lambda: M.fused_moe(x, w1, w2, w, ids, table, cfg, workspace=ws)  # noqa: E731
 x = torch.randn(S, H, device="cuda", generator=gen).to(torch.bfloat16)
 ids, w = topk(S, k, E, a.skew, gen)
 ws = M.Workspace(S, H, I, E, k)
 for _ in range(a.reps):
-    out = M.fused_moe(x, w1, w2, w, ids, table, cfg, workspace=ws)
+    out = run()
 torch.cuda.synchronize()
 if a.prof:
     from paper_2604_26039_b200 import _lib
@@ -51,7 +60,7 @@ if a.prof:
     _lib.load().ramp_set_profile_buffer(buf.data_ptr())
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    out = M.fused_moe(x, w1, w2, w, ids, table, cfg, workspace=ws)
+    out = run()
     e1.record()
     torch.cuda.synchronize()
     _lib.load().ramp_set_profile_buffer(None)

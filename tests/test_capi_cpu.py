@@ -81,3 +81,25 @@ def test_no_device_reported(lib):
 
     if not torch.cuda.is_available():
         assert lib.ramp_device_ok() == 0
+
+
+def test_ep_argument_validation_without_gpu(lib):
+    """The expert-parallel entry points reject bad geometry before any launch."""
+    buf = (ctypes.c_int32 * 64)()
+    p = ctypes.cast(buf, ctypes.c_void_p)
+    # world must divide E
+    rc = lib.ramp_ep_pack(p, p, p, 4, 128, 10, 2, 4, 4, 0, p, p, p, p, p, p, p, None)
+    assert rc == 1 and b"multiple of world" in lib.ramp_last_error()
+    rc = lib.ramp_ep_pack(p, p, p, 4, 100, 8, 2, 4, 4, 0, p, p, p, p, p, p, p, None)
+    assert rc == 1 and b"H (d_model)" in lib.ramp_last_error()
+    rc = lib.ramp_ep_pack(p, p, p, 4, 128, 8, 2, 4, 4, 7, p, p, p, p, p, p, p, None)
+    assert rc == 1 and b"wire" in lib.ramp_last_error()
+    rc = lib.ramp_ep_pack(p, p, p, 4, 128, 8, 2, 4, 4, 1, p, None, p, p, p, p, p, None)  # MXFP8 needs send_sf
+    assert rc == 1 and b"null send buffer" in lib.ramp_last_error()
+    rc = lib.ramp_ep_reduce(p, p, 4, 128, 0, 4, p, None)
+    assert rc == 1
+    rc = lib.ramp_ep_dispatch(None, p, p, p, 4, 128, 8, 2, 4, 0, p, p, p, p, p, p, p, p, p, p, p, None)
+    assert rc == 1 and b"communicator" in lib.ramp_last_error()
+    comm = ctypes.c_void_p()
+    rc = lib.ramp_ep_comm_init(ctypes.byref(comm), p, 0, 0)
+    assert rc == 1 and b"world" in lib.ramp_last_error()

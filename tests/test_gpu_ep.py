@@ -234,7 +234,10 @@ def test_nccl_exchange_world1(wire):
                     cap_out = ep_moe_layer(xt, it, wt, E, fn, wire=wire, comm=comm)
             g.replay()
             torch.cuda.synchronize()
-            return ident, tdist, nccl, cap_out
+            res = ident, tdist, nccl, cap_out.clone()
+            del g  # a captured graph holds the communicator's operations: free it before the communicator
+            torch.cuda.synchronize()
+            return res
         finally:
             comm.close()
 
@@ -243,7 +246,12 @@ def test_nccl_exchange_world1(wire):
     # differs); one bf16 round of the partial sums separates the exchange
     # paths from the identity one
     assert _rel(tdist, nccl) < 1e-3 and _rel(nccl, graphed) < 1e-3 and _rel(ident, nccl) < 1e-2
-    ref = fused_moe_ref(x, w1, w2, w, ids)
+    if wire == "fp8":  # against the W8A8 MXFP8 semantics on the dequantised weights
+        wq = prepare_mxfp8_weights(torch.from_numpy(w1).cuda(), torch.from_numpy(w2).cuda())
+        d1, d2 = (t.cpu().numpy() for t in wq.dequantize())
+        ref, tol = fused_moe_ref_fp8(x, d1, d2, w, ids), 2e-2
+    else:
+        ref, tol = fused_moe_ref(x, w1, w2, w, ids), 1e-2
     for o in (ident, nccl):
         err = float(np.linalg.norm(o.float().cpu().numpy() - ref) / np.linalg.norm(ref))
-        assert err < (6e-2 if wire == "fp8" else 1e-2), err
+        assert err < tol, err
