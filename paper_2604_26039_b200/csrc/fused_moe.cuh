@@ -27,8 +27,9 @@
 //                   jobs (better SM fill at decode sizes) and one reduction
 //                   per assignment instead of one per stripe.
 //
-// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM
-// allocator, w3 spare, w4-7 epilogue (TMEM lane == weight row).
+// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM
+// allocator, w3 spare, w4-11 epilogue (TMEM lane == weight row; warps w and
+// w + 4 share a lane quarter and split the columns).
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -41,7 +42,14 @@
 
 namespace ramp {
 
-constexpr int kMoeThreads = 256;
+// Two groups of 4 epilogue warps (warps 4-7 and 8-11): each TMEM lane
+// quarter is read by two warps that split an accumulator's columns, so the
+// epilogue (SwiGLU + MXFP8 requantisation, the scatter-reduce) keeps pace
+// with the MMAs at large token blocks.
+constexpr int kEpiHalves = 2;
+constexpr int kEpiThreads = 128 * kEpiHalves;
+constexpr int kMoeThreads = 128 + kEpiThreads;
+constexpr int kGatherWarps = kMoeThreads / 32 - 2;  // phase 0: every warp but the producer and MMA issuer
 constexpr int kCtrlBytes = 4096;                  // barriers + per-job metadata
 constexpr int kStageBytesScatter = 16 * 128 * 4;  // 16 tokens x 128 rows fp32 transpose buffer
 constexpr int kSubTileBytes = 128 * 128;          // 128 rows x 64 bf16 (one SW128 box)
@@ -350,14 +358,14 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&cs.acc_full[b]), 1);
-      mbar_init(smem_u32(&cs.acc_empty[b]), 128);
+      mbar_init(smem_u32(&cs.acc_empty[b]), kEpiThreads);
       mbar_init(smem_u32(&cs.chunk_full[b]), 1);
-      mbar_init(smem_u32(&cs.chunk_empty[b]), 128);
+      mbar_init(smem_u32(&cs.chunk_empty[b]), kEpiThreads);
     }
-    mbar_init(smem_u32(&cs.act_full), 128);
+    mbar_init(smem_u32(&cs.act_full), kEpiThreads);
     for (int q = 0; q < 4; ++q) {
       mbar_init(smem_u32(&cs.job_full[q]), 1);
-      mbar_init(smem_u32(&cs.job_empty[q]), 1 + 128);
+      mbar_init(smem_u32(&cs.job_empty[q]), 1 + kEpiThreads);
     }
     fence_mbar_init();
   }
@@ -451,7 +459,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     // bytes are consecutive in the atom (one 4-byte store).  kUnroll loads
     // per lane are in flight before the first store: the row sources are
     // L2-resident and this pass gates every token tile (grid barrier 0).
-    constexpr int kGatherWarps = 6, kUnroll = 8;
+    constexpr int kUnroll = 8;
     const int row_vec = p.H / 8;  // multiple of 16 (H % 128 == 0)
     const int gw = blockIdx.x * kGatherWarps + (warp - 2), nw = gridDim.x * kGatherWarps;
     const int4* xv = reinterpret_cast<const int4*>(p.x);
@@ -543,7 +551,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     if (warp == 2 && lane == 0) atomicAdd(p.gbar, 1);
   }
   if (!kFp8 && warp >= 2 && !direct_x) {
-    constexpr int kGatherWarps = 6, kUnroll = 8;
+    constexpr int kUnroll = 8;
     const int row_vec = p.H / 8;  // 16-byte vectors per row
     const int gw = blockIdx.x * kGatherWarps + (warp - 2), nw = gridDim.x * kGatherWarps;
     const int4* xv = reinterpret_cast<const int4*>(p.x);
@@ -1032,8 +1040,13 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     }
   } else if (warp >= 4) {
     // ============================ epilogue ===============================
-    const int et = threadIdx.x - 128;  // TMEM lane == weight row of the 128-row MMA tile
+    const int et2 = threadIdx.x - 128;  // 0 .. kEpiThreads-1
+    const int et = et2 & 127;           // TMEM lane == weight row of the 128-row MMA tile
+    const int half = et2 >> 7;          // which of the two column halves this warp serves
     const uint32_t lane_off = static_cast<uint32_t>(et & ~31) << 16;
+    // the bar.sync id / smem slice private to this half (nA == 1 SwiGLU exchange)
+    const uint32_t hbar = 4 + half;
+    float* const hbuf = tbuf + half * 1024;
     uint32_t jl = 0, acc_cnt[2] = {0, 0}, chunk_cnt[2] = {0, 0};
     unsigned long long c_meta = 0, c_wacc = 0, c_swiglu = 0, c_wchunk = 0, c_scatter = 0;
     ProfClock pc;
@@ -1053,18 +1066,18 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       // token rows and top-k weights of the M-tile, for the jobs that
       // scatter (split mode's phase-1 jobs only write act: no setup)
       if (jb.kind == 1 || G.mode == kModeFused) {
-        named_bar_sync(1, 128);  // previous job's readers of epi_tok / epi_w are done
-        for (int q = et; q < G.bm; q += 128) {
+        named_bar_sync(1, kEpiThreads);  // previous job's readers of epi_tok / epi_w are done
+        for (int q = et2; q < G.bm; q += kEpiThreads) {
           const int a = p.sorted_ids[row0 + q];
           const bool valid = a < p.n_assign;
           cs.epi_tok[q] = valid ? a / p.top_k : -1;
           cs.epi_w[q] = valid ? __ldg(p.topk_w + a) : 0.0f;
         }
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiThreads);
       }
       c_meta += pc.lap();
       mbar_wait(smem_u32(&cs.acc_full[r]), acc_cnt[r] & 1);
-      START_STAMP(jl == 0 && et == 0, kTsFirstAcc);
+      START_STAMP(jl == 0 && et2 == 0, kTsFirstAcc);
       ++acc_cnt[r];
       c_wacc += pc.lap();
       tc_fence_after();
@@ -1081,7 +1094,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             // stores 16 contiguous bytes of one token row)
             const int l = et & 31;
             const int col0 = jb.s * G.n_i + f - l;  // first feature of the warp's group
-            uint8_t* wbuf = reinterpret_cast<uint8_t*>(tbuf) + (et >> 5) * 512;
+            uint8_t* wbuf = reinterpret_cast<uint8_t*>(tbuf) + (et2 >> 5) * 512;
             uint32_t my_sf = 0;
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
@@ -1131,28 +1144,31 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         if (G.sk == 1) {
           if (nA == 1) {
             // ttn = 128: lanes 0-63 hold gate rows, lanes 64-127 the matching up rows
-            for (int j0 = 0; j0 < bmN; j0 += 16) {
+            // (the halves take alternate 16-column groups)
+            for (int j0 = 16 * half; j0 < bmN; j0 += 32) {
               float g[16], u[16];
               tmem_ld16(acc + j0, g);
               tmem_ld_wait();
               if (et >= 64) {
-  #pragma unroll
-                for (int q = 0; q < 16; ++q) tbuf[q * 64 + (et - 64)] = g[q];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) hbuf[q * 64 + (et - 64)] = g[q];
               }
-              named_bar_sync(1, 128);
+              named_bar_sync(hbar, 128);
               if (et < 64) {
-  #pragma unroll
-                for (int q = 0; q < 16; ++q) u[q] = tbuf[q * 64 + et];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) u[q] = hbuf[q * 64 + et];
                 store_act(et, j0, g, u);
               }
-              named_bar_sync(1, 128);
+              named_bar_sync(hbar, 128);
             }
           } else {
-            // Thread et owns features f = th*128 + et of the stripe.
-            for (int th = 0; th < nA / 2; ++th) {
+            // Thread et owns features f = th*128 + et of the stripe; the
+            // (th, 32-column) items alternate between the two halves.
+            const int nj = (bmN + 31) / 32;
+            for (int it = half; it < (nA / 2) * nj; it += kEpiHalves) {
+              const int th = it / nj, j0 = (it % nj) * 32;
               const int f = th * 128 + et;
-              // two 16-column chunks per TMEM round trip
-              for (int j0 = 0; j0 < bmN; j0 += 32) {
+              {  // two 16-column chunks per TMEM round trip
                 float g[16], u[16], g1[16], u1[16];
                 const bool two = j0 + 16 < bmN;
                 tmem_ld16(acc + th * bmN + j0, g);
@@ -1178,9 +1194,11 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           };
           // (same quad register transpose as scatter16: no smem, no barrier)
           const int b4 = et & 3;
-          for (int t = 0; t < nA; ++t) {
+          const int nj = (G.bm + 15) / 16;
+          for (int it = half; it < nA * nj; it += kEpiHalves) {
+            const int t = it / nj, j0 = (it % nj) * 16;
             const int c4 = col_of(t, et & ~3);
-            for (int j0 = 0; j0 < G.bm; j0 += 16) {
+            {
               float v[16];
               tmem_ld16(acc + t * bmN + j0, v);
               tmem_ld_wait();
@@ -1207,18 +1225,25 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             mbar_wait(smem_u32(&cs.chunk_full[b]), chunk_cnt[b] & 1);
             c_wchunk += pc.lap();
             tc_fence_after();
-            for (int j0 = 0; j0 < G.bm; j0 += 32) {  // two 16-column chunks per TMEM round trip
+            bool freed = false;
+            // two 16-column chunks per TMEM round trip; the halves alternate
+            for (int j0 = 32 * half; j0 < G.bm; j0 += 32 * kEpiHalves) {
               float v[16], v1[16];
               const bool two = j0 + 16 < G.bm;
               tmem_ld16(tmem + lane_off + b * bmN + j0, v);
               if (two) tmem_ld16(tmem + lane_off + b * bmN + j0 + 16, v1);
               tmem_ld_wait();
-              if (j0 + 32 >= G.bm) {
+              if (j0 + 32 * kEpiHalves >= G.bm) {  // this half's last TMEM read of the chunk
                 tc_fence_before();
                 mbar_arrive(smem_u32(&cs.chunk_empty[b]));
+                freed = true;
               }
               scatter16(v, j0, G.bm, et, cs, p.out_acc, p.H, hc * 128);
               if (two) scatter16(v1, j0 + 16, G.bm, et, cs, p.out_acc, p.H, hc * 128);
+            }
+            if (!freed) {  // no columns for this half
+              tc_fence_before();
+              mbar_arrive(smem_u32(&cs.chunk_empty[b]));
             }
             ++chunk_cnt[b];
             c_scatter += pc.lap();
@@ -1229,20 +1254,20 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           if (G.sk > 1) {
             // count this slice in; the last of the sk slices finishes the stripe
             __threadfence();
-            named_bar_sync(1, 128);
-            if (et == 0) {
+            named_bar_sync(1, kEpiThreads);
+            if (et2 == 0) {
               int* cnt = p.split_cnt + jb.m * G.stripes + jb.s;
               const int old = atomicAdd(cnt, 1);
               cs.fin = old == G.sk - 1;
               if (cs.fin) *cnt = 0;  // every slice has arrived: reset for the next call
               __threadfence();
             }
-            named_bar_sync(1, 128);
+            named_bar_sync(1, kEpiThreads);
             publish = cs.fin != 0;
             if (publish) {
               const int two_i = 2 * p.I;
               for (int f = et; f < G.n_i; f += 128) {
-                for (int j0 = 0; j0 < G.bm; j0 += 16) {
+                for (int j0 = 16 * half; j0 < G.bm; j0 += 16 * kEpiHalves) {
                   float g[16], u[16];
 #pragma unroll
                   for (int q = 0; q < 16; ++q) {
@@ -1262,8 +1287,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           }
           if (publish) {
             // publish phase-1 completion of this (m, s) stripe for the phase-3 jobs
-            named_bar_sync(1, 128);
-            if (et == 0) {
+            named_bar_sync(1, kEpiThreads);
+            if (et2 == 0) {
               __threadfence();
               atomicAdd(p.done + jb.m, 1);
             }
@@ -1273,26 +1298,33 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       } else {
         // ---- split phase 3 epilogue: n3 128-row chunks, full I reduced in TMEM
         // (two 16-column chunks per TMEM round trip)
-        for (int t = 0; t < G.n3; ++t) {
+        // (the halves take alternate (chunk, 32-column) items)
+        const int nj = (G.bm + 31) / 32, n_it = G.n3 * nj;
+        bool freed = false;
+        for (int it = half; it < n_it; it += kEpiHalves) {
+          const int t = it / nj, j0 = (it % nj) * 32;
           const int col0 = (jb.hc * G.n3 + t) * 128;
-          for (int j0 = 0; j0 < G.bm; j0 += 32) {
-            float v[16], v1[16];
-            const bool two = j0 + 16 < G.bm;
-            tmem_ld16(acc + t * G.bmN + j0, v);
-            if (two) tmem_ld16(acc + t * G.bmN + j0 + 16, v1);
-            tmem_ld_wait();
-            if (t == G.n3 - 1 && j0 + 32 >= G.bm) {
-              tc_fence_before();
-              mbar_arrive(smem_u32(&cs.acc_empty[r]));
-            }
-            scatter16(v, j0, G.bm, et, cs, p.out_acc, p.H, col0);
-            if (two) scatter16(v1, j0 + 16, G.bm, et, cs, p.out_acc, p.H, col0);
+          float v[16], v1[16];
+          const bool two = j0 + 16 < G.bm;
+          tmem_ld16(acc + t * G.bmN + j0, v);
+          if (two) tmem_ld16(acc + t * G.bmN + j0 + 16, v1);
+          tmem_ld_wait();
+          if (it + kEpiHalves >= n_it) {  // this half's last TMEM read of the job
+            tc_fence_before();
+            mbar_arrive(smem_u32(&cs.acc_empty[r]));
+            freed = true;
           }
+          scatter16(v, j0, G.bm, et, cs, p.out_acc, p.H, col0);
+          if (two) scatter16(v1, j0 + 16, G.bm, et, cs, p.out_acc, p.H, col0);
+        }
+        if (!freed) {
+          tc_fence_before();
+          mbar_arrive(smem_u32(&cs.acc_empty[r]));
         }
         c_scatter += pc.lap();
       }
     }
-    if (p.prof && et == 0) {
+    if (p.prof && et2 == 0) {
       unsigned long long* pr = p.prof + blockIdx.x * kNumProf;
       pr[kTsEpilogueDone] = globaltimer();
       pr[kEpiMeta] = c_meta;
