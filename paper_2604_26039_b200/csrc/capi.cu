@@ -28,7 +28,7 @@ int cuda_fail(cudaError_t err, const char* where) {
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct WorkspaceLayout {
-  size_t ctrl, hist, sorted, tiles, done, acc, xs, act, acc_a, split_cnt, xq, xsf, actq, actsf, total;
+  size_t ctrl, hist, sorted, tiles, done, acc, xs, act, acc_a, split_cnt, xq, xsf, actq, actsf, xqt, xsft, total;
   int64_t capacity, rows;
 };
 
@@ -64,6 +64,8 @@ WorkspaceLayout layout_for(int32_t S, int32_t H, int32_t I, int32_t E, int32_t t
   w.xsf = take((size_t)mt_max * (H / 128 + 1) * 512);
   w.actq = take((size_t)w.rows * I);
   w.actsf = take((size_t)mt_max * (I / 128 + 1) * 512);
+  w.xqt = take((size_t)S * H);        // FP8: tokens quantised once, [S, H] e4m3
+  w.xsft = take((size_t)S * (H / 32)); //      and their scales [S, H/32]
   w.total = off;
   return w;
 }
@@ -266,12 +268,25 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   ra.top_k = top_k;
   ra.pdl_early = ramp::pdl_mode() == 1;
   ra.pdl_prev = ramp::pdl_prev_enabled() ? 1 : 0;
+  // FP8 from bf16 tokens, large batches: quantise each token once (all SMs
+  // but a few) ahead of the route kernel (its programmatic dependent) instead
+  // of re-quantising every gathered row in the megakernel's phase 0 (top_k x
+  // the work).  Small batches keep the single in-megakernel pass: the extra
+  // launch costs more than it saves (measured: +3-5 % at S*k <= 1024,
+  // -3 / -7 % at S*k = 4096 / 16384 on Qwen3-30B-A3B).
+  constexpr int64_t kQuantTokensMinAssign = 4096;
+  const bool quant_tokens = fp8 && !xsf_in && (int64_t)S * top_k >= kQuantTokensMinAssign;
+  if (quant_tokens && (phases & 2)) ra.pdl_prev = 2;
   ra.logits = logits;
   ra.logits_bf16 = logits_bf16;
   ra.renorm = renorm;
   ra.w_out = w_out;
   const int zero_blocks = 0;
   cudaError_t err = cudaSuccess;
+  if (quant_tokens && (phases & 2)) {
+    err = ramp::launch_mx_quant_tokens(x, S, H, ws + L.xqt, ws + L.xsft, st);
+    if (err != cudaSuccess) return cuda_fail(err, "token quantisation kernel");
+  }
   if (phases & 1) {
     err = ramp::launch_route(ra, zero_blocks, st);
     if (err != cudaSuccess) return cuda_fail(err, "route kernel");
@@ -302,8 +317,8 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   ml.x_sf = ws + L.xsf;
   ml.act_q = ws + L.actq;
   ml.act_sf = ws + L.actsf;
-  ml.xq_in = xsf_in ? static_cast<const uint8_t*>(x) : nullptr;  // x holds e4m3 rows then
-  ml.xsf_in = xsf_in;
+  ml.xq_in = xsf_in ? static_cast<const uint8_t*>(x) : (quant_tokens ? ws + L.xqt : nullptr);  // e4m3 rows
+  ml.xsf_in = xsf_in ? xsf_in : (quant_tokens ? ws + L.xsft : nullptr);
   ml.table = *table;
   ml.S = S;
   ml.H = H;

@@ -452,96 +452,117 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   // calls need no grid barrier before the first MMA.
   const bool direct_x = !kFp8 && bmN == 16;
   if (kFp8 && warp >= 2) {
-    // FP8: gather + quantise every row to MXFP8 (per-32 power-of-two scales)
-    // into x_q and the per-M-tile scale atoms x_sf.
-    // A lane quantises 8 features (one 16-byte load, one 8-byte store); 4
-    // lanes form a 32-group and 16 lanes a 128-wide k-block, whose 4 scale
-    // bytes are consecutive in the atom (one 4-byte store).  kUnroll loads
-    // per lane are in flight before the first store: the row sources are
-    // L2-resident and this pass gates every token tile (grid barrier 0).
-    constexpr int kUnroll = 8;
-    const int row_vec = p.H / 8;  // multiple of 16 (H % 128 == 0)
-    const int gw = blockIdx.x * kGatherWarps + (warp - 2), nw = gridDim.x * kGatherWarps;
-    const int4* xv = reinterpret_cast<const int4*>(p.x);
-    for (int r0 = gw; r0 < n_post_pad; r0 += 32 * nw) {
-      const int rl = r0 + lane * nw;
-      const int asg_l = rl < n_post_pad ? __ldcg(p.sorted_ids + rl) : p.n_assign;
-      const int nrows = min(32, (n_post_pad - r0 + nw - 1) / nw);
-      for (int q = 0; q < nrows; ++q) {
-        const int asg = __shfl_sync(0xffffffffu, asg_l, q);
-        const int r = r0 + q * nw;
-        const int m = r / G.bm, jr = r - m * G.bm;
-        const int4* src = xv + static_cast<int64_t>(asg < p.n_assign ? asg / p.top_k : 0) * row_vec;
-        uint8_t* dst = p.x_q + static_cast<int64_t>(r) * p.H;
-        uint8_t* sf_row = p.x_sf + static_cast<int64_t>(m) * G.kbH * 512 + (jr & 31) * 16 + (jr >> 5) * 4;
-        if (p.xq_in != nullptr) {
-          // tokens that arrived already in MXFP8 (the EP wire): copy the
-          // e4m3 bytes (16 per lane-chunk) and move the row-major scales
-          // (4 bytes per k-block) into this M-tile's atoms
-          const int row16 = p.H / 16;
-          const int64_t src_row = asg < p.n_assign ? asg / p.top_k : -1;
-          const int4* qsrc = reinterpret_cast<const int4*>(p.xq_in) + (src_row < 0 ? 0 : src_row) * row16;
-          int4* qdst = reinterpret_cast<int4*>(dst);
-          for (int c0 = lane; c0 < row16; c0 += 32 * kUnroll) {
+    // FP8 phase 0, two forms (the host picks by batch size):
+    // * the token rows arrive already in MXFP8 (xq_in / xsf_in: the token
+    //   quantisation kernel, run once per token ahead of the route kernel for
+    //   large batches, or an MXFP8 expert-parallel wire): only move them into
+    //   expert-sorted order (x_q, 16-byte chunks) and their row-major scales
+    //   into the M-tiles' atoms (x_sf, one k-block per 4-byte word); a warp's
+    //   32 rows are flattened into one chunk stream so every lane keeps
+    //   kUnroll loads in flight whatever the row length;
+    // * small batches: quantise every gathered row here (no extra launch).
+    if (p.xq_in != nullptr) {
+      constexpr int kUnroll = 8;
+      const int row16 = p.H / 16, row_sf = p.H / 32;
+      const int gw = blockIdx.x * kGatherWarps + (warp - 2), nw = gridDim.x * kGatherWarps;
+      const int4* qsrc = reinterpret_cast<const int4*>(p.xq_in);
+      for (int r0 = gw; r0 < n_post_pad; r0 += 32 * nw) {
+        const int rl = r0 + lane * nw;
+        const int asg_l = rl < n_post_pad ? __ldcg(p.sorted_ids + rl) : p.n_assign;
+        const int src_l = asg_l < p.n_assign ? asg_l / p.top_k : -1;  // token row, -1 = padding
+        const int nrows = min(32, (n_post_pad - r0 + nw - 1) / nw);
+        const int nch = nrows * row16;
+        for (int b0 = 0; b0 < nch; b0 += 32 * kUnroll) {  // warp-uniform trip count (shuffles inside)
+          int4 v[kUnroll];
+          int dst_row[kUnroll], cc[kUnroll];
+  #pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int c = b0 + lane + 32 * u;
+            const int q = min(c / row16, nrows - 1);
+            cc[u] = c - q * row16;
+            const int src = __shfl_sync(0xffffffffu, src_l, q);
+            dst_row[u] = c < nch ? r0 + q * nw : -1;
+            v[u] = make_int4(0, 0, 0, 0);
+            if (c < nch && src >= 0) v[u] = __ldg(qsrc + static_cast<int64_t>(src) * row16 + cc[u]);
+          }
+  #pragma unroll
+          for (int u = 0; u < kUnroll; ++u)
+            if (dst_row[u] >= 0)
+              reinterpret_cast<int4*>(p.x_q + static_cast<int64_t>(dst_row[u]) * p.H)[cc[u]] = v[u];
+        }
+        const int nsw = nrows * G.kbH;
+        for (int b0 = 0; b0 < nsw; b0 += 32) {
+          const int c0 = b0 + lane;
+          const int q = min(c0 / G.kbH, nrows - 1), kb = c0 - q * G.kbH;
+          const int src = __shfl_sync(0xffffffffu, src_l, q);
+          if (c0 < nsw) {
+            const uint32_t sc =
+                src < 0 ? 0u : __ldg(reinterpret_cast<const uint32_t*>(p.xsf_in + static_cast<int64_t>(src) * row_sf) + kb);
+            const int r = r0 + q * nw, m = r / G.bm, jr = r - m * G.bm;
+            *reinterpret_cast<uint32_t*>(p.x_sf + (static_cast<int64_t>(m) * G.kbH + kb) * 512 + (jr & 31) * 16 +
+                                         (jr >> 5) * 4) = sc;
+          }
+        }
+      }
+    } else {
+      constexpr int kUnroll = 8;
+      const int row_vec = p.H / 8;  // multiple of 16 (H % 128 == 0)
+      const int gw = blockIdx.x * kGatherWarps + (warp - 2), nw = gridDim.x * kGatherWarps;
+      const int4* xv = reinterpret_cast<const int4*>(p.x);
+      for (int r0 = gw; r0 < n_post_pad; r0 += 32 * nw) {
+        const int rl = r0 + lane * nw;
+        const int asg_l = rl < n_post_pad ? __ldcg(p.sorted_ids + rl) : p.n_assign;
+        const int nrows = min(32, (n_post_pad - r0 + nw - 1) / nw);
+        for (int q = 0; q < nrows; ++q) {
+          const int asg = __shfl_sync(0xffffffffu, asg_l, q);
+          const int r = r0 + q * nw;
+          const int m = r / G.bm, jr = r - m * G.bm;
+          const int4* src = xv + static_cast<int64_t>(asg < p.n_assign ? asg / p.top_k : 0) * row_vec;
+          uint8_t* dst = p.x_q + static_cast<int64_t>(r) * p.H;
+          uint8_t* sf_row = p.x_sf + static_cast<int64_t>(m) * G.kbH * 512 + (jr & 31) * 16 + (jr >> 5) * 4;
+          for (int c0 = lane; c0 < row_vec; c0 += 32 * kUnroll) {
             int4 v[kUnroll];
-#pragma unroll
+  #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
               v[u] = make_int4(0, 0, 0, 0);
-              if (c0 + 32 * u < row16 && src_row >= 0) v[u] = __ldg(qsrc + c0 + 32 * u);
+              if (c0 + 32 * u < row_vec && asg < p.n_assign) v[u] = __ldg(src + c0 + 32 * u);
             }
-#pragma unroll
-            for (int u = 0; u < kUnroll; ++u)
-              if (c0 + 32 * u < row16) qdst[c0 + 32 * u] = v[u];
-          }
-          for (int kb = lane; kb < G.kbH; kb += 32) {
-            const uint32_t sc =
-                src_row < 0 ? 0u : __ldg(reinterpret_cast<const uint32_t*>(p.xsf_in + src_row * (p.H / 32)) + kb);
-            *reinterpret_cast<uint32_t*>(sf_row + static_cast<int64_t>(kb) * 512) = sc;
-          }
-          continue;
-        }
-        for (int c0 = lane; c0 < row_vec; c0 += 32 * kUnroll) {
-          int4 v[kUnroll];
-#pragma unroll
-          for (int u = 0; u < kUnroll; ++u) {
-            v[u] = make_int4(0, 0, 0, 0);
-            if (c0 + 32 * u < row_vec && asg < p.n_assign) v[u] = __ldg(src + c0 + 32 * u);
-          }
-#pragma unroll
-          for (int u = 0; u < kUnroll; ++u) {
-            const int c = c0 + 32 * u;
-            if (c - lane >= row_vec) break;  // warp-uniform
-            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
-            float f[8];
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              const float2 t2 = __bfloat1622float2(h2[t]);
-              f[2 * t] = t2.x;
-              f[2 * t + 1] = t2.y;
+  #pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+              const int c = c0 + 32 * u;
+              if (c - lane >= row_vec) break;  // warp-uniform
+              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+              float f[8];
+  #pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const float2 t2 = __bfloat1622float2(h2[t]);
+                f[2 * t] = t2.x;
+                f[2 * t + 1] = t2.y;
+              }
+              uint32_t am = 0;
+  #pragma unroll
+              for (int t = 0; t < 8; ++t) am = max(am, __float_as_uint(fabsf(f[t])));
+              am = max(am, __shfl_xor_sync(0xffffffffu, am, 1));
+              am = max(am, __shfl_xor_sync(0xffffffffu, am, 2));
+              const int ex = mx_exponent(am);
+              const float inv = mx_inv_scale(ex);
+              uint2 qv;
+              qv.x = static_cast<uint32_t>(e4m3x2_from_float(f[0] * inv, f[1] * inv)) |
+                     (static_cast<uint32_t>(e4m3x2_from_float(f[2] * inv, f[3] * inv)) << 16);
+              qv.y = static_cast<uint32_t>(e4m3x2_from_float(f[4] * inv, f[5] * inv)) |
+                     (static_cast<uint32_t>(e4m3x2_from_float(f[6] * inv, f[7] * inv)) << 16);
+              const bool in = c < row_vec;  // row_vec may be an odd multiple of 16
+              if (in) *reinterpret_cast<uint2*>(dst + c * 8) = qv;
+              // the 4 group exponents of this lane's k-block (lanes 16h .. 16h+15)
+              const int b16 = lane & 16;
+              const uint32_t e0 = __shfl_sync(0xffffffffu, ex + 127, b16);
+              const uint32_t e1 = __shfl_sync(0xffffffffu, ex + 127, b16 + 4);
+              const uint32_t e2 = __shfl_sync(0xffffffffu, ex + 127, b16 + 8);
+              const uint32_t e3 = __shfl_sync(0xffffffffu, ex + 127, b16 + 12);
+              if (in && (lane & 15) == 0)
+                *reinterpret_cast<uint32_t*>(sf_row + static_cast<int64_t>(c >> 4) * 512) =
+                    e0 | (e1 << 8) | (e2 << 16) | (e3 << 24);
             }
-            uint32_t am = 0;
-#pragma unroll
-            for (int t = 0; t < 8; ++t) am = max(am, __float_as_uint(fabsf(f[t])));
-            am = max(am, __shfl_xor_sync(0xffffffffu, am, 1));
-            am = max(am, __shfl_xor_sync(0xffffffffu, am, 2));
-            const int ex = mx_exponent(am);
-            const float inv = mx_inv_scale(ex);
-            uint2 qv;
-            qv.x = static_cast<uint32_t>(e4m3x2_from_float(f[0] * inv, f[1] * inv)) |
-                   (static_cast<uint32_t>(e4m3x2_from_float(f[2] * inv, f[3] * inv)) << 16);
-            qv.y = static_cast<uint32_t>(e4m3x2_from_float(f[4] * inv, f[5] * inv)) |
-                   (static_cast<uint32_t>(e4m3x2_from_float(f[6] * inv, f[7] * inv)) << 16);
-            const bool in = c < row_vec;  // row_vec may be an odd multiple of 16
-            if (in) *reinterpret_cast<uint2*>(dst + c * 8) = qv;
-            // the 4 group exponents of this lane's k-block (lanes 16h .. 16h+15)
-            const int b16 = lane & 16;
-            const uint32_t e0 = __shfl_sync(0xffffffffu, ex + 127, b16);
-            const uint32_t e1 = __shfl_sync(0xffffffffu, ex + 127, b16 + 4);
-            const uint32_t e2 = __shfl_sync(0xffffffffu, ex + 127, b16 + 8);
-            const uint32_t e3 = __shfl_sync(0xffffffffu, ex + 127, b16 + 12);
-            if (in && (lane & 15) == 0)
-              *reinterpret_cast<uint32_t*>(sf_row + static_cast<int64_t>(c >> 4) * 512) =
-                  e0 | (e1 << 8) | (e2 << 16) | (e3 << 24);
           }
         }
       }

@@ -35,7 +35,8 @@ struct RouteArgs {
   const void* x;         // [S, H] bf16 tokens
   void* x_sorted;        // [rows, H] bf16, gathered by the helper blocks (null: skip)
   int32_t S, H, top_k;
-  int32_t pdl_prev;      // launched as a PDL secondary of the previous kernel (waits before reading)
+  int32_t pdl_prev;      // launched as a PDL secondary of the previous kernel: 1 = waits before reading
+                         // its inputs, 2 = reads nothing of it (waits only before completing)
   int32_t pdl_early;     // trigger the dependent launch at entry (1) or after the alignment (0)
   // router fusion: when logits != null the route kernel first computes the
   // softmax top-k into topk_ids (== ids_out) and w_out
@@ -117,5 +118,8 @@ int nccl_comm_destroy(void* comm);
 int nccl_all_to_all(void* comm, int world, const void* const* send, void* const* recv, const size_t* block_bytes,
                     int n_bufs, cudaStream_t stream, const char** why);
 int64_t config_smem_bytes(int bm, int ttn, int stg, int mode, bool fp8, int kps = 1);
+// MXFP8 quantisation of token rows [S, H] bf16 -> e4m3 [S, H] + UE8M0 [S, H/32] (row-major)
+cudaError_t launch_mx_quant_tokens(const void* x, int64_t S, int32_t H, uint8_t* q, uint8_t* sf,
+                                   cudaStream_t stream);
 
 }  // namespace ramp

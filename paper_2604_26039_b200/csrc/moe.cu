@@ -77,6 +77,59 @@ static bool make_map_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64
   return make_map(map, ptr, 2, dims, strides, box, bytes);
 }
 
+// MXFP8 quantisation of the token rows, once per token (the FP8 layer's
+// phase 0 then only moves bytes into expert-sorted order): a lane turns 8
+// bf16 into 8 e4m3 (one 16-byte load, one 8-byte store), 4 lanes share a
+// 32-group's UE8M0 scale (the exact rule of mx_exponent, csrc/ptx.cuh).
+// Launched ahead of the route kernel, which runs as its programmatic
+// dependent: the two overlap (the route kernel does not read these rows and
+// waits for this grid only before it completes).
+__global__ void __launch_bounds__(256) mx_quant_tokens_kernel(const __nv_bfloat16* __restrict__ x, int64_t n8,
+                                                              uint8_t* __restrict__ q, uint8_t* __restrict__ sf) {
+  pdl_launch_dependents();
+  const int4* xv = reinterpret_cast<const int4*>(x);
+  for (int64_t c0 = blockIdx.x * (int64_t)blockDim.x; c0 < n8; c0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = c0 + threadIdx.x;  // 8-element chunk (groups never straddle rows: H % 32 == 0)
+    int4 v = make_int4(0, 0, 0, 0);
+    if (c < n8) v = __ldg(xv + c);
+    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&v);
+    float f[8];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float2 t2 = __bfloat1622float2(h2[t]);
+      f[2 * t] = t2.x;
+      f[2 * t + 1] = t2.y;
+    }
+    uint32_t am = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) am = max(am, __float_as_uint(fabsf(f[t])));
+    am = max(am, __shfl_xor_sync(0xffffffffu, am, 1));
+    am = max(am, __shfl_xor_sync(0xffffffffu, am, 2));
+    const int ex = mx_exponent(am);
+    const float inv = mx_inv_scale(ex);
+    uint2 qv;
+    qv.x = static_cast<uint32_t>(e4m3x2_from_float(f[0] * inv, f[1] * inv)) |
+           (static_cast<uint32_t>(e4m3x2_from_float(f[2] * inv, f[3] * inv)) << 16);
+    qv.y = static_cast<uint32_t>(e4m3x2_from_float(f[4] * inv, f[5] * inv)) |
+           (static_cast<uint32_t>(e4m3x2_from_float(f[6] * inv, f[7] * inv)) << 16);
+    if (c < n8) {
+      reinterpret_cast<uint2*>(q)[c] = qv;
+      if ((threadIdx.x & 3) == 0) sf[c >> 2] = static_cast<uint8_t>(ex + 127);
+    }
+  }
+}
+
+cudaError_t launch_mx_quant_tokens(const void* x, int64_t S, int32_t H, uint8_t* q, uint8_t* sf,
+                                   cudaStream_t stream) {
+  const int64_t n8 = S * H / 8;
+  if (n8 == 0) return cudaSuccess;
+  // leave SMs free so the route block (its programmatic dependent) becomes resident at once
+  const int64_t want = (n8 + 255) / 256;
+  const int blocks = static_cast<int>(want < 96 ? want : 96);
+  mx_quant_tokens_kernel<<<blocks, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(x), n8, q, sf);
+  return cudaGetLastError();
+}
+
 int64_t config_smem_bytes(int bm, int ttn, int stg, int mode, bool fp8, int kps) {
   if (bm < 1 || bm > kMaxBm || (ttn != 128 && ttn != 256 && ttn != 512) || stg < 1 || stg > kMaxStages)
     return 0;

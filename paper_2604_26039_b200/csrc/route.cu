@@ -46,7 +46,7 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
   // Launched as a programmatic dependent of the previous kernel in the stream
   // (typically the previous layer's megakernel): everything above overlaps its
   // tail; nothing above touches the inputs or the workspace.
-  if (a.pdl_prev) pdl_wait();
+  if (a.pdl_prev == 1) pdl_wait();
   if (threadIdx.x == 0) st.bad = 0;
   if constexpr (kGating) {
     // router fusion: the top-k is computed here (host checked n <= kIdCache)
@@ -165,6 +165,9 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
   }
   RCLK(21);
   stamp(4);
+  // the previous grid (the FP8 token quantisation) must be complete before
+  // this one is, so the megakernel's wait on this grid covers it too
+  if (a.pdl_prev == 2) pdl_wait();
   if (!a.pdl_early) pdl_launch_dependents();
 }
 
