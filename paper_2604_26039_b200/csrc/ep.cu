@@ -124,16 +124,21 @@ __global__ void __launch_bounds__(kEpThreads) ep_pack_kernel(EpPackArgs a) {
     }
   }
   __syncthreads();
-  // (4) token rows: one warp per token, the row read once (kUnroll 16-byte
-  // loads in flight per lane) and written to every destination rank
+  // (4) token rows: (token, row segment) items over the block's warps -- a
+  // segment is 32 x kUnroll 16-byte chunks, read once (kUnroll loads in
+  // flight per lane) and written to every destination rank; a block holds
+  // few tokens when S is small, so rows are split across warps
   constexpr int kUnroll = 4;
   const int row_vec = a.H / 8;  // 16-byte chunks of 8 bf16
+  const int n_seg = (row_vec + 32 * kUnroll - 1) / (32 * kUnroll);
   const int4* xv = reinterpret_cast<const int4*>(a.x);
-  for (int q = warp; q < t1 - t0; q += kEpThreads / 32) {
+  for (int item = warp; item < (t1 - t0) * n_seg; item += kEpThreads / 32) {
+    const int q = item / n_seg, seg = item - q * n_seg;
     const int tt = t0 + q;
     const uint32_t mq = s_mask[q];
     if (!mq) continue;
-    for (int c0 = lane; c0 < row_vec; c0 += 32 * kUnroll) {
+    {
+      const int c0 = seg * 32 * kUnroll + lane;
       int4 v[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u)
