@@ -451,12 +451,20 @@ def ep_leg(dev, world, rank, iters=10, warmup=3):
     if not dist.is_initialized():
         return {"skipped": "needs a torch.distributed process group"}
     geom = BASELINE_MODELS[EP_MODEL]
-    path = ROOT / "paper_2604_26039_b200" / "data" / f"coeffs_{EP_LOCAL}_b200_fp8.json"
-    if not path.exists():
-        return {"skipped": f"{path.name} missing (scripts/profile_b200.py --model {EP_LOCAL} --dtype fp8)"}
     if geom.E % world:
         return {"skipped": f"E={geom.E} does not split over {world} ranks"}
     per = geom.E // world
+    # the table fitted for this rank's local expert count when one ships
+    # (world 1: all 256 experts, "DeepSeek-V3"; world 8: 32, "DeepSeek-V3-EP8"),
+    # else the EP8 one (the kernel geometry N, K is the same; the B4 traffic
+    # terms were fitted on 32-expert histograms)
+    local_name = {1: EP_MODEL, 8: EP_LOCAL}.get(world, EP_LOCAL)
+    path = ROOT / "paper_2604_26039_b200" / "data" / f"coeffs_{local_name}_b200_fp8.json"
+    if not path.exists():
+        path = ROOT / "paper_2604_26039_b200" / "data" / f"coeffs_{EP_LOCAL}_b200_fp8.json"
+    if not path.exists():
+        return {"skipped": f"{path.name} missing (scripts/profile_b200.py --model {EP_LOCAL} --dtype fp8)"}
+    table_matches = path.name == f"coeffs_{local_name}_b200_fp8.json" and world in (1, 8)
     lgeom = MoeGeometry(name=f"{EP_MODEL}-EP{world}", E=per, N=geom.N, K=geom.K, top_k=geom.top_k)
     pool = enumerate_b200_configs(lgeom, HardwareModel.b200(), dtype="fp8")
     store = read_coeff_store(path)
@@ -525,8 +533,8 @@ def ep_leg(dev, world, rank, iters=10, warmup=3):
     if world == 1:
         out["identity_us_per_layer"] = ident_us
         out["note"] = ("world 1: the exchange runs over a one-rank NCCL communicator (self send/recv); "
-                       "identity_us_per_layer = the no-exchange shortcut. The local table is the EP8 fit "
-                       "(32 local experts) applied to 256 local experts")
+                       "identity_us_per_layer = the no-exchange shortcut")
+    out["table_fitted_for_local_experts"] = table_matches
     return out
 
 

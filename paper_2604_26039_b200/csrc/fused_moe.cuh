@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     //   kUnroll loads in flight whatever the row length;
     // * small batches: quantise every gathered row here (no extra launch).
     if (p.xq_in != nullptr) {
-      constexpr int kUnroll = 8;
+      constexpr int kUnroll = 16;  // pure copy: 256 B in flight per lane
       const int row16 = p.H / 16, row_sf = p.H / 32;
       const int gw = blockIdx.x * kGatherWarps + (warp - 2), nw = gridDim.x * kGatherWarps;
       const int4* qsrc = reinterpret_cast<const int4*>(p.xq_in);
