@@ -31,7 +31,9 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--cfg", type=int, default=-1)
 a = ap.parse_args()
 geom = BASELINE_MODELS[a.model]
-table_model = "DeepSeek-V3-EP8" if a.model == "DeepSeek-V3" else a.model
+table_model = a.model
+if not (ROOT / "paper_2604_26039_b200" / "data" / f"coeffs_{table_model}_b200_fp8.json").exists():
+    table_model = "DeepSeek-V3-EP8" if a.model == "DeepSeek-V3" else a.model
 pool = enumerate_b200_configs(geom, HardwareModel.b200(), dtype="fp8")
 store = read_coeff_store(ROOT / "paper_2604_26039_b200" / "data" / f"coeffs_{table_model}_b200_fp8.json")
 _, sm, co = parse_coeff_store(store)
