@@ -255,13 +255,7 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   ra.sorted_ids = reinterpret_cast<int32_t*>(ws + L.sorted);
   ra.tile_expert = reinterpret_cast<int32_t*>(ws + L.tiles);
   ra.sel_out = sel_out;
-  // The megakernel gathers the token rows and clears the accumulator after
-  // converting it, so the route kernel is a single block.
-  ra.acc_clear = nullptr;
-  ra.acc_clear_n = 0;
   ra.done = reinterpret_cast<int*>(ws + L.done);
-  ra.x = x;
-  ra.x_sorted = nullptr;
   ra.prof = ramp::g_prof_buffer ? ramp::g_prof_buffer + 148 * 32 : nullptr;
   ra.S = S;
   ra.H = H;
@@ -281,14 +275,13 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   ra.logits_bf16 = logits_bf16;
   ra.renorm = renorm;
   ra.w_out = w_out;
-  const int zero_blocks = 0;
   cudaError_t err = cudaSuccess;
   if (quant_tokens && (phases & 2)) {
     err = ramp::launch_mx_quant_tokens(x, S, H, ws + L.xqt, ws + L.xsft, st);
     if (err != cudaSuccess) return cuda_fail(err, "token quantisation kernel");
   }
   if (phases & 1) {
-    err = ramp::launch_route(ra, zero_blocks, st);
+    err = ramp::launch_route(ra, st);
     if (err != cudaSuccess) return cuda_fail(err, "route kernel");
   }
   if (!(phases & 2)) return RAMP_OK;

@@ -1,15 +1,16 @@
 // Persistent fused-MoE megakernel for sm_100a (north_star (2)).
 //
 // The layer  out[t] = sum_j w[t,j] * W2[e] (silu(W1g[e] x_t) * W1u[e] x_t)
-// runs as ONE launch of one CTA per SM that walks a list of jobs.  Token rows
-// were pre-gathered by the route kernel into expert-sorted order (x_sorted),
-// so every operand tile arrives with a single TMA box:
+// runs as ONE launch of one CTA per SM that walks a list of jobs.  Phase 0
+// gathers the token rows into expert-sorted order (x_sorted; FP8: MXFP8 bytes
+// + scale atoms) behind a grid barrier, so every operand tile arrives with a
+// single TMA box (token blocks of <= 16 rows skip it: TMA gather4 from x):
 //
 //   phase 1  acc[ttn x bm] = W1[e][gate|up stripe] . x_sorted[M-tile]^T
 //            one 3D TMA box {64, n_i, 2} brings the gate AND up rows of a
 //            k-block, one 2D box brings bm token rows; tcgen05.mma kind::f16
 //            with M = 128 weight rows, N = bm tokens ("swap-AB", so bm can be
-//            4..128), fp32 accumulators in TMEM.
+//            4..256), fp32 accumulators in TMEM.
 //   phase 2  act = silu(gate) * up   (TMEM -> registers -> bf16)
 //   phase 3  acc[128 x bm] = W2[e][h-chunk, :] . act^T, then the epilogue
 //            scales by the top-k weight and scatter-reduces into the fp32
@@ -86,16 +87,16 @@ __host__ __device__ inline int moe_smem_bytes(int bm, int ttn, int stg, int mode
   return 1024 + kCtrlBytes + kStageBytesScatter + stg * (fp8 ? stage_bytes_fp8(bm, ttn, kps) : stage_bytes(bm, ttn, kps)) +
          (fp8 ? 0 : act_bytes(bm, ttn, mode));
 }
-__host__ __device__ inline int bmn_index(int bmN) { return bmN <= 16 ? 0 : bmN <= 32 ? 1 : bmN <= 64 ? 2 : 3; }
+__host__ __device__ inline int bmn_index(int bmN) { return bmN <= 16 ? 0 : bmN <= 32 ? 1 : bmN <= 64 ? 2 : bmN <= 128 ? 3 : 4; }
 
 struct MoeMaps {
-  CUtensorMap xs[4];   // x_sorted [rows, H],  box {64, 16/32/64/128}
-  CUtensorMap act[4];  // act_g    [rows, I],  box {64, 16/32/64/128}
+  CUtensorMap xs[5];   // x_sorted [rows, H],  box {64, 16/32/64/128/256}
+  CUtensorMap act[5];  // act_g    [rows, I],  box {64, 16/32/64/128/256}
   CUtensorMap w1[3];   // W1 as [2E, I, H],    box {64, n_i, 2} for n_i = 64 / 128 / 256
   CUtensorMap w2;      // W2 as [E*H, I],      box {64, 128}
   CUtensorMap x;       // x [S, H], box {64, 1}: TMA gather4 of token rows (bm <= 16 configs)
   // FP8 path (byte tensors, 128 elements per 128-byte swizzled row)
-  CUtensorMap xq[4];   // x_q   [rows, H] e4m3, box {128, 16/32/64/128}
+  CUtensorMap xq[4];   // x_q   [rows, H] e4m3, box {128, 16/32/64/128} (FP8: bm <= 128)
   CUtensorMap actq[4]; // act_q [rows, I] e4m3, box {128, 16/32/64/128}
   CUtensorMap w1q[2];  // W1 e4m3 as [2E, I, H], box {128, n_i, 2} for n_i = 128 / 256
   CUtensorMap w2q;     // W2 e4m3 as [E*H, I],   box {128, 128}
@@ -181,8 +182,8 @@ struct CtrlSmem {
   int32_t job_slot[4];
   uint32_t tmem_base;
   int32_t fin;  // split-K: this CTA completed the (m, s) reduction
-  int32_t epi_tok[128];
-  float epi_w[128];
+  int32_t epi_tok[256];
+  float epi_w[256];
 #ifdef RAMP_PROF_LAT
   unsigned long long t_issue[kMaxStages], t_commit[kMaxStages];
 #endif
@@ -346,8 +347,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
 
   // Prologue (overlaps the route kernel's tail under PDL): descriptors,
   // barriers, TMEM.  Nothing here reads the route kernel's outputs.
-  if (warp == 0 && lane < 13) {
-    // bf16: xs[4], act[4], w1[3], w2, x; fp8: xq[4], actq[4], w1q[2], w2q (contiguous)
+  if (warp == 0 && lane < 15) {
+    // bf16: xs[5], act[5], w1[3], w2, x; fp8: xq[4], actq[4], w1q[2], w2q (contiguous)
     const CUtensorMap* all = kFp8 ? &maps.xq[0] : &maps.xs[0];
     if (!kFp8 || lane < 11) tma_prefetch_desc(all + lane);
   }
@@ -400,6 +401,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   G.mode = cf.mode;
   G.bm = cf.bm;
   G.bmN = bm_mma(G.bm);
+  if (kFp8 && G.bmN > 128) __trap();  // FP8 token blocks are at most 128 rows (one scale atom)
   const int ttn = cf.ttn;
   G.nA = ttn >= 256 ? ttn / 128 : 1;  // ttn = 128: one tile = 64 gate rows + 64 up rows
   G.n_i = ttn / 2;
@@ -481,7 +483,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             const int q = min(c / row16, nrows - 1);
             cc[u] = c - q * row16;
             const int src = __shfl_sync(0xffffffffu, src_l, q);
-            dst_row[u] = c < nch ? r0 + q * nw : -1;
+            dst_row[u] = c < nch && src >= 0 ? r0 + q * nw : -1;  // padding rows: never read back
             v[u] = make_int4(0, 0, 0, 0);
             if (c < nch && src >= 0) v[u] = __ldg(qsrc + static_cast<int64_t>(src) * row16 + cc[u]);
           }
@@ -515,9 +517,12 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         const int nrows = min(32, (n_post_pad - r0 + nw - 1) / nw);
         for (int q = 0; q < nrows; ++q) {
           const int asg = __shfl_sync(0xffffffffu, asg_l, q);
+          // padding rows are skipped: their MMA columns / act rows are never
+          // scattered, and every column of an MMA depends only on its own row
+          if (asg >= p.n_assign) continue;  // warp-uniform
           const int r = r0 + q * nw;
           const int m = r / G.bm, jr = r - m * G.bm;
-          const int4* src = xv + static_cast<int64_t>(asg < p.n_assign ? asg / p.top_k : 0) * row_vec;
+          const int4* src = xv + static_cast<int64_t>(asg / p.top_k) * row_vec;
           uint8_t* dst = p.x_q + static_cast<int64_t>(r) * p.H;
           uint8_t* sf_row = p.x_sf + static_cast<int64_t>(m) * G.kbH * 512 + (jr & 31) * 16 + (jr >> 5) * 4;
           for (int c0 = lane; c0 < row_vec; c0 += 32 * kUnroll) {
@@ -603,9 +608,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           }
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) {
-            if (c0 + 32 * u < row_vec) {
-              d0[c0 + 32 * u] = v0[u];
-              if (two) d1[c0 + 32 * u] = v1[u];
+            if (c0 + 32 * u < row_vec) {  // padding rows are skipped (never read back)
+              if (a0 < p.n_assign) d0[c0 + 32 * u] = v0[u];
+              if (two && a1 < p.n_assign) d1[c0 + 32 * u] = v1[u];
             }
           }
         }

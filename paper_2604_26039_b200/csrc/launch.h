@@ -8,7 +8,7 @@
 
 namespace ramp {
 
-constexpr int kMaxBm = 128;  // largest token block the megakernel supports
+constexpr int kMaxBm = 256;  // largest token block the megakernel supports (256: BF16, ttn <= 256)
 inline int bm_mma_host(int bm) { return bm <= 16 ? 16 : (bm + 15) / 16 * 16; }
 // TMEM columns kSfCol..511 hold the FP8 MMAs' scale factors (4 columns per
 // 512-byte atom, up to 16 atoms per stage); FP8 accumulators stay below.
@@ -20,7 +20,7 @@ struct RouteArgs {
   int32_t E;
   int32_t forced_cfg;
   ramp_table_t table;
-  int32_t* ctrl;         // [16]: cfg, n_post_pad, n_mtiles, n_eval, bad_ids, ready flag, helpers done
+  int32_t* ctrl;         // [16]: cfg, n_post_pad, n_mtiles, n_eval, bad_ids, -, -, job counter, grid barriers
   int32_t* hist_out;     // [E] or null
   int32_t* sorted_ids;   // [capacity]
   int32_t* tile_expert;  // [capacity]
@@ -28,12 +28,8 @@ struct RouteArgs {
   int32_t* n_eval_out;   // or null
   int64_t* grid_out;     // [n_cfg] or null
   double* pred_out;      // [n_cfg] or null
-  float* acc_clear;      // fp32 accumulator cleared by the helper blocks
-  int64_t acc_clear_n;
   int* done;             // split-mode per-M-tile counters, zeroed by block 0
   unsigned long long* prof;  // optional globaltimer stamps (diagnostics)
-  const void* x;         // [S, H] bf16 tokens
-  void* x_sorted;        // [rows, H] bf16, gathered by the helper blocks (null: skip)
   int32_t S, H, top_k;
   int32_t pdl_prev;      // launched as a PDL secondary of the previous kernel: 1 = waits before reading
                          // its inputs, 2 = reads nothing of it (waits only before completing)
@@ -47,7 +43,7 @@ struct RouteArgs {
 
 int pdl_mode();          // RAMP_PDL: 0 off, 1 trigger at route entry (default), 2 trigger at route exit
 
-cudaError_t launch_route(const RouteArgs& a, int zero_blocks, cudaStream_t stream);
+cudaError_t launch_route(const RouteArgs& a, cudaStream_t stream);
 cudaError_t launch_align(const int32_t* ids, int64_t n, int E, int bm, int32_t* hist, int32_t* sorted_ids,
                          int32_t* tile_expert, int32_t* n_post_pad, cudaStream_t stream);
 cudaError_t launch_select(const int32_t* hist, int E, const ramp_table_t& t, int32_t* cfg_out,

@@ -135,6 +135,9 @@ int64_t config_smem_bytes(int bm, int ttn, int stg, int mode, bool fp8, int kps)
     return 0;
   if (mode != kModeFused && mode != kModeSplit) return 0;
   if (kps != 1 && (kps != 2 && kps != 4)) return 0;
+  // TMEM: the phase-1 accumulator (ttn/128 tiles of bm_mma columns) within 512 columns
+  if ((ttn >= 256 ? ttn / 128 : 1) * bm_mma_host(bm) > 512) return 0;
+  if (fp8 && bm_mma_host(bm) > 128) return 0;
   const int b = moe_smem_bytes(bm, ttn, stg, mode, fp8, kps);
   return b <= kSmemLimit ? b : 0;
 }
@@ -153,7 +156,7 @@ static int sm_count_cached() {
 static bool build_maps(const MoeLaunch& l, MoeMaps& maps) {
   bool ok = true;
   if (!l.fp8) {
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 5; ++i) {
       ok = ok && make_map_2d(&maps.xs[i], l.x_sorted, l.rows, l.H, 16u << i);
       ok = ok && make_map_2d(&maps.act[i], l.act_g, l.rows, l.I, 16u << i);
     }

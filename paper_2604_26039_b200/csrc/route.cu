@@ -159,10 +159,6 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0 && a.x_sorted != nullptr && gridDim.x > 1) {
-    __threadfence();
-    st_release_gpu(a.ctrl + 5, 1);
-  }
   RCLK(21);
   stamp(4);
   // the previous grid (the FP8 token quantisation) must be complete before
@@ -235,7 +231,7 @@ static cudaError_t launch_route_t(const RouteArgs& a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_route(const RouteArgs& a, int /*zero_blocks*/, cudaStream_t stream) {
+cudaError_t launch_route(const RouteArgs& a, cudaStream_t stream) {
   const bool dispatch = a.forced_cfg < 0;
   if (a.logits) return dispatch ? launch_route_t<true, true>(a, stream) : launch_route_t<true, false>(a, stream);
   return dispatch ? launch_route_t<false, true>(a, stream) : launch_route_t<false, false>(a, stream);

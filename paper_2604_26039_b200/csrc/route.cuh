@@ -82,7 +82,9 @@ __device__ inline RouteSmem carve_route_smem(unsigned char* base, int E, int64_t
   s.hist = reinterpret_cast<int32_t*>(base);
   s.off = s.hist + E;
   s.cnt = s.off + E + 1;
-  s.ids = s.cnt + 32 * E;
+  // 16-byte aligned: filled with cp.async 16-byte copies (the byte budget's
+  // 64-byte tail covers this and the stage's alignment)
+  s.ids = reinterpret_cast<int32_t*>((reinterpret_cast<uintptr_t>(s.cnt + 32 * E) + 15) & ~static_cast<uintptr_t>(15));
   s.cached = n <= kIdCache;
   const uintptr_t st = reinterpret_cast<uintptr_t>(s.ids + (s.cached ? n : 0));
   s.stage = reinterpret_cast<int32_t*>((st + 15) & ~static_cast<uintptr_t>(15));
@@ -266,9 +268,23 @@ __device__ inline void block_topk(const void* __restrict__ logits, bool bf16, in
 __device__ inline void block_count(const int32_t* __restrict__ ids, int64_t n, int E, RouteSmem& s,
                                    int* bad, bool ids_in_smem = false) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (s.cached && !ids_in_smem)
-        for (int64_t i = tid; i < n; i += blockDim.x) s.ids[i] = __ldg(ids + i);
+  if (s.cached && !ids_in_smem) {
+    // asynchronous 16-byte copies: every thread's loads are in flight at
+    // once (the synchronous loop exposed one L2 round trip per 1024 ids)
+    const bool vec = (n & 3) == 0 && (reinterpret_cast<uintptr_t>(ids) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(s.ids) & 15) == 0;
+    if (vec) {
+      for (int64_t q = tid; q < n / 4; q += blockDim.x)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(
+                         __cvta_generic_to_shared(s.ids + 4 * q))),
+                     "l"(ids + 4 * q)
+                     : "memory");
+    } else {
+      for (int64_t i = tid; i < n; i += blockDim.x) s.ids[i] = __ldg(ids + i);
+    }
+  }
   for (int x = tid; x < 32 * E; x += blockDim.x) s.cnt[x] = 0;
+  asm volatile("cp.async.wait_all;" ::: "memory");
   RCLK(1);
   __syncthreads();
   RCLK(2);

@@ -1,0 +1,33 @@
+"""bench.py's report helpers on synthetic per-point data (CPU): the roofline
+object keeps achieved / peak == frac, sums roofline times over the step, and
+the side legs are compacted for the JSON line."""
+
+import json
+
+import pytest
+
+
+def test_roofline_summary_and_compact_leg(tmp_path, monkeypatch):
+    import bench
+    from paper_2604_26039_b200.catalog import BASELINE_MODELS
+
+    geom = BASELINE_MODELS[bench.MODEL]
+    pts = bench.sweep_points(geom)
+    assert len(pts) == 27
+    per_point = [{"S": p["S"], "beta": p["beta"], "us": 100.0, "megakernel_us": 90.0} for p in pts]
+    step_us = 100.0 * len(pts)
+    k3_bytes = sum(bench.layer_bytes(geom, p["hist"], p["S"]) for p in pts)
+    roof = bench.roofline_summary(geom, pts, per_point, step_us, k3_bytes, 90.0 * len(pts))
+    assert roof["frac"] == pytest.approx(roof["achieved"] / roof["peak"])
+    hbm, tf, _ = bench.load_peaks()
+    want = sum(max(bench.layer_bytes(geom, p["hist"], p["S"]) / hbm / 1e3,
+                   bench.layer_flops(geom, p["S"]) / tf / 1e6) for p in pts) / step_us
+    assert roof["frac"] == pytest.approx(want)
+    assert roof["points_hbm_bound"] + roof["points_tensor_bound"] == 27
+    assert 0 < roof["bytes_only_frac"] <= roof["frac"] + 1e-12
+    leg = {"workload": "w" * 300, "points": [{"S": 8, "beta": 0.5, "us": 1.0, "tflops": 2.0, "extra": 3}],
+           "us_geomean": 1.0}
+    c = bench.compact_leg(leg, ("S", "beta", "us"))
+    assert c["points_S_beta_us"] == [[8, 0.5, 1.0]] and "points" not in c and len(c["workload"]) == 120
+    assert bench.compact_leg({"error": "x"}, ("S",)) == {"error": "x"}
+    json.dumps(roof)

@@ -660,3 +660,28 @@ def test_split_k_counters_many_small_tiles(dtype):
         for c in cfgs:
             out, _ = _run_fused(x, w1, w2, w, ids, table, c)
             assert _rel(out, ref) < RTOL_BF16, (pool.by_id(c).to_dict(), _rel(out, ref))
+
+
+def test_fused_moe_wide_tiles():
+    """bm = 256 token blocks (MMA N = 256; the opt-in `wide_tiles` pool
+    extension, BF16 with ttn <= 256): every such config against the oracle,
+    with full, partial and padded 256-row M-tiles."""
+    from paper_2604_26039_b200.catalog import MoeGeometry
+    from paper_2604_26039_b200.config_space import enumerate_b200_configs
+
+    E, H, I, k, S = 8, 512, 256, 4, 700
+    pool = enumerate_b200_configs(MoeGeometry(name="t", E=E, N=2 * I, K=H, top_k=k), wide_tiles=True)
+    cols = pool.columns()
+    n = len(pool)
+    M = _M()
+    table = M.DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
+                          group_m=cols["group_m"].astype(np.int64), mode=cols["mode"], kps=cols["kps"],
+                          h3=cols["h3"], a=np.ones(n), b=np.zeros(n), c=np.zeros(n), d=np.zeros(n), N=2 * I,
+                          kappa_ok=True, sm_count=148)
+    wide = [c.id for c in pool if c.bm == 256]
+    assert len(wide) >= 8
+    x, w1, w2, w, ids = random_moe(S, H, I, E, k, seed=13, skew=0.3)
+    ref = fused_moe_ref(x, w1, w2, w, ids)
+    for c in wide:
+        out, sel = _run_fused(x, w1, w2, w, ids, table, c)
+        assert _rel(out, ref) < RTOL_BF16, (pool.by_id(c).to_dict(), _rel(out, ref))
