@@ -1,3 +1,10 @@
+"""Every config of the MXFP8 pools (Qwen3-30B-A3B, DeepSeek-V3) at the shipped
+tables' test routings (tests/test_gpu_shipped.py, reduced E, real d_model /
+d_ff) against the oracle, one call at a time with a synchronize after each --
+a hang names its config (development tool; run under `timeout`).
+
+    timeout 400 python scripts/fp8_config_sweep.py [Qwen3|DeepSeek]
+"""
 import sys, os, time
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
