@@ -29,6 +29,8 @@ ap.add_argument("--k", type=int, default=8)
 ap.add_argument("--prof", action="store_true")
 ap.add_argument("--fp8", action="store_true", help="the MXFP8 megakernel (FP8 pool)")
 ap.add_argument("--kps", type=int, default=1)
+ap.add_argument("--beta", type=float, default=None,
+                help="route with the reference sampler's histogram at this beta (instead of --skew)")
 a = ap.parse_args()
 E, H, I, k, S = a.E, a.H, a.I, a.k, a.S
 gen = torch.Generator(device="cuda").manual_seed(0)
@@ -49,7 +51,16 @@ if a.fp8:
 else:
     run = lambda: M.fused_moe(x, w1, w2, w, ids, table, cfg, workspace=ws)  # noqa: E731
 x = torch.randn(S, H, device="cuda", generator=gen).to(torch.bfloat16)
-ids, w = topk(S, k, E, a.skew, gen)
+if a.beta is None:
+    ids, w = topk(S, k, E, a.skew, gen)
+else:
+    from paper_2604_26039_b200.routing import sample_histogram
+    from paper_2604_26039_b200.sweep import make_inputs
+
+    g_ = MoeGeometry(name="p", E=E, N=2 * I, K=H, top_k=k)
+    hist = sample_histogram(E, S, k, a.beta, 4242).histogram
+    x, ids, w = make_inputs(g_, hist, 4242)
+    print("active experts", hist.active_experts)
 ws = M.Workspace(S, H, I, E, k)
 for _ in range(a.reps):
     out = run()
