@@ -266,10 +266,12 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   // but a few) ahead of the route kernel (its programmatic dependent) instead
   // of re-quantising every gathered row in the megakernel's phase 0 (top_k x
   // the work).  Small batches keep the single in-megakernel pass: the extra
-  // launch costs more than it saves (measured: +3-5 % at S*k <= 1024,
-  // -3 / -7 % at S*k = 4096 / 16384 on Qwen3-30B-A3B).
-  constexpr int64_t kQuantTokensMinAssign = 4096;
-  const bool quant_tokens = fp8 && !xsf_in && (int64_t)S * top_k >= kQuantTokensMinAssign;
+  // launch costs more than it saves (measured on Qwen3-30B-A3B, H = 2048:
+  // +3-5 % at S*k <= 1024, -3 / -7 % at S*k = 4096 / 16384).  The in-kernel
+  // pass quantises S*k rows of H elements, so the switch is on that volume:
+  // DeepSeek-V3 (H = 7168) at S*k = 2048 spent 24 us in it.
+  constexpr int64_t kQuantTokensMinElems = int64_t(4096) * 2048;
+  const bool quant_tokens = fp8 && !xsf_in && (int64_t)S * top_k * H >= kQuantTokensMinElems;
   if (quant_tokens && (phases & 2)) ra.pdl_prev = 2;
   ra.logits = logits;
   ra.logits_bf16 = logits_bf16;

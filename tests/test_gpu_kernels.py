@@ -466,7 +466,7 @@ def test_fused_moe_fp8_baseline_shapes(name, E, H, I, k, S, skew):
     _fp8_case(x, w1, w2, w, ids, table, [-1] + [c.id for c in pool][::6])
 
 
-# (S * top_k >= 4096: tokens quantised once by the separate kernel ahead of the route kernel)
+# (S * top_k * H >= 4096 * 2048: tokens quantised once by the separate kernel ahead of the route kernel)
 @pytest.mark.parametrize("model,S,beta", [("Qwen3-30B-A3B", 256, 0.5), ("DeepSeek-V3", 64, 0.5),
                                           ("Qwen3-30B-A3B", 1024, 0.5), ("DeepSeek-V3", 640, 0.5)])
 def test_fused_moe_fp8_full_geometry_rows(model, S, beta):
