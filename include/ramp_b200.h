@@ -203,6 +203,26 @@ int ramp_fused_moe_fp8_prequant(const uint8_t* x_q, const uint8_t* x_sf, const v
                                 int32_t S, int32_t H, int32_t I, int32_t E, int32_t top_k, const ramp_table_t* table,
                                 int32_t forced_cfg, void* out, int32_t* sel_out, void* workspace,
                                 size_t workspace_bytes, int32_t phases, void* stream);
+/* Token-row strides of the per-token inputs (0 = dense), for tokens that sit
+ * inside wider rows -- e.g. the received rows of an expert-parallel message
+ * (ramp_ep_row_layout), where x, its scales, the ids and the weights of one
+ * token share a row.  x_stride: bytes between rows of x (multiple of 16);
+ * sf_stride: bytes between rows of x_sf (multiple of 4); ids_stride / w_stride:
+ * elements between rows of topk_ids / topk_w (>= top_k). */
+typedef struct {
+  int64_t x_stride;
+  int64_t sf_stride;
+  int64_t ids_stride;
+  int64_t w_stride;
+} ramp_row_strides_t;
+/* ramp_fused_moe_bf16_ex / ramp_fused_moe_fp8 / ramp_fused_moe_fp8_prequant
+ * with row-strided token inputs: BF16 when w1_sf is null; else MXFP8, the
+ * tokens bf16 when x_sf is null, already MXFP8 (x = e4m3 bytes) when not. */
+int ramp_fused_moe_strided(const void* x, const uint8_t* x_sf, const void* w1, const uint8_t* w1_sf, const void* w2,
+                           const uint8_t* w2_sf, const float* topk_w, const int32_t* topk_ids,
+                           const ramp_row_strides_t* strides, int32_t S, int32_t H, int32_t I, int32_t E,
+                           int32_t top_k, const ramp_table_t* table, int32_t forced_cfg, void* out, int32_t* sel_out,
+                           void* workspace, size_t workspace_bytes, int32_t phases, void* stream);
 int64_t ramp_config_smem_bytes_fp8(int32_t bm, int32_t ttn, int32_t stg);
 /* Same with kps k-blocks (128 K-elements each) per stage (1 or 2); 0 if not realisable. */
 int64_t ramp_config_smem_bytes_fp8_kps(int32_t bm, int32_t ttn, int32_t stg, int32_t kps);
@@ -231,25 +251,32 @@ void ramp_set_profile_buffer(unsigned long long* dev_buf);
  * otherwise write).  Rank r of `world` owns experts [r*E/world, (r+1)*E/world).
  * Every exchange moves fixed-capacity blocks -- `cap` rows per destination
  * (cap = S never drops a pair) -- so no split size is read on the host and
- * the layer is CUDA-graph capturable:
- *   send_x   [world][cap][H] bf16, or e4m3 with send_sf [world][cap][H/32]
- *            UE8M0 (RAMP_EP_WIRE_MXFP8: 0.52x the bytes; the FP8 megakernel
- *            consumes it directly, ramp_fused_moe_fp8_prequant)
- *   send_ids [world][cap][k] rank-local expert ids, -1 = another rank's slot
- *            or a padding row (skipped by the route kernel: no work)
- *   send_w   [world][cap][k] fp32 weights (0 on -1 slots)
+ * the layer is CUDA-graph capturable.  A row is one self-contained message
+ * of row_bytes (ramp_ep_row_layout), so a dispatch is ONE send / receive per
+ * peer:
+ *   send     [world][cap][row_bytes]; row = the token (H bf16, or H e4m3 +
+ *            H/32 UE8M0 scales at off_sf: RAMP_EP_WIRE_MXFP8, 0.52x the
+ *            bytes, consumed as is by the FP8 megakernel), its top_k
+ *            rank-local expert ids at off_ids (int32, -1 = another rank's slot
+ *            or a padding row: skipped by the route kernel, no work) and their
+ *            fp32 weights at off_w (0 on -1 slots)
  *   pos      [S][world] row of (token, rank) in the send blocks, -1 = none
  *   counts   [world] rows sent; *overflow = 1 if some rank needed > cap rows
- * Receive buffers have the same shapes (block s came from rank s).
+ * The receive buffer has the same shape (block s came from rank s); the local
+ * layer reads it in place through ramp_fused_moe_strided (all four strides =
+ * row_bytes).
  */
 #define RAMP_EP_WIRE_BF16 0
 #define RAMP_EP_WIRE_MXFP8 1
 typedef struct ramp_ep_comm ramp_ep_comm;
 
+/* Row layout of the wire: out4 = {off_sf (-1 for bf16), off_ids, off_w,
+ * row_bytes}, every offset and row_bytes a multiple of 16 (off_w: of 4). */
+int ramp_ep_row_layout(int32_t H, int32_t top_k, int32_t wire, int32_t* out4);
 /* pack only (the exchange is left to the caller, e.g. torch.distributed) */
 int ramp_ep_pack(const void* x, const int32_t* topk_ids, const float* topk_w, int32_t S, int32_t H, int32_t E,
-                 int32_t top_k, int32_t world, int32_t cap, int32_t wire, void* send_x, uint8_t* send_sf,
-                 int32_t* send_ids, float* send_w, int32_t* pos, int32_t* counts, int32_t* overflow, void* stream);
+                 int32_t top_k, int32_t world, int32_t cap, int32_t wire, void* send, int32_t* pos, int32_t* counts,
+                 int32_t* overflow, void* stream);
 /* out[t] = sum over ranks d (in rank order) of back[d][pos[t][d]] (fp32 sum, bf16 out) */
 int ramp_ep_reduce(const void* back, const int32_t* pos, int32_t S, int32_t H, int32_t world, int32_t cap,
                    void* out, void* stream);
@@ -258,11 +285,11 @@ int ramp_ep_reduce(const void* back, const int32_t* pos, int32_t S, int32_t H, i
 int ramp_ep_get_unique_id(unsigned char* out128);
 int ramp_ep_comm_init(ramp_ep_comm** comm, const unsigned char* id128, int32_t world, int32_t rank);
 int ramp_ep_comm_destroy(ramp_ep_comm* comm);
-/* pack + one grouped NCCL all-to-all of x (+ scales), ids and weights */
+/* pack + one grouped NCCL all-to-all of the row blocks (one send and one
+ * receive per peer) */
 int ramp_ep_dispatch(ramp_ep_comm* comm, const void* x, const int32_t* topk_ids, const float* topk_w, int32_t S,
-                     int32_t H, int32_t E, int32_t top_k, int32_t cap, int32_t wire, void* send_x, uint8_t* send_sf,
-                     int32_t* send_ids, float* send_w, int32_t* pos, int32_t* counts, int32_t* overflow,
-                     void* recv_x, uint8_t* recv_sf, int32_t* recv_ids, float* recv_w, void* stream);
+                     int32_t H, int32_t E, int32_t top_k, int32_t cap, int32_t wire, void* send, int32_t* pos,
+                     int32_t* counts, int32_t* overflow, void* recv, void* stream);
 /* NCCL all-to-all of the partial outputs [world*cap][H] bf16 back into
  * back[world][cap][H], then ramp_ep_reduce into out[S][H] */
 int ramp_ep_combine(ramp_ep_comm* comm, const void* partial, void* back, const int32_t* pos, int32_t S, int32_t H,

@@ -39,24 +39,44 @@ def mx_dequantize_bytes(q: np.ndarray, sf: np.ndarray) -> np.ndarray:
         np.float32)
 
 
+def row_layout_ref(H: int, k: int, wire: str):
+    """(off_sf, off_ids, off_w, row_bytes) of one wire row: the token at 0 (H
+    bf16, or H e4m3 + H/32 UE8M0 at off_sf = H), k int32 ids at the next
+    16-byte boundary, k fp32 weights right after, row padded to 16 bytes."""
+    fp8 = wire == "fp8"
+    tok = H + H // 32 if fp8 else 2 * H
+    off_ids = -(-tok // 16) * 16
+    off_w = off_ids + 4 * k
+    return (H if fp8 else -1), off_ids, off_w, -(-(off_w + 4 * k) // 16) * 16
+
+
+def _bf16_bytes(x: np.ndarray) -> np.ndarray:
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(torch.bfloat16).view(torch.uint8).numpy()
+
+
 def ep_pack_ref(x, ids, w, E: int, world: int, cap: int, wire: str = "bf16"):
-    """numpy: returns send_x ([world*cap, H] bf16-as-fp32 or e4m3 bytes),
-    send_sf ([world*cap, H/32] or None), send_ids, send_w, pos [S, world],
-    counts [world], overflow (0/1).  Unwritten payload rows are zero."""
+    """numpy: returns send [world*cap, row_bytes] uint8 (the wire rows, see
+    row_layout_ref; bytes the kernel does not define -- padding rows' tokens,
+    alignment gaps -- are zero here), pos [S, world], counts [world],
+    overflow (0/1)."""
     x = np.asarray(x, dtype=np.float32)
     ids = np.asarray(ids)
     w = np.asarray(w, dtype=np.float32)
     S, H = x.shape
     k = ids.shape[1]
     per = E // world
-    send_x = np.zeros((world * cap, H), dtype=np.uint8 if wire == "fp8" else np.float32)
-    send_sf = np.zeros((world * cap, H // 32), dtype=np.uint8) if wire == "fp8" else None
-    send_ids = np.full((world * cap, k), -1, dtype=np.int32)
-    send_w = np.zeros((world * cap, k), dtype=np.float32)
+    off_sf, off_ids, off_w, rb = row_layout_ref(H, k, wire)
+    send = np.zeros((world * cap, rb), dtype=np.uint8)
+    fill_ids = np.full(k, -1, dtype=np.int32).view(np.uint8)
+    for r in range(world * cap):  # padding rows: ids -1, weights 0
+        send[r, off_ids:off_ids + 4 * k] = fill_ids
     pos = np.full((S, world), -1, dtype=np.int32)
     counts = np.zeros(world, dtype=np.int64)
     overflow = 0
-    q, sf = mx_quantize_bytes(x) if wire == "fp8" and S else (None, None)
+    if wire == "fp8":
+        q, sf = mx_quantize_bytes(x) if S else (None, None)
+    else:
+        xb = _bf16_bytes(x) if S else None
     for t in range(S):
         for d in range(world):
             own = [(j, int(e)) for j, e in enumerate(ids[t]) if 0 <= e < E and e // per == d]
@@ -70,13 +90,31 @@ def ep_pack_ref(x, ids, w, E: int, world: int, cap: int, wire: str = "bf16"):
             pos[t, d] = row
             r = d * cap + row
             if wire == "fp8":
-                send_x[r], send_sf[r] = q[t], sf[t]
+                send[r, :H] = q[t]
+                send[r, off_sf:off_sf + H // 32] = sf[t]
             else:
-                send_x[r] = x[t]
+                send[r, :2 * H] = xb[t]
+            rid = np.full(k, -1, dtype=np.int32)
+            rw = np.zeros(k, dtype=np.float32)
             for j, e in own:
-                send_ids[r, j] = e - d * per
-                send_w[r, j] = w[t, j]
-    return send_x, send_sf, send_ids, send_w, pos, np.minimum(counts, cap).astype(np.int32), overflow
+                rid[j] = e - d * per
+                rw[j] = w[t, j]
+            send[r, off_ids:off_ids + 4 * k] = rid.view(np.uint8)
+            send[r, off_w:off_w + 4 * k] = rw.view(np.uint8)
+    return send, pos, np.minimum(counts, cap).astype(np.int32), overflow
+
+
+def ep_rows_defined(send: np.ndarray, counts, cap: int, H: int, k: int, wire: str) -> np.ndarray:
+    """Byte mask of the wire rows the pack kernel defines: the ids / weights
+    of every row, the token (and scales) of the rows below each count."""
+    off_sf, off_ids, off_w, rb = row_layout_ref(H, k, wire)
+    m = np.zeros(send.shape, dtype=bool)
+    m[:, off_ids:off_w + 4 * k] = True
+    tok = [(0, H), (off_sf, off_sf + H // 32)] if wire == "fp8" else [(0, 2 * H)]
+    for d, c in enumerate(counts):
+        for a, b in tok:
+            m[d * cap:d * cap + int(c), a:b] = True
+    return m
 
 
 def ep_reduce_ref(back, pos, world: int, cap: int) -> np.ndarray:
@@ -96,11 +134,8 @@ class RefKernels:
     """paper_2604_26039_b200.ep's `kernels=` interface on CPU tensors."""
 
     def pack(self, x, topk_ids, topk_w, E, world, cap, wire):
-        sx, ssf, sid, sw, pos, cnt, ovf = ep_pack_ref(x.float().numpy(), topk_ids.numpy(), topk_w.numpy(), E, world,
-                                                     cap, wire)
-        send_x = torch.from_numpy(sx) if wire == "fp8" else torch.from_numpy(sx).to(x.dtype)
-        return (send_x, None if ssf is None else torch.from_numpy(ssf), torch.from_numpy(sid),
-                torch.from_numpy(sw), torch.from_numpy(pos), torch.from_numpy(cnt),
+        send, pos, cnt, ovf = ep_pack_ref(x.float().numpy(), topk_ids.numpy(), topk_w.numpy(), E, world, cap, wire)
+        return (torch.from_numpy(send), torch.from_numpy(pos), torch.from_numpy(cnt),
                 torch.tensor([ovf], dtype=torch.int32))
 
     def reduce(self, back, pos, world, cap):

@@ -59,12 +59,15 @@ SIGNATURES["ramp_fused_moe_fp8_prequant"] = (
     [ctypes.c_void_p] * 8 + [ctypes.c_int32] * 5 + [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
                                                     ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32, ctypes.c_void_p])
 _vp, _i32 = ctypes.c_void_p, ctypes.c_int32
-SIGNATURES["ramp_ep_pack"] = (ctypes.c_int, [_vp] * 3 + [_i32] * 7 + [_vp] * 8)
+SIGNATURES["ramp_fused_moe_strided"] = (
+    ctypes.c_int, [_vp] * 9 + [_i32] * 5 + [_vp, _i32, _vp, _vp, _vp, ctypes.c_size_t, _i32, _vp])
+SIGNATURES["ramp_ep_row_layout"] = (ctypes.c_int, [_i32] * 3 + [_vp])
+SIGNATURES["ramp_ep_pack"] = (ctypes.c_int, [_vp] * 3 + [_i32] * 7 + [_vp] * 5)
 SIGNATURES["ramp_ep_reduce"] = (ctypes.c_int, [_vp, _vp] + [_i32] * 4 + [_vp, _vp])
 SIGNATURES["ramp_ep_get_unique_id"] = (ctypes.c_int, [_vp])
 SIGNATURES["ramp_ep_comm_init"] = (ctypes.c_int, [ctypes.POINTER(_vp), _vp, _i32, _i32])
 SIGNATURES["ramp_ep_comm_destroy"] = (ctypes.c_int, [_vp])
-SIGNATURES["ramp_ep_dispatch"] = (ctypes.c_int, [_vp] * 4 + [_i32] * 6 + [_vp] * 12)
+SIGNATURES["ramp_ep_dispatch"] = (ctypes.c_int, [_vp] * 4 + [_i32] * 6 + [_vp] * 6)
 SIGNATURES["ramp_ep_combine"] = (ctypes.c_int, [_vp] * 4 + [_i32] * 3 + [_vp, _vp])
 SIGNATURES["ramp_fused_moe_bf16_ex"] = (
     ctypes.c_int, SIGNATURES["ramp_fused_moe_bf16"][1][:-1] + [ctypes.c_int32, ctypes.c_void_p])
@@ -100,6 +103,13 @@ class RampTable(ctypes.Structure):
         ("step_cache_cap", ctypes.c_int32),
         ("h3", ctypes.c_void_p),
     ]
+
+
+class RowStrides(ctypes.Structure):
+    """ramp_row_strides_t (include/ramp_b200.h): token-row strides, 0 = dense."""
+
+    _fields_ = [("x_stride", ctypes.c_int64), ("sf_stride", ctypes.c_int64), ("ids_stride", ctypes.c_int64),
+                ("w_stride", ctypes.c_int64)]
 
 
 class RampError(RuntimeError):

@@ -214,7 +214,8 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
                       int32_t top_k, const ramp_table_t* table, int32_t forced_cfg, void* out, int32_t* sel_out,
                       void* workspace, size_t workspace_bytes, int32_t phases, void* stream, bool fp8,
                       const void* logits = nullptr, int32_t logits_bf16 = 0, int32_t renorm = 0,
-                      float* w_out = nullptr, const uint8_t* xsf_in = nullptr) {
+                      float* w_out = nullptr, const uint8_t* xsf_in = nullptr,
+                      const ramp_row_strides_t* rs = nullptr) {
   if (phases < 1 || phases > 3) return fail(RAMP_EINVAL, "phases must be 1 (route), 2 (megakernel) or 3");
   if (int rc = check_table(table)) return rc;
   if (S < 0) return fail(RAMP_EINVAL, "S must be >= 0");
@@ -246,6 +247,7 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
 
   ramp::RouteArgs ra{};
   ra.topk_ids = topk_ids;
+  ra.ids_stride = rs ? rs->ids_stride : 0;
   ra.n_assign = (int64_t)S * top_k;
   ra.E = E;
   ra.forced_cfg = forced_cfg;
@@ -271,7 +273,8 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   // pass quantises S*k rows of H elements, so the switch is on that volume:
   // DeepSeek-V3 (H = 7168) at S*k = 2048 spent 24 us in it.
   constexpr int64_t kQuantTokensMinElems = int64_t(4096) * 2048;
-  const bool quant_tokens = fp8 && !xsf_in && (int64_t)S * top_k * H >= kQuantTokensMinElems;
+  // (dense tokens only: the quantisation kernel reads x as [S, H])
+  const bool quant_tokens = fp8 && !xsf_in && !(rs && rs->x_stride) && (int64_t)S * top_k * H >= kQuantTokensMinElems;
   if (quant_tokens && (phases & 2)) ra.pdl_prev = 2;
   ra.logits = logits;
   ra.logits_bf16 = logits_bf16;
@@ -314,6 +317,9 @@ static int fused_impl(const void* x, const void* w1, const uint8_t* w1_sf, const
   ml.act_sf = ws + L.actsf;
   ml.xq_in = xsf_in ? static_cast<const uint8_t*>(x) : (quant_tokens ? ws + L.xqt : nullptr);  // e4m3 rows
   ml.xsf_in = xsf_in ? xsf_in : (quant_tokens ? ws + L.xsft : nullptr);
+  ml.x_stride = rs && !quant_tokens ? rs->x_stride : 0;
+  ml.sf_stride = rs && xsf_in ? rs->sf_stride : 0;
+  ml.w_stride = rs ? rs->w_stride : 0;
   ml.table = *table;
   ml.S = S;
   ml.H = H;
@@ -378,6 +384,38 @@ int ramp_fused_moe_fp8_prequant(const uint8_t* x_q, const uint8_t* x_sf, const v
                     sel_out, workspace, workspace_bytes, phases, stream, true, nullptr, 0, 0, nullptr, x_sf);
 }
 
+int ramp_fused_moe_strided(const void* x, const uint8_t* x_sf, const void* w1, const uint8_t* w1_sf, const void* w2,
+                           const uint8_t* w2_sf, const float* topk_w, const int32_t* topk_ids,
+                           const ramp_row_strides_t* strides, int32_t S, int32_t H, int32_t I, int32_t E,
+                           int32_t top_k, const ramp_table_t* table, int32_t forced_cfg, void* out, int32_t* sel_out,
+                           void* workspace, size_t workspace_bytes, int32_t phases, void* stream) {
+  const bool fp8 = w1_sf != nullptr;
+  ramp_row_strides_t rs{};
+  if (strides) rs = *strides;
+  const int64_t x_bytes = (fp8 && x_sf) ? H : 2 * (int64_t)H;
+  if (rs.x_stride < 0 || rs.sf_stride < 0 || rs.ids_stride < 0 || rs.w_stride < 0)
+    return fail(RAMP_EINVAL, "strides must be >= 0");
+  if (rs.x_stride && (rs.x_stride < x_bytes || rs.x_stride % 16 != 0))
+    return fail(RAMP_EINVAL, "x_stride must be >= the row's bytes and a multiple of 16");
+  if (rs.sf_stride && (!x_sf || rs.sf_stride < H / 32 || rs.sf_stride % 4 != 0))
+    return fail(RAMP_EINVAL, "sf_stride needs x_sf, >= H/32 and a multiple of 4");
+  if ((rs.ids_stride && rs.ids_stride < top_k) || (rs.w_stride && rs.w_stride < top_k))
+    return fail(RAMP_EINVAL, "ids_stride / w_stride must be >= top_k");
+  if (rs.ids_stride == top_k) rs.ids_stride = 0;
+  if (rs.w_stride == top_k) rs.w_stride = 0;
+  if (rs.x_stride == x_bytes) rs.x_stride = 0;
+  if (rs.sf_stride == H / 32) rs.sf_stride = 0;
+  if (fp8) {
+    if (S > 0 && !w2_sf) return fail(RAMP_EINVAL, "null scale-factor tensor");
+    if (x_sf && reinterpret_cast<uintptr_t>(x_sf) % 4 != 0) return fail(RAMP_EINVAL, "x_sf must be 4-byte aligned");
+    if (I % 256 != 0) return fail(RAMP_EINVAL, "FP8 path needs d_ff a multiple of 256");
+  } else if (x_sf || w2_sf) {
+    return fail(RAMP_EINVAL, "x_sf / w2_sf given without w1_sf (BF16 layer)");
+  }
+  return fused_impl(x, w1, w1_sf, w2, w2_sf, topk_w, topk_ids, S, H, I, E, top_k, table, forced_cfg, out, sel_out,
+                    workspace, workspace_bytes, phases, stream, fp8, nullptr, 0, 0, nullptr, x_sf, &rs);
+}
+
 // ------------------------------------------------------------ expert parallelism
 struct ramp_ep_comm {
   void* nccl;
@@ -397,16 +435,26 @@ static int ep_check(const void* x, const int32_t* topk_ids, const float* topk_w,
   return RAMP_OK;
 }
 
+int ramp_ep_row_layout(int32_t H, int32_t top_k, int32_t wire, int32_t* out4) {
+  if (!out4) return fail(RAMP_EINVAL, "null output");
+  if (H < 128 || H % 128 != 0) return fail(RAMP_EINVAL, "H (d_model) must be a positive multiple of 128");
+  if (top_k < 1) return fail(RAMP_EINVAL, "top_k must be >= 1");
+  if (wire != RAMP_EP_WIRE_BF16 && wire != RAMP_EP_WIRE_MXFP8) return fail(RAMP_EINVAL, "unknown wire format");
+  ramp::ep_row_layout(H, top_k, wire == RAMP_EP_WIRE_MXFP8, out4);
+  return RAMP_OK;
+}
+
 int ramp_ep_pack(const void* x, const int32_t* topk_ids, const float* topk_w, int32_t S, int32_t H, int32_t E,
-                 int32_t top_k, int32_t world, int32_t cap, int32_t wire, void* send_x, uint8_t* send_sf,
-                 int32_t* send_ids, float* send_w, int32_t* pos, int32_t* counts, int32_t* overflow, void* stream) {
+                 int32_t top_k, int32_t world, int32_t cap, int32_t wire, void* send, int32_t* pos, int32_t* counts,
+                 int32_t* overflow, void* stream) {
   if (int rc = ep_check(x, topk_ids, topk_w, S, H, E, top_k, world, cap, wire)) return rc;
-  if (!send_x || !send_ids || !send_w || !pos || !counts || !overflow ||
-      (wire == RAMP_EP_WIRE_MXFP8 && !send_sf))
+  if ((!send && (int64_t)world * cap > 0) || (!pos && S > 0) || !counts || !overflow)
     return fail(RAMP_EINVAL, "null send buffer");
-  if (reinterpret_cast<uintptr_t>(send_x) % 16 != 0) return fail(RAMP_EINVAL, "send_x must be 16-byte aligned");
-  ramp::EpPackArgs a{topk_ids, topk_w, x, S, H, top_k, E, world, cap, send_x, send_sf, send_ids, send_w,
-                     pos, counts, overflow};
+  if (reinterpret_cast<uintptr_t>(send) % 16 != 0) return fail(RAMP_EINVAL, "send must be 16-byte aligned");
+  int32_t lay[4];
+  ramp::ep_row_layout(H, top_k, wire == RAMP_EP_WIRE_MXFP8, lay);
+  ramp::EpPackArgs a{topk_ids, topk_w, x, S, H, top_k, E, world, cap, static_cast<uint8_t*>(send),
+                     lay[0], lay[1], lay[2], lay[3], pos, counts, overflow};
   cudaError_t err = ramp::launch_ep_pack(a, wire == RAMP_EP_WIRE_MXFP8, static_cast<cudaStream_t>(stream));
   if (err != cudaSuccess) return cuda_fail(err, "ramp_ep_pack");
   return RAMP_OK;
@@ -449,23 +497,20 @@ int ramp_ep_comm_destroy(ramp_ep_comm* comm) {
 }
 
 int ramp_ep_dispatch(ramp_ep_comm* comm, const void* x, const int32_t* topk_ids, const float* topk_w, int32_t S,
-                     int32_t H, int32_t E, int32_t top_k, int32_t cap, int32_t wire, void* send_x, uint8_t* send_sf,
-                     int32_t* send_ids, float* send_w, int32_t* pos, int32_t* counts, int32_t* overflow,
-                     void* recv_x, uint8_t* recv_sf, int32_t* recv_ids, float* recv_w, void* stream) {
+                     int32_t H, int32_t E, int32_t top_k, int32_t cap, int32_t wire, void* send, int32_t* pos,
+                     int32_t* counts, int32_t* overflow, void* recv, void* stream) {
   if (!comm) return fail(RAMP_EINVAL, "null communicator");
-  if (!recv_x || !recv_ids || !recv_w || (wire == RAMP_EP_WIRE_MXFP8 && !recv_sf))
-    return fail(RAMP_EINVAL, "null receive buffer");
+  if (!recv) return fail(RAMP_EINVAL, "null receive buffer");
   const int32_t P = comm->world;
-  if (int rc = ramp_ep_pack(x, topk_ids, topk_w, S, H, E, top_k, P, cap, wire, send_x, send_sf, send_ids, send_w,
-                            pos, counts, overflow, stream))
+  if (int rc = ramp_ep_pack(x, topk_ids, topk_w, S, H, E, top_k, P, cap, wire, send, pos, counts, overflow, stream))
     return rc;
-  const bool fp8 = wire == RAMP_EP_WIRE_MXFP8;
-  const void* snd[4] = {send_x, send_ids, send_w, send_sf};
-  void* rcv[4] = {recv_x, recv_ids, recv_w, recv_sf};
-  const size_t bytes[4] = {(size_t)cap * H * (fp8 ? 1 : 2), (size_t)cap * top_k * 4, (size_t)cap * top_k * 4,
-                           (size_t)cap * (H / 32)};
+  int32_t lay[4];
+  ramp::ep_row_layout(H, top_k, wire == RAMP_EP_WIRE_MXFP8, lay);
+  const void* snd[1] = {send};
+  void* rcv[1] = {recv};
+  const size_t bytes[1] = {(size_t)cap * lay[3]};
   const char* why = nullptr;
-  if (ramp::nccl_all_to_all(comm->nccl, P, snd, rcv, bytes, fp8 ? 4 : 3, static_cast<cudaStream_t>(stream), &why))
+  if (ramp::nccl_all_to_all(comm->nccl, P, snd, rcv, bytes, 1, static_cast<cudaStream_t>(stream), &why))
     return fail(RAMP_ECUDA, std::string("NCCL dispatch: ") + (why ? why : "?"));
   return RAMP_OK;
 }

@@ -13,7 +13,11 @@
 //            weights (0 there); rows past the count carry ids -1 (the route
 //            kernel skips them: no work).  Token rows travel as bf16 or as
 //            MXFP8 (E4M3 + one UE8M0 scale per 32 features, the FP8
-//            megakernel's operand format).  pos[t][d] remembers the row.
+//            megakernel's operand format).  A row is one self-contained
+//            message -- token, scales, ids, weights at fixed offsets
+//            (ep_row_layout) -- so the exchange is one send / receive per
+//            peer and the receiver's megakernel reads the rows in place
+//            (row-strided inputs).  pos[t][d] remembers the row.
 //   (all-to-all of the P blocks: NCCL, or torch.distributed in the tests)
 //   combine  the per-(token, rank) partial outputs that came back, summed in
 //            fp32 in rank order into out[S,H] bf16 (deterministic).
@@ -36,11 +40,24 @@ namespace ramp {
 constexpr int kEpThreads = 256;
 constexpr int kEpMaxWorld = 32;
 
-__device__ __forceinline__ uint32_t ep_mask(const int32_t* ids, int t, int k, int E, int per) {
+void ep_row_layout(int32_t H, int32_t k, bool fp8_wire, int32_t out4[4]) {
+  auto up16 = [](int32_t v) { return (v + 15) & ~15; };
+  const int32_t tok = fp8_wire ? H + H / 32 : 2 * H;
+  out4[0] = fp8_wire ? H : -1;
+  out4[1] = up16(tok);
+  out4[2] = out4[1] + 4 * k;
+  out4[3] = up16(out4[2] + 4 * k);
+}
+
+// per = experts per rank; shift = log2(per) when per is a power of two
+// (every model here), else -1 (integer division)
+__device__ __forceinline__ int ep_owner(int id, int per, int shift) { return shift >= 0 ? id >> shift : id / per; }
+
+__device__ __forceinline__ uint32_t ep_mask(const int32_t* ids, int t, int k, int E, int per, int shift) {
   uint32_t m = 0;
   for (int j = 0; j < k; ++j) {
     const int id = __ldg(ids + static_cast<int64_t>(t) * k + j);
-    if (id >= 0 && id < E) m |= 1u << (id / per);
+    if (id >= 0 && id < E) m |= 1u << ep_owner(id, per, shift);
   }
   return m;
 }
@@ -53,14 +70,21 @@ __global__ void __launch_bounds__(kEpThreads) ep_pack_kernel(EpPackArgs a) {
   __shared__ int s_pos[kEpThreads][8];  // first 8 destinations' rows of this block's tokens (pos[] has all)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int P = a.world, per = a.E / a.world;
+  const int shift = (per & (per - 1)) == 0 ? __ffs(per) - 1 : -1;
   const int T = (a.S + gridDim.x - 1) / gridDim.x;  // tokens per block (<= kEpThreads)
-  const int t0 = blockIdx.x * T, t1 = min(a.S, t0 + T);
+  const int t0 = min(a.S, static_cast<int>(blockIdx.x) * T), t1 = min(a.S, t0 + T);
   if (tid < kEpMaxWorld) s_before[tid] = s_total[tid] = 0;
+  // this block's token rows start streaming into L2 now; the row copies of
+  // step (4) wait for the counts and the scan, not for HBM
+  if (tid < t1 - t0) bulk_prefetch_l2(static_cast<const uint8_t*>(a.x) + static_cast<int64_t>(t0 + tid) * a.H * 2,
+                                      static_cast<uint32_t>(a.H) * 2);
   __syncthreads();
-  // (1) how many tokens before this block's chunk go to each rank, and in total
+  // (1) how many tokens before this block's chunk go to each rank, and in
+  // total; the destination masks of the block's own tokens are kept
   for (int base = 0; base < a.S; base += kEpThreads) {
     const int t = base + tid;
-    const uint32_t m = t < a.S ? ep_mask(a.ids, t, a.k, a.E, per) : 0u;
+    const uint32_t m = t < a.S ? ep_mask(a.ids, t, a.k, a.E, per, shift) : 0u;
+    if (t >= t0 && t < t1) s_mask[t - t0] = m;
     for (int d = 0; d < P; ++d) {
       const uint32_t b = __ballot_sync(0xffffffffu, (m >> d) & 1u);
       const uint32_t bb = __ballot_sync(0xffffffffu, ((m >> d) & 1u) && t < t0);
@@ -71,10 +95,17 @@ __global__ void __launch_bounds__(kEpThreads) ep_pack_kernel(EpPackArgs a) {
     }
   }
   __syncthreads();
+  if (blockIdx.x == 0 && tid == 0) {  // written, not accumulated: no zero-fill needed before the launch
+    int o = 0;
+    for (int d = 0; d < P; ++d) {
+      a.counts[d] = min(s_total[d], a.cap);
+      o |= s_total[d] > a.cap;  // the caller's capacity is too small: the pairs past it are dropped
+    }
+    *a.overflow = o;
+  }
   // (2) rows of this block's tokens: block-wide exclusive scan per rank
   const int t = t0 + tid;
-  const uint32_t m = t < t1 ? ep_mask(a.ids, t, a.k, a.E, per) : 0u;
-  s_mask[tid] = m;
+  const uint32_t m = t < t1 ? s_mask[tid] : 0u;
   for (int d = 0; d < P; ++d) {
     const uint32_t b = __ballot_sync(0xffffffffu, (m >> d) & 1u);
     if (lane == 0) s_warp[d][warp] = __popc(b);
@@ -93,33 +124,38 @@ __global__ void __launch_bounds__(kEpThreads) ep_pack_kernel(EpPackArgs a) {
     const bool hit = (m >> d) & 1u;
     const uint32_t b = __ballot_sync(0xffffffffu, hit);
     int row = hit ? s_warp[d][warp] + __popc(b & ((1u << lane) - 1u)) : -1;
-    if (row >= a.cap) {
-      atomicExch(a.overflow, 1);  // the caller's capacity is too small: this pair is dropped
-      row = -1;
-    }
+    if (row >= a.cap) row = -1;  // dropped (overflow flagged above)
     if (t < t1) {
       a.pos[static_cast<int64_t>(t) * P + d] = row;
       if (d < 8) s_pos[tid][d] = row;
     }
-    if (row >= 0) {
-      const int64_t r = static_cast<int64_t>(d) * a.cap + row;
-      for (int j = 0; j < a.k; ++j) {
-        const int id = __ldg(a.ids + static_cast<int64_t>(t) * a.k + j);
-        const bool own = id >= 0 && id < a.E && id / per == d;
-        a.send_ids[r * a.k + j] = own ? id - d * per : -1;
-        a.send_w[r * a.k + j] = own ? __ldg(a.w + static_cast<int64_t>(t) * a.k + j) : 0.0f;
-      }
+  }
+  __syncthreads();
+  // (3) the slots of every row: one (token, slot) per thread, so each
+  // thread's two loads are in flight together (no load-after-store chain)
+  for (int it = tid; it < (t1 - t0) * a.k; it += kEpThreads) {
+    const int q = it / a.k, j = it - q * a.k;
+    const int64_t src = static_cast<int64_t>(t0 + q) * a.k + j;
+    const int id = __ldg(a.ids + src);
+    const float wv = __ldg(a.w + src);
+    const int own_d = id >= 0 && id < a.E ? ep_owner(id, per, shift) : -1;
+    for (int d = 0; d < P; ++d) {
+      const int row = d < 8 ? s_pos[q][d] : __ldcg(a.pos + static_cast<int64_t>(t0 + q) * P + d);
+      if (row < 0) continue;
+      uint8_t* msg = a.send + (static_cast<int64_t>(d) * a.cap + row) * a.row_bytes;
+      reinterpret_cast<int32_t*>(msg + a.off_ids)[j] = own_d == d ? id - d * per : -1;
+      reinterpret_cast<float*>(msg + a.off_w)[j] = own_d == d ? wv : 0.0f;
     }
   }
-  if (blockIdx.x == 0 && tid < P) a.counts[tid] = min(s_total[tid], a.cap);
-  // (3) rows past each rank's count: ids -1 / weights 0 (no work on arrival)
+  // rows past each rank's count: ids -1 / weights 0 (no work on arrival)
   const int64_t n_rows = static_cast<int64_t>(P) * a.cap;
   for (int64_t i = blockIdx.x * (int64_t)kEpThreads + tid; i < n_rows; i += (int64_t)gridDim.x * kEpThreads) {
     const int d = static_cast<int>(i / a.cap), row = static_cast<int>(i % a.cap);
     if (row >= s_total[d]) {
+      uint8_t* msg = a.send + i * a.row_bytes;
       for (int j = 0; j < a.k; ++j) {
-        a.send_ids[i * a.k + j] = -1;
-        a.send_w[i * a.k + j] = 0.0f;
+        reinterpret_cast<int32_t*>(msg + a.off_ids)[j] = -1;
+        reinterpret_cast<float*>(msg + a.off_w)[j] = 0.0f;
       }
     }
   }
@@ -148,7 +184,7 @@ __global__ void __launch_bounds__(kEpThreads) ep_pack_kernel(EpPackArgs a) {
           if (!((mq >> d) & 1u)) continue;
           const int row = d < 8 ? s_pos[q][d] : a.pos[static_cast<int64_t>(tt) * P + d];
           if (row < 0) continue;
-          int4* dst = reinterpret_cast<int4*>(a.send_x) + (static_cast<int64_t>(d) * a.cap + row) * row_vec;
+          int4* dst = reinterpret_cast<int4*>(a.send + (static_cast<int64_t>(d) * a.cap + row) * a.row_bytes);
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u)
             if (c0 + 32 * u < row_vec) dst[c0 + 32 * u] = v[u];
@@ -185,9 +221,9 @@ __global__ void __launch_bounds__(kEpThreads) ep_pack_kernel(EpPackArgs a) {
             if (!((mq >> d) & 1u)) continue;
             const int row = d < 8 ? s_pos[q][d] : a.pos[static_cast<int64_t>(tt) * P + d];
             if (row < 0) continue;
-            const int64_t r = static_cast<int64_t>(d) * a.cap + row;
-            *reinterpret_cast<uint2*>(static_cast<uint8_t*>(a.send_x) + r * a.H + c * 8) = qv;
-            if ((lane & 3) == 0) a.send_sf[r * (a.H / 32) + (c >> 2)] = static_cast<uint8_t>(ex + 127);
+            uint8_t* msg = a.send + (static_cast<int64_t>(d) * a.cap + row) * a.row_bytes;
+            *reinterpret_cast<uint2*>(msg + c * 8) = qv;
+            if ((lane & 3) == 0) msg[a.off_sf + (c >> 2)] = static_cast<uint8_t>(ex + 127);
           }
         }
       }
@@ -238,10 +274,12 @@ static int sm_count() {
 }
 
 cudaError_t launch_ep_pack(const EpPackArgs& a, bool fp8, cudaStream_t st) {
-  if (a.S == 0) {
-    return cudaSuccess;
-  }
-  const int blocks = max(min(sm_count(), a.S), (a.S + kEpThreads - 1) / kEpThreads);
+  // S == 0 still launches: the empty rank's blocks must carry ids -1, and
+  // counts / overflow are written
+  // up to two blocks per SM (both resident): at decode / small-batch sizes a
+  // block holds one or two tokens, whose row segments then fit one round of
+  // its 8 warps
+  const int blocks = max(1, max(min(2 * sm_count(), a.S), (a.S + kEpThreads - 1) / kEpThreads));
   if (fp8)
     ep_pack_kernel<true><<<blocks, kEpThreads, 0, st>>>(a);
   else
@@ -253,7 +291,9 @@ cudaError_t launch_ep_combine(const void* back, const int32_t* pos, int32_t S, i
                               void* out, cudaStream_t st) {
   if (S == 0) return cudaSuccess;
   const int64_t n = static_cast<int64_t>(S) * (H / 8);
-  const int64_t want = (n + kEpThreads - 1) / kEpThreads, cap_blocks = 4 * sm_count();
+  // one 16-byte chunk per thread: every thread's pos -> row loads are its
+  // only dependent pair (a grid-stride loop would chain two of them)
+  const int64_t want = (n + kEpThreads - 1) / kEpThreads, cap_blocks = 64 * sm_count();
   const int blocks = static_cast<int>(want < cap_blocks ? want : cap_blocks);
   ep_combine_kernel<<<blocks, kEpThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(back), pos, S, H, P, cap,
                                                    static_cast<__nv_bfloat16*>(out));

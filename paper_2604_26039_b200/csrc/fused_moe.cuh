@@ -126,6 +126,9 @@ struct MoeParams {
   uint8_t* act_sf;             // [M-tiles][I/128][512]
   const uint8_t* xq_in;        // optional: tokens already MXFP8, [S, H] e4m3 (then x is unused)
   const uint8_t* xsf_in;       //           and their scales [S, H/32] UE8M0, row-major
+  int64_t x_row16;             // 16-byte chunks between token rows of x / xq_in (H/8 / H/16 when dense)
+  int64_t sf_row4;             // 4-byte words between token rows of xsf_in (H/128 when dense)
+  int64_t w_stride;            // floats between token rows of topk_w (0: dense [S*top_k])
   ramp_table_t table;
   int32_t S, H, I, E, top_k, n_assign;
   unsigned long long* prof;    // optional per-CTA cycle counters [gridDim][16] (diagnostics)
@@ -465,7 +468,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     // * small batches: quantise every gathered row here (no extra launch).
     if (p.xq_in != nullptr) {
       constexpr int kUnroll = 16;  // pure copy: 256 B in flight per lane
-      const int row16 = p.H / 16, row_sf = p.H / 32;
+      const int row16 = p.H / 16;
       const int gw = blockIdx.x * kGatherWarps + (warp - 2), nw = gridDim.x * kGatherWarps;
       const int4* qsrc = reinterpret_cast<const int4*>(p.xq_in);
       for (int r0 = gw; r0 < n_post_pad; r0 += 32 * nw) {
@@ -485,7 +488,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
             const int src = __shfl_sync(0xffffffffu, src_l, q);
             dst_row[u] = c < nch && src >= 0 ? r0 + q * nw : -1;  // padding rows: never read back
             v[u] = make_int4(0, 0, 0, 0);
-            if (c < nch && src >= 0) v[u] = __ldg(qsrc + static_cast<int64_t>(src) * row16 + cc[u]);
+            if (c < nch && src >= 0) v[u] = __ldg(qsrc + src * p.x_row16 + cc[u]);
           }
   #pragma unroll
           for (int u = 0; u < kUnroll; ++u)
@@ -499,7 +502,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           const int src = __shfl_sync(0xffffffffu, src_l, q);
           if (c0 < nsw) {
             const uint32_t sc =
-                src < 0 ? 0u : __ldg(reinterpret_cast<const uint32_t*>(p.xsf_in + static_cast<int64_t>(src) * row_sf) + kb);
+                src < 0 ? 0u : __ldg(reinterpret_cast<const uint32_t*>(p.xsf_in) + src * p.sf_row4 + kb);
             const int r = r0 + q * nw, m = r / G.bm, jr = r - m * G.bm;
             *reinterpret_cast<uint32_t*>(p.x_sf + (static_cast<int64_t>(m) * G.kbH + kb) * 512 + (jr & 31) * 16 +
                                          (jr >> 5) * 4) = sc;
@@ -522,7 +525,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           if (asg >= p.n_assign) continue;  // warp-uniform
           const int r = r0 + q * nw;
           const int m = r / G.bm, jr = r - m * G.bm;
-          const int4* src = xv + static_cast<int64_t>(asg / p.top_k) * row_vec;
+          const int4* src = xv + (asg / p.top_k) * p.x_row16;
           uint8_t* dst = p.x_q + static_cast<int64_t>(r) * p.H;
           uint8_t* sf_row = p.x_sf + static_cast<int64_t>(m) * G.kbH * 512 + (jr & 31) * 16 + (jr >> 5) * 4;
           for (int c0 = lane; c0 < row_vec; c0 += 32 * kUnroll) {
@@ -593,8 +596,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         const int a0 = __shfl_sync(0xffffffffu, asg_l, q);
         const int a1 = __shfl_sync(0xffffffffu, asg_l, (q + 1) & 31);
         const bool two = q + 1 < nrows;
-        const int4* s0 = xv + static_cast<int64_t>(a0 < p.n_assign ? a0 / p.top_k : 0) * row_vec;
-        const int4* s1 = xv + static_cast<int64_t>(a1 < p.n_assign ? a1 / p.top_k : 0) * row_vec;
+        const int4* s0 = xv + (a0 < p.n_assign ? a0 / p.top_k : 0) * p.x_row16;
+        const int4* s1 = xv + (a1 < p.n_assign ? a1 / p.top_k : 0) * p.x_row16;
         int4* d0 = dv + static_cast<int64_t>(r0 + q * nw) * row_vec;
         int4* d1 = dv + static_cast<int64_t>(r0 + (q + 1) * nw) * row_vec;
         for (int c0 = lane; c0 < row_vec; c0 += 32 * kUnroll) {
@@ -1096,8 +1099,9 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         for (int q = et2; q < G.bm; q += kEpiThreads) {
           const int a = p.sorted_ids[row0 + q];
           const bool valid = a < p.n_assign;
-          cs.epi_tok[q] = valid ? a / p.top_k : -1;
-          cs.epi_w[q] = valid ? __ldg(p.topk_w + a) : 0.0f;
+          const int t = a / p.top_k;
+          cs.epi_tok[q] = valid ? t : -1;
+          cs.epi_w[q] = valid ? __ldg(p.topk_w + (p.w_stride ? t * p.w_stride + (a - t * p.top_k) : a)) : 0.0f;
         }
         named_bar_sync(1, kEpiThreads);
       }

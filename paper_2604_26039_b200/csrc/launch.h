@@ -16,6 +16,7 @@ constexpr int kSfCol = 448;
 
 struct RouteArgs {
   const int32_t* topk_ids;
+  int64_t ids_stride;    // int32s between consecutive tokens' ids; 0 = dense [S, top_k]
   int64_t n_assign;
   int32_t E;
   int32_t forced_cfg;
@@ -75,6 +76,10 @@ struct MoeLaunch {
   uint8_t* act_sf;  // [M-tiles][I/128][512]
   const uint8_t* xq_in;   // optional pre-quantised tokens [S, H] e4m3 (FP8 path)
   const uint8_t* xsf_in;  // and their row-major scales [S, H/32]
+  // token-row strides (0 = dense): bytes between rows of x / xq_in and of
+  // xsf_in, floats between rows of topk_w (e.g. the rows of an expert-parallel
+  // message: ramp_ep_row_layout)
+  int64_t x_stride, sf_stride, w_stride;
   int64_t rows;     // capacity of x_sorted / act_g
   ramp_table_t table;
   int32_t S, H, I, E, top_k;
@@ -92,14 +97,16 @@ struct EpPackArgs {
   const float* w;       // [S, k]
   const void* x;        // [S, H] bf16
   int32_t S, H, k, E, world, cap;
-  void* send_x;         // [world][cap][H] bf16, or e4m3 bytes (MXFP8 wire)
-  uint8_t* send_sf;     // [world][cap][H/32] UE8M0 (MXFP8 wire)
-  int32_t* send_ids;    // [world][cap][k] rank-local ids, -1 = another rank's slot / padding row
-  float* send_w;        // [world][cap][k]
+  uint8_t* send;        // [world][cap][row_bytes] messages (ep_row_layout): the token (bf16, or e4m3
+                        // + UE8M0 scales at off_sf), its k rank-local ids at off_ids (-1 = another
+                        // rank's slot / padding row) and weights at off_w
+  int32_t off_sf, off_ids, off_w, row_bytes;
   int32_t* pos;         // [S][world] send row of (token, rank), -1 = not sent
   int32_t* counts;      // [world] rows sent to each rank
   int32_t* overflow;    // set to 1 when a rank needs more than cap rows (those pairs are dropped)
 };
+// {off_sf (-1: bf16 wire), off_ids, off_w, row_bytes} of one wire row
+void ep_row_layout(int32_t H, int32_t k, bool fp8_wire, int32_t out4[4]);
 cudaError_t launch_ep_pack(const EpPackArgs& a, bool fp8_wire, cudaStream_t stream);
 cudaError_t launch_ep_combine(const void* back, const int32_t* pos, int32_t S, int32_t H, int32_t world,
                               int32_t cap, void* out, cudaStream_t stream);

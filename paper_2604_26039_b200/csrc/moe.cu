@@ -168,7 +168,12 @@ static bool build_maps(const MoeLaunch& l, MoeMaps& maps) {
       ok = ok && ((l.I % (64 << i)) != 0 || make_map(&maps.w1[i], l.w1, 3, dims, strides, box));
     }
     ok = ok && make_map_2d(&maps.w2, l.w2, (uint64_t)l.E * l.H, l.I, 128);
-    ok = ok && make_map_2d(&maps.x, l.x, (uint64_t)l.S, l.H, 1);
+    {  // token rows straight from x (TMA gather4, decode-size blocks), row-strided
+      const uint64_t dims[2] = {(uint64_t)l.H, (uint64_t)l.S};
+      const uint64_t strides[1] = {l.x_stride ? (uint64_t)l.x_stride : (uint64_t)l.H * 2};
+      const uint32_t box[2] = {64, 1};
+      ok = ok && make_map(&maps.x, l.x, 2, dims, strides, box);
+    }
   } else {
     for (int i = 0; i < 4; ++i) {
       ok = ok && make_map_2d(&maps.xq[i], l.x_q, l.rows, l.H, 16u << i, true);
@@ -204,11 +209,12 @@ cudaError_t launch_fused_moe(const MoeLaunch& l, cudaStream_t stream, const char
   // (workspace, weights, shape) and reuse (the encoder costs ~1 us per map).
   struct MapKey {
     const void *xs, *act, *w1, *w2, *x;
-    int64_t rows;
+    int64_t rows, x_stride;
     int32_t S, H, I, E;
     bool fp8;
     bool operator==(const MapKey& o) const {
-      return xs == o.xs && act == o.act && w1 == o.w1 && w2 == o.w2 && x == o.x && rows == o.rows && S == o.S &&
+      return xs == o.xs && act == o.act && w1 == o.w1 && w2 == o.w2 && x == o.x && rows == o.rows &&
+             x_stride == o.x_stride && S == o.S &&
              H == o.H && I == o.I && E == o.E && fp8 == o.fp8;
     }
   };
@@ -220,8 +226,8 @@ cudaError_t launch_fused_moe(const MoeLaunch& l, cudaStream_t stream, const char
   static MapEntry cache[16];
   static int cache_next = 0;
   static std::mutex cache_mu;
-  const MapKey key{l.fp8 ? l.x_q : l.x_sorted, l.fp8 ? l.act_q : l.act_g, l.w1, l.w2, l.x, l.rows, l.S, l.H, l.I,
-                   l.E, l.fp8};
+  const MapKey key{l.fp8 ? l.x_q : l.x_sorted, l.fp8 ? l.act_q : l.act_g, l.w1, l.w2, l.x, l.rows, l.x_stride,
+                   l.S, l.H, l.I, l.E, l.fp8};
   alignas(64) MoeMaps maps;  // copied into the launch's parameter buffer
   bool hit = false;
   {
@@ -268,6 +274,11 @@ cudaError_t launch_fused_moe(const MoeLaunch& l, cudaStream_t stream, const char
   p.act_sf = l.act_sf;
   p.xq_in = l.xq_in;
   p.xsf_in = l.xsf_in;
+  // token-row strides: of xq_in when the tokens come pre-quantised, else of x
+  const int64_t x_dense = l.xq_in ? l.H : 2 * (int64_t)l.H;
+  p.x_row16 = (l.x_stride ? l.x_stride : x_dense) / 16;
+  p.sf_row4 = (l.sf_stride ? l.sf_stride : l.H / 32) / 4;
+  p.w_stride = l.w_stride;
   p.table = l.table;
   p.S = l.S;
   p.H = l.H;

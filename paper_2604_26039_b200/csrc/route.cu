@@ -54,7 +54,7 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
                const_cast<int32_t*>(a.topk_ids), a.w_out);
   }
   __syncthreads();
-  block_count(a.topk_ids, a.n_assign, a.E, s, &st.bad, kGating);
+  block_count(a.topk_ids, a.n_assign, a.E, s, &st.bad, kGating, a.top_k, a.ids_stride);
   stamp(1);
   int sel = a.forced_cfg;
   int n_eval = 0;
@@ -142,7 +142,7 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
     block_place(a.n_assign, a.E, bm, s, st.warp_tot, a.sorted_ids, a.tile_expert, n_post_pad, a.prof, publish);
   } else {
     block_align(a.topk_ids, a.n_assign, a.E, bm, s, st.warp_tot, a.sorted_ids, a.tile_expert, n_post_pad,
-                a.prof, publish);
+                a.prof, publish, a.top_k, a.ids_stride);
   }
   stamp(3);
   const int npp = s.off[a.E];

@@ -265,22 +265,38 @@ __device__ inline void block_topk(const void* __restrict__ logits, bool bf16, in
 // Ids outside [0, E) set *bad (ExpertHistogram rejects them, ramp/routing.py:45-50),
 // except -1: a slot whose expert lives on another rank (vLLM's expert-parallel
 // convention) -- skipped, it is neither counted nor aligned.
+// Assignment i of a row-strided id source (ids_stride > 0: token t's top_k ids
+// start at ids + t * ids_stride, e.g. the rows of an expert-parallel message;
+// 0: dense [S, top_k]).
+__device__ __forceinline__ int32_t ld_id(const int32_t* __restrict__ ids, int64_t i, int k, int64_t stride) {
+  return stride == 0 ? __ldg(ids + i) : __ldg(ids + (i / k) * stride + i % k);
+}
+
 __device__ inline void block_count(const int32_t* __restrict__ ids, int64_t n, int E, RouteSmem& s,
-                                   int* bad, bool ids_in_smem = false) {
+                                   int* bad, bool ids_in_smem = false, int ids_k = 1, int64_t ids_stride = 0) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (s.cached && !ids_in_smem) {
     // asynchronous 16-byte copies: every thread's loads are in flight at
     // once (the synchronous loop exposed one L2 round trip per 1024 ids)
-    const bool vec = (n & 3) == 0 && (reinterpret_cast<uintptr_t>(ids) & 15) == 0 &&
-                     (reinterpret_cast<uintptr_t>(s.ids) & 15) == 0;
-    if (vec) {
+    const bool al = (reinterpret_cast<uintptr_t>(ids) & 15) == 0 && (reinterpret_cast<uintptr_t>(s.ids) & 15) == 0;
+    if (ids_stride == 0 && al && (n & 3) == 0) {
       for (int64_t q = tid; q < n / 4; q += blockDim.x)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(
                          __cvta_generic_to_shared(s.ids + 4 * q))),
                      "l"(ids + 4 * q)
                      : "memory");
+    } else if (ids_stride != 0 && al && (ids_k & 3) == 0 && (ids_stride & 3) == 0) {
+      // row-strided: each token's k ids are k/4 aligned 16-byte chunks
+      const int per = ids_k >> 2;
+      for (int64_t q = tid; q < n / 4; q += blockDim.x) {
+        const int64_t t = q / per, c = q - t * per;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(
+                         __cvta_generic_to_shared(s.ids + 4 * q))),
+                     "l"(ids + t * ids_stride + 4 * c)
+                     : "memory");
+      }
     } else {
-      for (int64_t i = tid; i < n; i += blockDim.x) s.ids[i] = __ldg(ids + i);
+      for (int64_t i = tid; i < n; i += blockDim.x) s.ids[i] = ld_id(ids, i, ids_k, ids_stride);
     }
   }
   for (int x = tid; x < 32 * E; x += blockDim.x) s.cnt[x] = 0;
@@ -294,7 +310,7 @@ __device__ inline void block_count(const int32_t* __restrict__ ids, int64_t n, i
     const int64_t i = c0 + lane;
     int e = -1;
     if (i < hi) {
-      e = s.cached ? s.ids[i] : __ldg(ids + i);
+      e = s.cached ? s.ids[i] : ld_id(ids, i, ids_k, ids_stride);
       if (e != -1 && (e < 0 || e >= E)) {
         *bad = 1;
         e = -1;
@@ -697,7 +713,8 @@ template <class Publish = NoPublish>
 __device__ inline void block_align(const int32_t* __restrict__ ids, int64_t n, int E, int bm,
                                    RouteSmem& s, int* warp_tot, int32_t* __restrict__ sorted_ids,
                                    int32_t* __restrict__ tile_expert, int32_t* n_post_pad_out,
-                                   unsigned long long* stamps = nullptr, Publish on_offsets = Publish{}) {
+                                   unsigned long long* stamps = nullptr, Publish on_offsets = Publish{},
+                                   int ids_k = 1, int64_t ids_stride = 0) {
   auto stamp = [&](int slot) {
     if (stamps && threadIdx.x == 0) {
       unsigned long long t;
@@ -729,7 +746,7 @@ __device__ inline void block_align(const int32_t* __restrict__ ids, int64_t n, i
     const int64_t i = c0 + lane;
     int e = -1;
     if (i < hi) {
-      e = s.cached ? s.ids[i] : __ldg(ids + i);
+      e = s.cached ? s.ids[i] : ld_id(ids, i, ids_k, ids_stride);
       if (e < 0 || e >= E) e = -1;
     }
     const unsigned peers = match_peers(e, nbits);

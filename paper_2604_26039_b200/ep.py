@@ -20,10 +20,14 @@ count carry ids -1) -- so no split size is ever read on the host: the whole
 layer is asynchronous and CUDA-graph capturable.  The pack (step 1's
 row/slot construction, bf16 or MXFP8 rows) and the reduce (step 3's sum)
 are device kernels of libramp_b200 (`ramp_ep_pack` / `ramp_ep_reduce`,
-csrc/ep.cu).  The exchanges run either through this library's own NCCL
-communicator (`EPComm`: `ramp_ep_dispatch` / `ramp_ep_combine`, one grouped
-NCCL send/recv per direction, the C ABI a reference-side integration binds)
-or through `torch.distributed.all_to_all_single` on the packed buffers (any
+csrc/ep.cu).  A wire row is one self-contained message -- the token, its
+scales, its k local ids and weights at fixed offsets (`row_layout`) -- so a
+dispatch is ONE send / receive per peer, and the receiving megakernel reads
+the fields in place (row-strided inputs, `ramp_fused_moe_strided`).  The
+exchanges run either through this library's own NCCL communicator
+(`EPComm`: `ramp_ep_dispatch` / `ramp_ep_combine`, one grouped NCCL
+send/recv per direction, the C ABI a reference-side integration binds) or
+through `torch.distributed.all_to_all_single` on the packed rows (any
 backend; what the gloo CPU tests drive, with the oracle's restatement of the
 two kernels injected as `kernels=`).
 
@@ -65,8 +69,38 @@ def expert_owner(ids: torch.Tensor, E: int, world: int) -> torch.Tensor:
     return torch.div(ids, per, rounding_mode="floor")
 
 
-def _row_bytes(H: int, wire: str) -> int:
-    return H + H // 32 if wire == "fp8" else 2 * H
+@dataclass(frozen=True)
+class RowLayout:
+    """Byte offsets of one wire row (csrc/ep.cu ep_row_layout,
+    ramp_ep_row_layout): token at 0 (H bf16, or H e4m3 then H/32 UE8M0 at
+    off_sf), k int32 local ids at off_ids, k fp32 weights at off_w."""
+
+    off_sf: int
+    off_ids: int
+    off_w: int
+    row_bytes: int
+
+
+def row_layout(H: int, k: int, wire: str) -> RowLayout:
+    fp8 = wire == "fp8"
+    tok = H + H // 32 if fp8 else 2 * H
+    off_ids = (tok + 15) // 16 * 16
+    off_w = off_ids + 4 * k
+    return RowLayout(H if fp8 else -1, off_ids, off_w, (off_w + 4 * k + 15) // 16 * 16)
+
+
+def row_fields(rows: torch.Tensor, H: int, k: int, wire: str):
+    """(x, ids, w) views of a [n, row_bytes] uint8 row buffer: x is [n, H]
+    bf16, or the pair (e4m3 bytes [n, H], UE8M0 [n, H/32]); ids [n, k] int32;
+    w [n, k] fp32 -- row-strided views, no copy."""
+    L = row_layout(H, k, wire)
+    ids = rows[:, L.off_ids:L.off_ids + 4 * k].view(torch.int32)
+    w = rows[:, L.off_w:L.off_w + 4 * k].view(torch.float32)
+    if wire == "fp8":
+        x = (rows[:, :H], rows[:, L.off_sf:L.off_sf + H // 32])
+    else:
+        x = rows[:, :2 * H].view(torch.bfloat16)
+    return x, ids, w
 
 
 class DeviceKernels:
@@ -82,19 +116,14 @@ class DeviceKernels:
                             ("topk_w", topk_w, torch.float32)):
             if t.dtype != dt or not t.is_cuda or not t.is_contiguous():
                 raise ValueError(f"{name} must be a contiguous {dt} CUDA tensor (there is no CPU path)")
-        fp8 = wire == "fp8"
-        send_x = torch.empty(world * cap, H, dtype=torch.uint8 if fp8 else torch.bfloat16, device=dev)
-        send_sf = torch.empty(world * cap, H // 32, dtype=torch.uint8, device=dev) if fp8 else None
-        send_ids = torch.empty(world * cap, k, dtype=torch.int32, device=dev)
-        send_w = torch.empty(world * cap, k, dtype=torch.float32, device=dev)
+        send = torch.empty(world * cap, row_layout(H, k, wire).row_bytes, dtype=torch.uint8, device=dev)
         pos = torch.empty(S, world, dtype=torch.int32, device=dev)
         counts = torch.empty(world, dtype=torch.int32, device=dev)
-        overflow = torch.zeros(1, dtype=torch.int32, device=dev)
+        overflow = torch.empty(1, dtype=torch.int32, device=dev)  # written by the pack kernel
         _lib.check(lib.ramp_ep_pack(x.data_ptr(), topk_ids.data_ptr(), topk_w.data_ptr(), S, H, E, k, world, cap,
-                                    WIRES[wire], send_x.data_ptr(), send_sf.data_ptr() if fp8 else None,
-                                    send_ids.data_ptr(), send_w.data_ptr(), pos.data_ptr(), counts.data_ptr(),
+                                    WIRES[wire], send.data_ptr(), pos.data_ptr(), counts.data_ptr(),
                                     overflow.data_ptr(), _stream()))
-        return send_x, send_sf, send_ids, send_w, pos, counts, overflow
+        return send, pos, counts, overflow
 
     def reduce(self, back, pos, world: int, cap: int):
         lib = _lib.load()
@@ -149,8 +178,10 @@ def dispatch(x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor, E: i
 
     Returns (plan, recv_x, recv_ids [P*cap, k] rank-local expert ids, recv_w
     [P*cap, k]); recv_x is [P*cap, H] bf16, or the pair (e4m3 bytes
-    [P*cap, H], UE8M0 scales [P*cap, H/32]) with wire="fp8".  Block s of the
-    received rows came from rank s; rows past its count have ids -1.
+    [P*cap, H], UE8M0 scales [P*cap, H/32]) with wire="fp8" -- all four are
+    row-strided views of the one received row buffer (`row_fields`), which
+    the megakernel reads in place.  Block s of the received rows came from
+    rank s; rows past its count have ids -1.
 
     exchange="auto" takes the identity shortcut at world 1 (every expert is
     local: the layer runs on the inputs, no pack, no collective);
@@ -170,42 +201,31 @@ def dispatch(x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor, E: i
     cap = S if cap is None else int(cap)
     if cap < 0:
         raise ValueError("cap must be >= 0")
-    fp8 = wire == "fp8"
     dev = x.device
-    recv_x = torch.empty(world * cap, H, dtype=torch.uint8 if fp8 else x.dtype, device=dev)
-    recv_sf = torch.empty(world * cap, H // 32, dtype=torch.uint8, device=dev) if fp8 else None
-    recv_ids = torch.empty(world * cap, k, dtype=torch.int32, device=dev)
-    recv_w = torch.empty(world * cap, k, dtype=torch.float32, device=dev)
+    L = row_layout(H, k, wire)
+    recv = torch.empty(world * cap, L.row_bytes, dtype=torch.uint8, device=dev)
     if comm is not None:
         lib = _lib.load()
-        send_x = torch.empty_like(recv_x)
-        send_sf = torch.empty_like(recv_sf) if fp8 else None
-        send_ids, send_w = torch.empty_like(recv_ids), torch.empty_like(recv_w)
+        send = torch.empty_like(recv)
         pos = torch.empty(S, world, dtype=torch.int32, device=dev)
         counts = torch.empty(world, dtype=torch.int32, device=dev)
-        overflow = torch.zeros(1, dtype=torch.int32, device=dev)
+        overflow = torch.empty(1, dtype=torch.int32, device=dev)  # written by the pack kernel
         for name, t, dt in (("x", x, torch.bfloat16), ("topk_ids", topk_ids, torch.int32),
                             ("topk_w", topk_w, torch.float32)):
             if t.dtype != dt or not t.is_cuda or not t.is_contiguous():
                 raise ValueError(f"{name} must be a contiguous {dt} CUDA tensor (there is no CPU path)")
         _lib.check(lib.ramp_ep_dispatch(
             comm.handle, x.data_ptr(), topk_ids.data_ptr(), topk_w.data_ptr(), S, H, E, k, cap, WIRES[wire],
-            send_x.data_ptr(), send_sf.data_ptr() if fp8 else None, send_ids.data_ptr(), send_w.data_ptr(),
-            pos.data_ptr(), counts.data_ptr(), overflow.data_ptr(), recv_x.data_ptr(),
-            recv_sf.data_ptr() if fp8 else None, recv_ids.data_ptr(), recv_w.data_ptr(), _stream()))
+            send.data_ptr(), pos.data_ptr(), counts.data_ptr(), overflow.data_ptr(), recv.data_ptr(), _stream()))
     else:
         kernels = kernels or DeviceKernels()
-        send_x, send_sf, send_ids, send_w, pos, counts, overflow = kernels.pack(x, topk_ids, topk_w, E, world, cap,
-                                                                                wire)
+        send, pos, counts, overflow = kernels.pack(x, topk_ids, topk_w, E, world, cap, wire)
         # equal blocks of cap rows: no split sizes to exchange first
-        dist.all_to_all_single(recv_x, send_x, group=group)
-        if fp8:
-            dist.all_to_all_single(recv_sf, send_sf, group=group)
-        dist.all_to_all_single(recv_ids, send_ids, group=group)
-        dist.all_to_all_single(recv_w, send_w, group=group)
+        dist.all_to_all_single(recv, send, group=group)
     plan = EPPlan(world=world, cap=cap, wire=wire, pos=pos, counts=counts, overflow=overflow,
-                  wire_bytes=world * cap * (_row_bytes(H, wire) + 8 * k))
-    return plan, ((recv_x, recv_sf) if fp8 else recv_x), recv_ids, recv_w
+                  wire_bytes=world * cap * L.row_bytes)
+    rx, rids, rw = row_fields(recv, H, k, wire)
+    return plan, rx, rids, rw
 
 
 def combine(plan: EPPlan, partial: torch.Tensor, group=None, comm: EPComm | None = None, kernels=None) -> torch.Tensor:

@@ -207,6 +207,38 @@ class Workspace:
         return bool(int(w.item()) != 0)
 
 
+def _row_stride(name: str, t: torch.Tensor) -> int:
+    """0 for a contiguous tensor; the row stride (elements) of a row-strided
+    2-D view with a unit inner stride (e.g. one field of the expert-parallel
+    wire's rows, ep.dispatch); anything else is rejected."""
+    if t.is_contiguous():
+        return 0
+    if t.dim() == 2 and t.stride(1) == 1 and t.stride(0) >= t.shape[1]:
+        return int(t.stride(0))
+    raise ValueError(f"{name} must be contiguous or a row-strided [rows, n] view with unit inner stride")
+
+
+def _strided_call(lib, x, x_sf, w1, w1_sf, w2, w2_sf, topk_w, topk_ids, strides, S, H, I, E, k, table, forced_cfg,
+                  out, workspace, phases):
+    _lib.check(lib.ramp_fused_moe_strided(
+        x.data_ptr(), None if x_sf is None else x_sf.data_ptr(), w1.data_ptr(),
+        None if w1_sf is None else w1_sf.data_ptr(), w2.data_ptr(), None if w2_sf is None else w2_sf.data_ptr(),
+        topk_w.data_ptr(), topk_ids.data_ptr(), ctypes.byref(strides), S, H, I, E, k, table.ref,
+        table.table_index(int(forced_cfg)), out.data_ptr(), workspace.sel.data_ptr(), workspace.buf.data_ptr(),
+        workspace.buf.numel(), int(phases), _stream()))
+
+
+def _token_strides(hidden_states, x_sf, topk_weights, topk_ids):
+    """ramp_row_strides_t of the per-token inputs, or None when all are dense."""
+    xs = _row_stride("hidden_states", hidden_states) * hidden_states.element_size()
+    sfs = 0 if x_sf is None else _row_stride("x_sf", x_sf)
+    ws = _row_stride("topk_weights", topk_weights)
+    ids = _row_stride("topk_ids", topk_ids)
+    if not (xs or sfs or ws or ids):
+        return None
+    return _lib.RowStrides(xs, sfs, ids, ws)
+
+
 def _raise_if_invalid_ids(ws: Workspace, E: int) -> None:
     # the reference's ExpertHistogram rejects out-of-range experts with a
     # ValueError (ramp/routing.py:45-50); the device flags them and skips them
@@ -233,7 +265,8 @@ def fused_moe(
 
     hidden_states [S, H] bf16; w1 [E, 2I, H] bf16 (gate rows first, vLLM
     layout); w2 [E, H, I] bf16; topk_weights [S, k] fp32; topk_ids [S, k]
-    int32.  `forced_cfg < 0` lets the on-device dispatcher choose the tile
+    int32 (the per-token inputs may also be row-strided views, e.g. fields of
+    the expert-parallel wire's rows).  `forced_cfg < 0` lets the on-device dispatcher choose the tile
     config from the live histogram; a config id forces it (static dispatch or
     the exhaustive sweep).  The selection record {cfg, n_post_pad, n_mtiles,
     n_eval} is left in `workspace.sel` (device int32[4]).  `phases` = 1 / 2
@@ -256,14 +289,22 @@ def fused_moe(
             raise ValueError(f"{name} must be {dt}, got {t.dtype}")
         if not t.is_cuda:
             raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    for name, t in (("w1", w1), ("w2", w2)):
         if not t.is_contiguous():
             raise ValueError(f"{name} must be contiguous")
+    strides = _token_strides(hidden_states, None, topk_weights, topk_ids)
     if tuple(topk_weights.shape) != (S, k):
         raise ValueError("topk_weights must be [S, top_k]")
     if out is None:
         out = torch.empty(S, H, dtype=torch.bfloat16, device=hidden_states.device)
     if workspace is None or not workspace.fits(S, H, I, E, k):
         workspace = Workspace(S, H, I, E, k, device=hidden_states.device)
+    if strides is not None:
+        _strided_call(lib, hidden_states, None, w1, None, w2, None, topk_weights, topk_ids, strides, S, H, I, E, k,
+                      table, forced_cfg, out, workspace, phases)
+        if validate and phases & 1:
+            _raise_if_invalid_ids(workspace, E)
+        return out
     _lib.check(
         lib.ramp_fused_moe_bf16_ex(
             hidden_states.data_ptr(), w1.data_ptr(), w2.data_ptr(), topk_weights.data_ptr(),
@@ -384,8 +425,11 @@ def fused_moe_fp8(
             raise ValueError(f"{name} must be {dt}, got {t.dtype}")
         if not t.is_cuda:
             raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    for name, t in (("w1_q", weights.w1_q), ("w2_q", weights.w2_q), ("w1_sf", weights.w1_sf),
+                    ("w2_sf", weights.w2_sf)):
         if not t.is_contiguous():
             raise ValueError(f"{name} must be contiguous")
+    strides = _token_strides(hidden_states, x_sf, topk_weights, topk_ids)
     if tuple(weights.w1_sf.shape) != (E * 2 * I // 128, H // 128, 512) or \
             tuple(weights.w2_sf.shape) != (E * H // 128, I // 128, 512):
         raise ValueError("scale atoms must be tiled [rows/128, K/128, 512] (quant.tile_scales)")
@@ -401,7 +445,10 @@ def fused_moe_fp8(
             weights.w2_sf.data_ptr(), topk_weights.data_ptr(), topk_ids.data_ptr(), S, H, I, E, k, table.ref,
             table.table_index(int(forced_cfg)), out.data_ptr(), workspace.sel.data_ptr(), workspace.buf.data_ptr(),
             workspace.buf.numel(), int(phases), _stream())
-    if x_sf is None:
+    if strides is not None:
+        _strided_call(lib, hidden_states, x_sf, weights.w1_q, weights.w1_sf, weights.w2_q, weights.w2_sf,
+                      topk_weights, topk_ids, strides, S, H, I, E, k, table, forced_cfg, out, workspace, phases)
+    elif x_sf is None:
         _lib.check(lib.ramp_fused_moe_fp8(hidden_states.data_ptr(), *tail))
     else:
         _lib.check(lib.ramp_fused_moe_fp8_prequant(hidden_states.data_ptr(), x_sf.data_ptr(), *tail))

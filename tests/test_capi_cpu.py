@@ -88,18 +88,49 @@ def test_ep_argument_validation_without_gpu(lib):
     buf = (ctypes.c_int32 * 64)()
     p = ctypes.cast(buf, ctypes.c_void_p)
     # world must divide E
-    rc = lib.ramp_ep_pack(p, p, p, 4, 128, 10, 2, 4, 4, 0, p, p, p, p, p, p, p, None)
+    rc = lib.ramp_ep_pack(p, p, p, 4, 128, 10, 2, 4, 4, 0, p, p, p, p, None)
     assert rc == 1 and b"multiple of world" in lib.ramp_last_error()
-    rc = lib.ramp_ep_pack(p, p, p, 4, 100, 8, 2, 4, 4, 0, p, p, p, p, p, p, p, None)
+    rc = lib.ramp_ep_pack(p, p, p, 4, 100, 8, 2, 4, 4, 0, p, p, p, p, None)
     assert rc == 1 and b"H (d_model)" in lib.ramp_last_error()
-    rc = lib.ramp_ep_pack(p, p, p, 4, 128, 8, 2, 4, 4, 7, p, p, p, p, p, p, p, None)
+    rc = lib.ramp_ep_pack(p, p, p, 4, 128, 8, 2, 4, 4, 7, p, p, p, p, None)
     assert rc == 1 and b"wire" in lib.ramp_last_error()
-    rc = lib.ramp_ep_pack(p, p, p, 4, 128, 8, 2, 4, 4, 1, p, None, p, p, p, p, p, None)  # MXFP8 needs send_sf
+    rc = lib.ramp_ep_pack(p, p, p, 4, 128, 8, 2, 4, 4, 1, None, p, p, p, None)
     assert rc == 1 and b"null send buffer" in lib.ramp_last_error()
     rc = lib.ramp_ep_reduce(p, p, 4, 128, 0, 4, p, None)
     assert rc == 1
-    rc = lib.ramp_ep_dispatch(None, p, p, p, 4, 128, 8, 2, 4, 0, p, p, p, p, p, p, p, p, p, p, p, None)
+    rc = lib.ramp_ep_dispatch(None, p, p, p, 4, 128, 8, 2, 4, 0, p, p, p, p, p, None)
     assert rc == 1 and b"communicator" in lib.ramp_last_error()
     comm = ctypes.c_void_p()
     rc = lib.ramp_ep_comm_init(ctypes.byref(comm), p, 0, 0)
     assert rc == 1 and b"world" in lib.ramp_last_error()
+
+
+def test_ep_row_layout_matches_python_and_oracle(lib):
+    """ramp_ep_row_layout, ep.row_layout and the oracle's restatement agree."""
+    from oracle.ep_ref import row_layout_ref
+    from paper_2604_26039_b200.ep import row_layout
+
+    out = (ctypes.c_int32 * 4)()
+    for H in (128, 384, 2048, 7168):
+        for k in (1, 2, 3, 8):
+            for wire, code in (("bf16", 0), ("fp8", 1)):
+                assert lib.ramp_ep_row_layout(H, k, code, out) == 0
+                got = tuple(out)
+                assert got == row_layout_ref(H, k, wire) == tuple(vars(row_layout(H, k, wire)).values())
+                assert got[1] % 16 == 0 and got[3] % 16 == 0
+    assert lib.ramp_ep_row_layout(100, 2, 0, out) == 1
+
+
+def test_strided_entry_validation_without_gpu(lib):
+    """ramp_fused_moe_strided rejects malformed strides before any launch."""
+    buf = (ctypes.c_int32 * 64)()
+    p = ctypes.cast(buf, ctypes.c_void_p)
+    t = _lib.RampTable()
+    st = _lib.RowStrides(100, 0, 0, 0)  # not a multiple of 16
+    rc = lib.ramp_fused_moe_strided(p, None, p, None, p, None, p, p, ctypes.byref(st), 4, 128, 128, 8, 2,
+                                    ctypes.byref(t), -1, p, None, p, 1 << 20, 3, None)
+    assert rc == 1 and b"x_stride" in lib.ramp_last_error()
+    st = _lib.RowStrides(0, 0, 1, 0)  # ids_stride below top_k
+    rc = lib.ramp_fused_moe_strided(p, None, p, None, p, None, p, p, ctypes.byref(st), 4, 128, 128, 8, 2,
+                                    ctypes.byref(t), -1, p, None, p, 1 << 20, 3, None)
+    assert rc == 1 and b"ids_stride" in lib.ramp_last_error()

@@ -44,7 +44,7 @@ def _worker(rank, world, port, E, S, k, H, I, q, wire, mode, cap, empty_rank=-1)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle.ep_ref import RefKernels, mx_dequantize_bytes, mx_quantize_bytes
-        from oracle.moe_ref import fused_moe_ref
+        from oracle.moe_ref import bf16_round, fused_moe_ref
         from paper_2604_26039_b200.ep import ep_moe_layer
 
         rng = np.random.default_rng(123)  # same weights on every rank
@@ -61,13 +61,15 @@ def _worker(rank, world, port, E, S, k, H, I, q, wire, mode, cap, empty_rank=-1)
         lo = rank * per
 
         def local_fn(rx, rids, rw):
-            xr = mx_dequantize_bytes(rx[0].numpy(), rx[1].numpy()) if isinstance(rx, tuple) else rx.numpy()
+            xr = mx_dequantize_bytes(rx[0].numpy(), rx[1].numpy()) if isinstance(rx, tuple) else rx.float().numpy()
             return torch.from_numpy(fused_moe_ref(xr, w1[lo:lo + per], w2[lo:lo + per], rw.numpy(), rids.numpy()))
 
         out = ep_moe_layer(torch.from_numpy(x), torch.from_numpy(ids), torch.from_numpy(w), E, local_fn, wire=wire,
                            cap=cap, kernels=RefKernels(), exchange="always")
         if wire == "fp8":  # the wire carries MXFP8 token rows: the reference sees the same rounding
             x = mx_dequantize_bytes(*mx_quantize_bytes(x))
+        else:  # bf16 token rows
+            x = bf16_round(x)
         ref = fused_moe_ref(x, w1, w2, w, ids)
         assert tuple(out.shape) == (S, H)
         q.put((rank, float(np.abs(out.numpy() - ref).max(initial=0.0)), float(np.abs(ref).max(initial=0.0))))
@@ -155,18 +157,23 @@ def _identity_worker(port, q, wire):
 def test_pack_ref_contract():
     """The oracle pack itself: one row per unique (token, rank), token order,
     local ids, padding rows -1, overflow flagged when cap is too small."""
-    from oracle.ep_ref import ep_pack_ref, ep_reduce_ref
+    from oracle.ep_ref import ep_pack_ref, ep_reduce_ref, row_layout_ref
 
     x = np.random.default_rng(0).standard_normal((4, 128)).astype(np.float32)
     ids = np.array([[0, 5], [5, 6], [1, 1], [7, -1]], dtype=np.int32)
     w = np.array([[0.1, 0.2], [0.3, 0.4], [0.5, 0.6], [0.7, 0.8]], dtype=np.float32)
-    sx, _, sid, sw, pos, cnt, ovf = ep_pack_ref(x, ids, w, 8, 2, 4)
+    send, pos, cnt, ovf = ep_pack_ref(x, ids, w, 8, 2, 4)
+    _, off_ids, off_w, rb = row_layout_ref(128, 2, "bf16")
+    assert send.shape == (8, rb) and rb % 16 == 0 and off_ids == 256
+    sid = np.ascontiguousarray(send[:, off_ids:off_ids + 8]).view(np.int32)
+    sw = np.ascontiguousarray(send[:, off_w:off_w + 8]).view(np.float32)
+    sx = torch.from_numpy(np.ascontiguousarray(send[:, :256])).view(torch.bfloat16).float().numpy()
     assert cnt.tolist() == [2, 3] and ovf == 0
     assert pos.tolist() == [[0, 0], [-1, 1], [1, -1], [-1, 2]]
     assert sid[0].tolist() == [0, -1] and sid[4].tolist() == [-1, 1] and sid[5].tolist() == [1, 2]
     assert sid[6].tolist() == [3, -1] and sid[3].tolist() == [-1, -1] and sid[7].tolist() == [-1, -1]
     assert sw[5].tolist() == pytest.approx([0.3, 0.4]) and sw[4].tolist() == pytest.approx([0.0, 0.2])
-    np.testing.assert_array_equal(sx[5], x[1])
+    np.testing.assert_array_equal(sx[5], torch.from_numpy(x[1]).to(torch.bfloat16).float().numpy())
     back = np.arange(8 * 128, dtype=np.float32).reshape(8, 128)
     red = ep_reduce_ref(back, pos, 2, 4)
     np.testing.assert_array_equal(red[0], back[0] + back[4])

@@ -18,7 +18,8 @@ import pytest
 
 torch = pytest.importorskip("torch")
 
-from oracle.ep_ref import ep_pack_ref, ep_reduce_ref, mx_dequantize_bytes, mx_quantize_bytes  # noqa: E402
+from oracle.ep_ref import (ep_pack_ref, ep_reduce_ref, ep_rows_defined, mx_dequantize_bytes,  # noqa: E402
+                           mx_quantize_bytes)
 from oracle.moe_ref import bf16_round, fused_moe_ref, fused_moe_ref_fp8  # noqa: E402
 from tests._util import random_moe  # noqa: E402
 
@@ -51,7 +52,7 @@ def _ids(rng, S, E, k, mode):
 
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
 @pytest.mark.parametrize("wire", ["bf16", "fp8"])
-@pytest.mark.parametrize("S,mode,cap", [(37, "distinct", None), (300, "dup", None), (64, "skew", 20)])
+@pytest.mark.parametrize("S,mode,cap", [(37, "distinct", None), (300, "dup", None), (64, "skew", 20), (0, "dup", 8)])
 def test_pack_and_reduce_bit_exact(world, wire, S, mode, cap):
     from paper_2604_26039_b200.ep import DeviceKernels
 
@@ -65,19 +66,16 @@ def test_pack_and_reduce_bit_exact(world, wire, S, mode, cap):
     got = K.pack(torch.from_numpy(x).cuda().to(torch.bfloat16), torch.from_numpy(ids).cuda(),
                  torch.from_numpy(w).cuda(), E, world, cap, wire)
     torch.cuda.synchronize()
-    sx, ssf, sid, sw, pos, cnt, ovf = (None if t is None else t.cpu() for t in got)
-    rx, rsf, rid, rw, rpos, rcnt, rovf = ep_pack_ref(x, ids, w, E, world, cap, wire)
+    send, pos, cnt, ovf = (t.cpu() for t in got)
+    rsend, rpos, rcnt, rovf = ep_pack_ref(x, ids, w, E, world, cap, wire)
     np.testing.assert_array_equal(pos.numpy(), rpos)
     np.testing.assert_array_equal(cnt.numpy(), rcnt)
     assert int(ovf.item()) == rovf
-    np.testing.assert_array_equal(sid.numpy(), rid)
-    np.testing.assert_array_equal(sw.numpy(), rw)
-    valid = np.concatenate([d * cap + np.arange(rcnt[d]) for d in range(world)]).astype(np.int64)
-    if wire == "fp8":
-        np.testing.assert_array_equal(sx.numpy()[valid], rx[valid])
-        np.testing.assert_array_equal(ssf.numpy()[valid], rsf[valid])
-    else:
-        np.testing.assert_array_equal(sx.float().numpy()[valid], rx[valid])
+    assert tuple(send.shape) == rsend.shape
+    # every byte the kernel defines (ids / weights of every row, token and
+    # scales of the rows below each count), bit for bit
+    m = ep_rows_defined(rsend, rcnt, cap, H, k, wire)
+    np.testing.assert_array_equal(send.numpy()[m], rsend[m])
     # reduce: rank-order fp32 sum of bf16 rows, rounded once
     back = bf16_round(rng.standard_normal((world * cap, H)).astype(np.float32))
     out = K.reduce(torch.from_numpy(back).cuda().to(torch.bfloat16), pos.cuda(), world, cap)
@@ -117,7 +115,7 @@ def _bf16_table(E, H, I, k):
 def test_simulated_multi_rank_layer(world, wire):
     """P ranks on one GPU: pack on every rank, all-to-all as block slicing,
     the local megakernel per rank, the reverse exchange, the reduce."""
-    from paper_2604_26039_b200.ep import DeviceKernels, make_local_megakernel
+    from paper_2604_26039_b200.ep import DeviceKernels, make_local_megakernel, row_fields
     from paper_2604_26039_b200.quant import prepare_mxfp8_weights
 
     E, k, H, I, S = 32, 4, 512, 256, 48
@@ -136,21 +134,18 @@ def test_simulated_multi_rank_layer(world, wire):
     partial = []
     for r in range(world):
         blk = slice(r * cap, (r + 1) * cap)  # block r of every sender
-        rx = torch.cat([p[0][blk] for p in packs])
-        rsf = torch.cat([p[1][blk] for p in packs]) if wire == "fp8" else None
-        rids = torch.cat([p[2][blk] for p in packs])
-        rw = torch.cat([p[3][blk] for p in packs])
+        rows = torch.cat([p[0][blk] for p in packs])
+        rx, rids, rw = row_fields(rows, H, k, wire)  # row-strided views, read in place by the megakernel
         lw1 = torch.from_numpy(w1[r * per:(r + 1) * per]).cuda()
         lw2 = torch.from_numpy(w2[r * per:(r + 1) * per]).cuda()
         if wire == "fp8":
             fn = make_local_megakernel(prepare_mxfp8_weights(lw1, lw2), _fp8_table(per, H, I, k))
-            partial.append(fn((rx, rsf), rids, rw))
         else:
             fn = make_local_megakernel((lw1.to(torch.bfloat16), lw2.to(torch.bfloat16)), _bf16_table(per, H, I, k))
-            partial.append(fn(rx, rids, rw))
+        partial.append(fn(rx, rids, rw))
     for s, (x, w, ids) in enumerate(ranks):
         back = torch.cat([partial[r][s * cap:(s + 1) * cap] for r in range(world)])
-        out = K.reduce(back, packs[s][4], world, cap).float().cpu().numpy()
+        out = K.reduce(back, packs[s][1], world, cap).float().cpu().numpy()
         if wire == "fp8":
             wq = prepare_mxfp8_weights(torch.from_numpy(w1).cuda(), torch.from_numpy(w2).cuda())
             d1, d2 = (t.cpu().numpy() for t in wq.dequantize())
@@ -255,3 +250,62 @@ def test_nccl_exchange_world1(wire):
     for o in (ident, nccl):
         err = float(np.linalg.norm(o.float().cpu().numpy() - ref) / np.linalg.norm(ref))
         assert err < tol, err
+
+
+def _rows_of(x_fields, ids, w, H, k, wire):
+    """A [S, row_bytes] wire-row buffer holding these tokens / ids / weights."""
+    from paper_2604_26039_b200.ep import row_fields, row_layout
+
+    S = ids.shape[0]
+    rows = torch.full((S, row_layout(H, k, wire).row_bytes), 0x5A, dtype=torch.uint8, device="cuda")
+    rx, rids, rw = row_fields(rows, H, k, wire)
+    if wire == "fp8":
+        rx[0].copy_(x_fields[0])
+        rx[1].copy_(x_fields[1])
+    else:
+        rx.copy_(x_fields)
+    rids.copy_(ids)
+    rw.copy_(w)
+    return rows, (rx, rids, rw)
+
+
+@pytest.mark.parametrize("S,bm", [(6, 16), (300, 64), (2100, 128)])
+@pytest.mark.parametrize("dtype", ["bf16", "fp8", "fp8_prequant"])
+def test_row_strided_inputs_match_dense(S, bm, dtype):
+    """ramp_fused_moe_strided (tokens, scales, ids and weights read in place
+    from the wire's rows) equals the dense entry on the same operands -- the
+    decode gather4 path (bm 16), the phase-0 gather, and S*k > kIdCache
+    (the route kernel's uncached id reads)."""
+    import paper_2604_26039_b200.moe as M
+    from paper_2604_26039_b200.catalog import MoeGeometry
+    from paper_2604_26039_b200.config_space import enumerate_b200_configs
+    from paper_2604_26039_b200.quant import prepare_mxfp8_weights
+
+    E, k, H, I = 16, 8, 512, 256
+    x, w1, w2, w, ids = random_moe(S, H, I, E, k, seed=S + bm)
+    xt = torch.from_numpy(x).cuda().to(torch.bfloat16)
+    wt, it = torch.from_numpy(w).cuda(), torch.from_numpy(ids).cuda()
+    fp8 = dtype != "bf16"
+    pool = enumerate_b200_configs(MoeGeometry(name="rows", E=E, N=2 * I, K=H, top_k=k), dtype="fp8" if fp8 else "bf16")
+    cfg = next(c.id for c in pool if c.bm == bm and c.mode == 1 and c.split_k == 1)
+    if fp8:
+        tab = _fp8_table(E, H, I, k)
+        wq = prepare_mxfp8_weights(torch.from_numpy(w1).cuda(), torch.from_numpy(w2).cuda())
+        if dtype == "fp8_prequant":
+            q, sf = (torch.from_numpy(a).cuda() for a in mx_quantize_bytes(x))
+            dense = M.fused_moe_fp8((q, sf), wq, wt, it, tab, cfg)
+            _, (rx, rids, rw) = _rows_of((q, sf), it, wt, H, k, "fp8")
+            assert not rx[0].is_contiguous() and not rids.is_contiguous()
+            got = M.fused_moe_fp8(rx, wq, rw, rids, tab, cfg)
+        else:
+            dense = M.fused_moe_fp8(xt, wq, wt, it, tab, cfg)
+            _, (rx, rids, rw) = _rows_of(xt, it, wt, H, k, "bf16")
+            got = M.fused_moe_fp8(rx, wq, rw, rids, tab, cfg)
+    else:
+        tab = _bf16_table(E, H, I, k)
+        w1b, w2b = (torch.from_numpy(a).cuda().to(torch.bfloat16) for a in (w1, w2))
+        dense = M.fused_moe(xt, w1b, w2b, wt, it, tab, cfg)
+        _, (rx, rids, rw) = _rows_of(xt, it, wt, H, k, "bf16")
+        got = M.fused_moe(rx, w1b, w2b, rw, rids, tab, cfg)
+    torch.cuda.synchronize()
+    assert _rel(got, dense) < 1e-3  # same operands: only the fp32 output atomics' order may differ
