@@ -288,11 +288,11 @@ __device__ inline void block_count(const int32_t* __restrict__ ids, int64_t n, i
     } else if (ids_stride != 0 && al && (ids_k & 3) == 0 && (ids_stride & 3) == 0) {
       // row-strided: each token's k ids are k/4 aligned 16-byte chunks
       const int per = ids_k >> 2;
-      for (int64_t q = tid; q < n / 4; q += blockDim.x) {
-        const int64_t t = q / per, c = q - t * per;
+      for (int q = tid; q < static_cast<int>(n / 4); q += blockDim.x) {  // n <= kIdCache here
+        const int t = q / per, c = q - t * per;
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(
                          __cvta_generic_to_shared(s.ids + 4 * q))),
-                     "l"(ids + t * ids_stride + 4 * c)
+                     "l"(ids + static_cast<int64_t>(t) * ids_stride + 4 * c)
                      : "memory");
       }
     } else {

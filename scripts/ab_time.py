@@ -29,7 +29,8 @@ ap.add_argument("--dtype", default="bf16", choices=("bf16", "fp8"))
 a = ap.parse_args()
 geom = BASELINE_MODELS[a.model]
 fp8 = a.dtype == "fp8"
-pool = enumerate_b200_configs(geom, HardwareModel.b200(), dtype=a.dtype, phase3_chunks=not fp8, wide_tiles=not fp8)
+pool = enumerate_b200_configs(geom, HardwareModel.b200(), dtype=a.dtype, phase3_chunks=not fp8, wide_tiles=not fp8,
+                              fp8_wide_kps=fp8)
 cols = pool.columns()
 n = len(pool)
 flat = DeviceTable(bm=cols["bm"], ttn=cols["ttn"], stg=cols["stg"], split_k=cols["split_k"],
