@@ -583,10 +583,13 @@ def test_device_step_cache():
     assert sel_a[0] != sel_b[0]
     cache = M.DeviceStepCache(8)
     cached = table(cache)
+    torch.cuda.synchronize()
     out, s1 = _run_fused(x, w1, w2, w, ids_a, cached, -1)
     assert s1[0] == sel_a[0] and s1[3] > 0
     out_b, s2 = _run_fused(x, w1, w2, w, ids_b, cached, -1)
-    assert s2[0] == sel_a[0] and s2[3] == 0, "same step, same M: the cached selection, no evaluations"
+    assert s2[0] == sel_a[0] and s2[3] == 0, (
+        f"same step, same M: the cached selection, no evaluations (sel_a {sel_a.tolist()} sel_b {sel_b.tolist()} "
+        f"s1 {s1.tolist()} s2 {s2.tolist()} cache {cache.buf.cpu().tolist()})")
     assert _rel(out_b, fused_moe_ref(x, w1, w2, w, ids_b)) < RTOL_BF16
     assert cache.entries() == {S * k: int(sel_a[0])}
     cache.advance()

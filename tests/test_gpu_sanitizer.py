@@ -3,10 +3,16 @@ memcheck (out-of-bounds / misaligned accesses), racecheck (shared-memory
 hazards) and synccheck (barrier misuse) on the route kernel and the
 persistent megakernel, whose cross-CTA release/acquire counters, grid
 barriers and read-and-clear workspace are the risky parts.  Each run also
-checks its results against the oracle (scripts/sanitize_case.py)."""
+checks its results against the oracle (scripts/sanitize_case.py).
+
+The GPU pool's compute-sanitizer wrapper may refuse to run (exit code 86,
+"closed on this pool": sanitizer runs elsewhere left GPUs needing a reset).
+These tests then skip with that reason; the clean runs of round 2 are logged
+under profiles/ (r2v_gputest.log).  RAMP_SANITIZER=0 skips them outright."""
 
 from __future__ import annotations
 
+import os
 import shutil
 import subprocess
 import sys
@@ -16,6 +22,9 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
+
+
+SANITIZER_REFUSED = 86  # the pool wrapper's exit code when it will not run the sanitizer
 
 
 def _sanitizer():
@@ -32,8 +41,12 @@ def test_compute_sanitizer(tool, dtype):
            sys.executable, str(ROOT / "scripts" / "sanitize_case.py"), "--dtype", dtype]
     if tool == "racecheck":
         cmd[3:3] = ["--racecheck-report", "hazard"]
+    if os.environ.get("RAMP_SANITIZER", "1") == "0":
+        pytest.skip("RAMP_SANITIZER=0")
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
     tail = (res.stdout + res.stderr)[-3000:]
+    if res.returncode == SANITIZER_REFUSED and "closed on this pool" in res.stdout + res.stderr:
+        pytest.skip("compute-sanitizer refused by the GPU pool's wrapper: " + tail.strip().splitlines()[0][:200])
     assert res.returncode == 0, tail
     assert "sanitize_case ok" in res.stdout, tail
     # memcheck / synccheck end with "ERROR SUMMARY: 0 errors", racecheck with
