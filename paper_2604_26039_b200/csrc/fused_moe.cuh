@@ -691,7 +691,12 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
 #endif
       const int row0 = jb.m * G.bm;
       if (jb.kind == 0) {
-        const uint32_t tx1 = u_kps * (nA * kSubTileBytes + bmN * 128 + (kFp8 ? (nA + 1) * 512 : 0));
+        // direct_x gathers only the token block's bm rows (4 per gather4): the
+        // MMA's padding columns bm..15 read stale shared memory, and column n
+        // of the product depends on token row n alone, so every consumer
+        // (SwiGLU stores, split-K partials, scatter) stops at bm
+        const int n_g4 = direct_x ? warp_uniform(min(16, (G.bm + 3) & ~3)) : 16;
+        const uint32_t tx1 = u_kps * (nA * kSubTileBytes + (direct_x ? n_g4 : bmN) * 128 + (kFp8 ? (nA + 1) * 512 : 0));
         const int wrow = jb.s * G.n_i;
         const int kb0 = G.kb_lo(jb), kb1 = G.kb_hi(jb);
         int first_pending = 0, npend = 0;
@@ -712,7 +717,8 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
           for (int u = 0; u < u_kps; ++u) {
 #pragma unroll
             for (int q = 0; q < 16; q += 4)
-              tma_gather4(sb + u_tok + u * 16 * 128 + q * 128, &maps.x, full, (kb + u) * 64, trow[q], trow[q + 1],
+              if (q < n_g4)  // (constant trow indices: the array stays in registers)
+                tma_gather4(sb + u_tok + u * 16 * 128 + q * 128, &maps.x, full, (kb + u) * 64, trow[q], trow[q + 1],
                           trow[q + 2], trow[q + 3], pol_x);
           }
         };
