@@ -597,6 +597,30 @@ def compact_leg(leg, keys):
     return out
 
 
+# Descriptive strings that live in the per-point file only (the driver keeps
+# a bounded tail of stdout: the JSON line stays under ~4 KB).
+_FILE_ONLY_KEYS = ("note", "traffic_source", "method", "impl", "how", "exchange", "timing")
+
+
+def compact_line(line):
+    """The printed line: every nested float to 4 significant digits and the
+    long descriptions dropped (the full line is in the per-point file)."""
+
+    def walk(o, top=False):
+        if isinstance(o, float) and not top:
+            return float(f"{o:.4g}")
+        if isinstance(o, dict):
+            return {k: walk(v) for k, v in o.items() if not (k in _FILE_ONLY_KEYS and isinstance(v, str))}
+        if isinstance(o, list):
+            return [walk(v) for v in o]
+        return o
+
+    out = {k: walk(v, top=True) for k, v in line.items() if k != "per_point_us"}
+    if isinstance(line.get("e2e"), dict):
+        out["e2e"]["value"] = line["e2e"]["value"]
+    return out
+
+
 def write_per_point(per_point):
     """The per-point detail goes to a file (the JSON line stays short)."""
     d = ROOT / "gpurun_out" if (ROOT / "gpurun_out").is_dir() else ROOT
@@ -960,7 +984,9 @@ def ours(args, geom):
         "mixtral": compact_leg(mix, ("S", "beta", "us")),
         "ep": ep_res,
     }
-    print(json.dumps(line), flush=True)
+    if pp_path:  # the full line (with the descriptions) next to the per-point detail
+        write_per_point({"olmoe": per_point, "fp8": fp8, "mixtral": mix, "line_full": line})
+    print(json.dumps(compact_line(line)), flush=True)
     if dist.is_initialized():
         dist.destroy_process_group()
 

@@ -31,3 +31,24 @@ def test_roofline_summary_and_compact_leg(tmp_path, monkeypatch):
     assert c["points_S_beta_us"] == [[8, 0.5, 1.0]] and "points" not in c and len(c["workload"]) == 120
     assert bench.compact_leg({"error": "x"}, ("S",)) == {"error": "x"}
     json.dumps(roof)
+
+
+def test_compact_line_keeps_headline_and_drops_descriptions():
+    """The printed JSON line stays short: nested floats to 4 significant
+    digits, long descriptions only in the per-point file, headline exact."""
+    import json
+
+    import bench
+
+    line = {"metric": "m", "value": 164.97961361312, "ms_per_step": 1.868297576904,
+            "e2e": {"value": 151.99775185443, "unit": "TFLOP/s", "how": "x" * 300},
+            "roofline": {"frac": 0.61905110807983, "note": "y" * 300, "traffic_source": "z" * 200},
+            "dispatch": {"method": "w" * 300, "regret_mean_pct": 1.2391145478},
+            "per_point_us": [[1, 0.2, 28.7]] * 27}
+    out = bench.compact_line(line)
+    assert out["value"] == line["value"] and out["ms_per_step"] == line["ms_per_step"]
+    assert out["e2e"]["value"] == line["e2e"]["value"] and "how" not in out["e2e"]
+    assert out["roofline"] == {"frac": 0.6191}
+    assert out["dispatch"] == {"regret_mean_pct": 1.239}
+    assert "per_point_us" not in out
+    assert len(json.dumps(out)) < 300
