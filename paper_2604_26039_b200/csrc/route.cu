@@ -61,6 +61,7 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
   // Device StepCache (ramp/dispatch.py:40-54): a selection cached for this
   // step's M skips the dispatcher; a new step clears the entries.
   int cached = -1;
+  int step_m = 0;  // thread 0: this call's M (kept in a register: st.warp_tot is reused by the alignment scan)
   int32_t* const scache = a.table.step_cache;
   if (kDispatch && scache) {
     if (threadIdx.x < 32) {
@@ -80,7 +81,7 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
         for (int q = 0; q < nc; ++q)
           if (scache[3 + 2 * q] == m) hit = scache[4 + 2 * q];
         st.cnt[31] = hit;
-        st.warp_tot[31] = m;
+        step_m = m;
       }
     }
     __syncthreads();
@@ -107,7 +108,7 @@ __device__ __forceinline__ void route_body(const RouteArgs& a) {
     if (scache && threadIdx.x == 0) {
       const int nc = scache[2];
       if (nc < a.table.step_cache_cap) {
-        scache[3 + 2 * nc] = st.warp_tot[31];
+        scache[3 + 2 * nc] = step_m;
         scache[4 + 2 * nc] = sel;
         scache[2] = nc + 1;
       }
