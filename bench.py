@@ -874,17 +874,32 @@ def ours(args, geom):
               "wall_s": round(time.time() - t_ra, 1)}
 
     # ---------------- e2e through the public API with host buffers
-    pinned = []
+    # Each layer's request (tokens, top-k ids, top-k weights) sits in ONE
+    # pinned host block and moves with one copy into one device block, the
+    # three tensors being typed views of it (16-byte aligned: H % 8 == 0,
+    # 4-byte ids / weights in rows of top_k).
+    def _views(buf, x, ids, w):
+        nx, ni = x.numel() * x.element_size(), ids.numel() * ids.element_size()
+        nw = w.numel() * w.element_size()
+        return (buf[:nx].view(x.dtype).view(x.shape), buf[nx:nx + ni].view(ids.dtype).view(ids.shape),
+                buf[nx + ni:nx + ni + nw].view(w.dtype).view(w.shape))
+
+    pinned, host_blocks, dev_blocks, dev_bufs = [], [], [], []
     for (x, ids, w), pt in zip(inputs, pts):
-        pinned.append((x.cpu().pin_memory(), ids.cpu().pin_memory(), w.cpu().pin_memory(),
-                       torch.empty(pt["S"], H, dtype=torch.bfloat16).pin_memory()))
-    h2d = sum(a.numel() * a.element_size() + b.numel() * b.element_size() + c.numel() * c.element_size()
-              for a, b, c, _ in pinned)
+        nb = x.numel() * x.element_size() + ids.numel() * ids.element_size() + w.numel() * w.element_size()
+        hb = torch.empty(nb, dtype=torch.uint8).pin_memory()
+        for dst, src in zip(_views(hb, x, ids, w), (x, ids, w)):
+            dst.copy_(src.cpu())
+        db = torch.empty(nb, dtype=torch.uint8, device=dev)
+        host_blocks.append(hb)
+        dev_blocks.append(db)
+        dev_bufs.append(_views(db, x, ids, w))
+        pinned.append((*_views(hb, x, ids, w), torch.empty(pt["S"], H, dtype=torch.bfloat16).pin_memory()))
+    h2d = sum(b.numel() for b in host_blocks)
     d2h = sum(o.numel() * o.element_size() for *_, o in pinned)
-    dev_bufs = [(torch.empty_like(x), torch.empty_like(i), torch.empty_like(w)) for x, i, w in inputs]
 
     # The serving loop as a CUDA graph: every replay copies each layer's
-    # inputs from pinned host memory (copy-in stream, running ahead), runs the
+    # inputs (one block) from pinned host memory (copy-in stream, running ahead), runs the
     # layer once its inputs have landed, and copies its output back to the
     # host (copy-out stream) while the next layer computes.
     cin, cout = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
@@ -895,10 +910,8 @@ def ours(args, geom):
         cin.wait_stream(side)
         cout.wait_stream(side)
         with torch.cuda.stream(cin):
-            for p, ((hx, hi, hw_, _), (dx, di, dw)) in enumerate(zip(pinned, dev_bufs)):
-                dx.copy_(hx, non_blocking=True)
-                di.copy_(hi, non_blocking=True)
-                dw.copy_(hw_, non_blocking=True)
+            for p, (hb, db) in enumerate(zip(host_blocks, dev_blocks)):
+                db.copy_(hb, non_blocking=True)  # the layer's x, ids and weights in one transfer
                 ev_in[p].record(cin)
         for p, (dx, di, dw) in enumerate(dev_bufs):
             side.wait_event(ev_in[p])
@@ -936,6 +949,8 @@ def ours(args, geom):
     # the outputs really came back: spot-check the last layer's host copy
     if not torch.equal(pinned[-1][3], outs[-1].cpu()):
         raise SystemExit("e2e: host output differs from the device result")
+    if not all(torch.equal(a, b) for a, b in zip(dev_bufs[-1], inputs[-1])):
+        raise SystemExit("e2e: the copied-in request differs from the layer's inputs")
     e2e_val = step_flops / (e2e_ms / 1e3) / 1e12
 
     # ---------------- CPU baseline (oracle port, bounded sample)
