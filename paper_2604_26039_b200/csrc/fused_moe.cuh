@@ -386,6 +386,10 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   tc_fence_after();
   const uint32_t tmem = cs.tmem_base;
   pdl_wait();  // the route kernel's selection and alignment are now visible
+  // the producer's expert of M-tiles 0..31 (decode-size calls have no
+  // others), loaded alongside the selection instead of once per job after it
+  // (entries past n_mtiles are never read back)
+  const int te_pref = warp == 0 ? __ldcg(p.tile_expert + lane) : 0;
   const int cfg = p.ctrl[0];
   const int n_post_pad = p.ctrl[1];
   if (ts && threadIdx.x == 0) ts[kTsStart] = globaltimer();
@@ -682,7 +686,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
       if (j < 0) break;
       START_STAMP(lane == 0 && first_stamp, kTsClaimed);
       const Job jb = G.job(j);
-      const int e = warp_uniform(__ldcg(p.tile_expert + jb.m));
+      const int e = warp_uniform(jb.m < 32 ? __shfl_sync(0xffffffffu, te_pref, jb.m) : __ldcg(p.tile_expert + jb.m));
 #ifdef RAMP_START_STAMPS
       if (ts && lane == 0 && first_stamp) {
         asm volatile("" ::"r"(e));
