@@ -706,13 +706,13 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
         int first_pending = 0, npend = 0;
         int trow[16];  // direct_x: token row of each of the 16 MMA columns
         bool have_trow = false;
-        // direct_x: the M-tile's assignments are loaded now and first used
-        // after the first stage's weight loads are issued (the load's latency
-        // overlaps them instead of preceding them)
-        const int a_raw = direct_x && lane < G.bm ? __ldcg(p.sorted_ids + row0 + lane) : p.n_assign;
         auto ensure_trow = [&]() {  // whole warp; only once sorted_ids are final
           if (!direct_x || have_trow) return;
-          const int mine = a_raw < p.n_assign ? a_raw / p.top_k : 0;
+          int mine = 0;
+          if (lane < G.bm) {
+            const int a = __ldcg(p.sorted_ids + row0 + lane);
+            mine = a < p.n_assign ? a / p.top_k : 0;
+          }
 #pragma unroll
           for (int q = 0; q < 16; ++q) trow[q] = __shfl_sync(0xffffffffu, mine, q);
           have_trow = true;
@@ -726,6 +726,7 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
                           trow[q + 2], trow[q + 3], pol_x);
           }
         };
+        if (gathered) ensure_trow();
         // token-side loads of one stage (tiles + FP8 scale atom), deferrable
         auto load_tokens = [&](uint32_t sb, uint32_t full, int kb) {
           for (int q = 0; q < u_kps; ++q)
@@ -752,12 +753,10 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
                 bulk_g2s(sb + sf_off + t * u_kps * 512, p.w1_sf + (rb * G.kbH + kb) * 512, u_kps * 512, full);
               }
             }
-            if (gathered && !direct_x) load_tokens(sb, full, kb);
-          }
-          if (direct_x) {  // (gathered from the start: no phase-0 barrier)
-            __syncwarp();
-            ensure_trow();
-            if (elect_one()) gather_tokens(ring_addr + stage * u_sbytes, smem_u32(&cs.full[stage]), kb);
+            if (gathered) {
+              if (direct_x) gather_tokens(sb, full, kb);
+              else load_tokens(sb, full, kb);
+            }
           }
           __syncwarp();
           if (!gathered) {
